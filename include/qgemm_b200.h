@@ -1,0 +1,196 @@
+/* qgemm_b200.h — C ABI of the B200-native compressed modular GEMM.
+ *
+ * Drop-in boundary for the reference's C++ header API (namespace qgemm,
+ * /root/reference/proj/include/qgemm/). The reference has no FFI: its
+ * boundary is the header-level functions cited beside each entry point
+ * below. Here they are plain C: integer status, plain structs, caller-owned
+ * buffers, no exceptions, no torch types. Device entry points are
+ * stream-ordered (`stream` is a cudaStream_t; NULL = legacy default stream)
+ * and take DEVICE pointers; the qg_host_* entry points take HOST buffers and
+ * do their own host<->device copies (the reference-facing value-semantics
+ * calls). Every device computation runs in hand-written sm_100a kernels;
+ * there is no CPU fallback: without a usable CUDA device the calls return
+ * QG_CUDA_ERROR.
+ *
+ * Layouts are exactly CompressedMatrix::data (matrix.hpp:44-63):
+ *   CA  (compress_rows_reversed) m x ceil(k/e) row-major words
+ *   CB  (compress_cols_forward)  ceil(k/e) x n row-major words
+ *   CBo (compress_outer_cols)    k x ceil(n/e) row-major words
+ *   CC  (right product / repack) m x ceil(n/e) row-major words
+ * Residues on the device are stored as double (exact small integers) or as
+ * uint32 (ResidueMatrix, matrix.hpp:14-26); results C are int32 row-major.
+ */
+#ifndef QGEMM_B200_H
+#define QGEMM_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QG_ABI_VERSION 1
+
+/* Status codes: 0 = ok, then the exception classes of errors.hpp:8-34 in
+ * declaration order, then std::invalid_argument (plan.hpp:128-129,
+ * gemm.hpp:455), then device-side failures. */
+typedef enum {
+  QG_OK = 0,
+  QG_INVALID_MODULUS = 1,      /* errors.hpp:13 */
+  QG_NO_COMPRESSION = 2,       /* errors.hpp:16 */
+  QG_SLOT_OVERFLOW = 3,        /* errors.hpp:19 */
+  QG_DIGIT_OVERFLOW = 4,       /* errors.hpp:22 */
+  QG_DIMENSION_MISMATCH = 5,   /* errors.hpp:25 */
+  QG_PLAN_MISMATCH = 6,        /* errors.hpp:28 */
+  QG_UNSUPPORTED_ALGORITHM = 7,/* errors.hpp:31 */
+  QG_PARSE_ERROR = 8,          /* errors.hpp:34 */
+  QG_INVALID_ARGUMENT = 9,     /* std::invalid_argument */
+  QG_CUDA_ERROR = 10,
+  QG_NCCL_ERROR = 11,
+  QG_NOT_EXACT = 12            /* a k-block violates the FP64 exactness bound */
+} qg_status;
+
+/* ExtractionMode, plan.hpp:14-17 */
+enum { QG_EXTRACT_RECIPROCAL_MUL = 0, QG_EXTRACT_ADD_HIGH_BITS = 1 };
+
+/* CompressionPlan, plan.hpp:29-42. Identical field meaning. */
+typedef struct {
+  uint32_t p;       /* prime modulus */
+  int32_t t;        /* Q = 2^t */
+  int32_t d;        /* packing degree */
+  int32_t e;        /* residues per word, e = d + 1 */
+  int32_t beta;     /* exact bits of the word backend (53 for double) */
+  uint64_t kmax;    /* largest legal common dimension for this t */
+  double inv_qd;    /* 2^(-t d) */
+  int32_t extraction;
+} qg_plan;
+
+/* A plan plus the k-block size the FP64 tensor-core contraction flushes at
+ * (FFLAS-style blocking, gemm.hpp:450-489, done in registers). kblock_words
+ * packed words per block; each block is both legal for Eq. 3
+ * (kblock_words*e <= kmax) and exact for a DMMA FMA chain (Eq. G). */
+typedef struct {
+  qg_plan plan;
+  uint64_t kblock_words;
+  uint64_t max_exact_words; /* Eq. G bound for (p, t, e), informational */
+} qg_gpu_plan;
+
+/* PackOrientation, matrix.hpp:28-39: direction 0 Forward / 1 Reversed;
+ * axis 0 Row / 1 Column; slots residues per word along the packed axis. */
+typedef struct {
+  int32_t direction;
+  int32_t axis;
+  int32_t slots;
+} qg_orientation;
+
+/* Element type of residue buffers. */
+typedef enum { QG_F64 = 0, QG_U32 = 1, QG_I32 = 2 } qg_dtype;
+
+/* ---------------------------------------------------------------- host */
+int qg_abi_version(void);
+const char* qg_status_string(int status);
+
+/* plan_compression, plan.hpp:125-159 */
+int qg_plan_compression(uint32_t p, uint64_t k, int beta, int mode, qg_plan* out);
+/* uncompressed_plan, plan.hpp:164-179 */
+int qg_uncompressed_plan(uint32_t p, uint64_t k, int beta, qg_plan* out);
+/* plan_packed_axis, plan.hpp:186-203 */
+int qg_plan_packed_axis(uint32_t p, uint64_t k, uint64_t axis_len, int beta, qg_plan* out);
+/* choose_panel, plan.hpp:209-224 */
+int qg_choose_panel(uint32_t p, uint64_t k, int beta, uint64_t* out);
+/* largest block (packed words) for which a DMMA contraction of this plan is
+ * provably exact (Eq. G with rho = 1, unfused products). */
+int qg_max_exact_block(const qg_plan* plan, uint64_t* words);
+/* k-block an existing plan for the tensor-core path (reference plan kept). */
+int qg_gpu_plan_from(const qg_plan* plan, uint64_t k, qg_gpu_plan* out);
+/* choose (t, e, kblock) for common dimension k on the tensor-core path:
+ * minimises predicted contraction time over all exact blocked plans. */
+int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out);
+
+/* -------------------------------------------------- device (stream-ordered) */
+/* random_residue_matrix, prng.hpp:31-38 (SplitMix64 stream, counter-based):
+ * rows [row0, row0+rows) of the rows_total x cols matrix of seed. */
+int qg_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols,
+                    void* dst, qg_dtype dtype, void* stream);
+
+/* compress_rows_reversed, gemm.hpp:104-118 (+ compress_reverse, pack.hpp:59-70).
+ * A: m x k residues (lda elements), CA: m x ceil(k/e) (ldca words). */
+int qg_compress_rows_reversed(const qg_plan* plan, const void* a, qg_dtype dtype, size_t m,
+                              size_t k, size_t lda, double* ca, size_t ldca, void* stream);
+/* compress_cols_forward, gemm.hpp:122-140 (+ compress_forward, pack.hpp:47-54). */
+int qg_compress_cols_forward(const qg_plan* plan, const void* b, qg_dtype dtype, size_t k,
+                             size_t n, size_t ldb, double* cb, size_t ldcb, void* stream);
+/* compress_outer_cols, gemm.hpp:145-158: k x n residues -> k x ceil(n/e) words. */
+int qg_compress_outer_cols(const qg_plan* plan, const void* b, qg_dtype dtype, size_t rows,
+                           size_t cols, size_t ldb, double* cb, size_t ldcb, void* stream);
+/* compress_outer_rows, gemm.hpp:161-178: m x k residues -> ceil(m/e) x k words. */
+int qg_compress_outer_rows(const qg_plan* plan, const void* a, qg_dtype dtype, size_t rows,
+                           size_t cols, size_t lda, double* ca, size_t ldca, void* stream);
+
+/* packed_common_product, gemm.hpp:210-244, with the reference's own
+ * per-product high-part semantics (word.hpp:28-30): acc = sum_g
+ * trunc(CA*CB*2^-td), bit-identical doubles. m x n accumulators. */
+int qg_packed_common_product(const qg_plan* plan, const double* ca, const double* cb,
+                             size_t m, size_t n, size_t k, double* acc, void* stream);
+/* reduce_common_entry over a buffer, gemm.hpp:247-250. */
+int qg_reduce_common(const qg_plan* plan, const double* acc, size_t count, int32_t* c,
+                     void* stream);
+
+/* mul_common_compressed(ca, cb), gemm.hpp:263-271, + blocked_accumulate's
+ * mod-p accumulation between k-blocks (gemm.hpp:450-489), fused: one DMMA
+ * contraction kernel, in-register per-block digit extraction, mod-p epilogue.
+ * C: m x n int32 (ldc). k = logical common dimension (residues). */
+int qg_mul_common(const qg_gpu_plan* gplan, const double* ca, const double* cb, size_t m,
+                  size_t n, size_t k, int32_t* c, size_t ldc, void* stream);
+/* mul_common_repacked, gemm.hpp:275-280: C rows re-packed forward in groups
+ * of e (ReduceAndCompress, pack.hpp:141-155). cc: m x ceil(n/e) words.
+ * workspace: m*n int32 (device) or NULL to allocate internally. */
+int qg_mul_common_repacked(const qg_gpu_plan* gplan, const double* ca, const double* cb,
+                           size_t m, size_t n, size_t k, double* cc, int32_t* workspace,
+                           void* stream);
+
+/* packed_right_product + redq_in_place = mul_right_compressed(a, cb),
+ * gemm.hpp:285-325: CC = REDQ(A x CBo). A: m x k residues as double (lda),
+ * CBo: k x ceil(n/e) words. cc: m x ceil(n/e). */
+int qg_mul_right(const qg_plan* plan, const double* a, size_t lda, const double* cbo,
+                 size_t m, size_t k, size_t n, double* cc, void* stream);
+/* packed_right_product alone (pre-REDQ words), gemm.hpp:285-310. */
+int qg_packed_right_product(const qg_plan* plan, const double* a, size_t lda,
+                            const double* cbo, size_t m, size_t k, size_t n, double* cc,
+                            void* stream);
+
+/* redq_in_place, gemm.hpp:313-316 / redq, pack.hpp:124-137. Words that do
+ * not fit e digits make the call return QG_DIGIT_OVERFLOW (checked on the
+ * device, reported after a stream sync). */
+int qg_redq(const qg_plan* plan, double* words, size_t count, void* stream);
+/* uncompress, gemm.hpp:182-204 (+ extract_all, pack.hpp:104-119). */
+int qg_uncompress(const qg_plan* plan, qg_orientation o, const double* words,
+                  size_t stored_rows, size_t stored_cols, size_t logical_rows,
+                  size_t logical_cols, int32_t* out, void* stream);
+
+/* --------------------------------------------- host buffers (value semantics) */
+/* mul_common_compressed(A, B, plan), gemm.hpp:254-260, on HOST ResidueMatrix
+ * data (uint32 row-major). Uses the tensor-core path with the plan k-blocked
+ * for exactness. Copies in, computes on the current device, copies C out. */
+int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                       size_t k, size_t n, uint32_t* c);
+/* blocked_accumulate(A, B, plan, kpanel), gemm.hpp:450-489 on HOST data:
+ * panels of kpanel residues, each packed under `plan`, mod-p accumulation. */
+int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
+                               size_t m, size_t k, size_t n, size_t kpanel, uint32_t* c);
+/* mul_right_compressed(A, compress_outer_cols(B)), gemm.hpp:320-325, on HOST
+ * data: cc gets the post-REDQ words (m x ceil(n/e)). */
+int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                      size_t k, size_t n, double* cc);
+
+/* ------------------------------------------------------------ diagnostics */
+/* Number of kernels this library launched since load (the bench's
+ * gpu_launches evidence). */
+uint64_t qg_kernel_launches(void);
+/* Name of the contraction kernel variant the last qg_mul_common used. */
+const char* qg_last_kernel(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QGEMM_B200_H */

@@ -1,0 +1,627 @@
+"""paper_0803_1975_b200 — B200-native compressed modular GEMM (Dumas et al.,
+arXiv 0803.1975), host-side mirror of the reference's ``qgemm`` header API.
+
+The reference API (``/root/reference/proj/include/qgemm/*.hpp``) is
+restated here with the same names, argument meaning and error behaviour;
+every computation goes through the C ABI of ``_lib/libqgemm_b200.so``
+(``include/qgemm_b200.h``), i.e. through hand-written sm_100a kernels.
+There is no CPU fallback: if the library is missing this module raises
+on import, and device calls without a CUDA device raise ``CudaError``.
+
+PyTorch is used only as plumbing: device buffers, the current CUDA stream
+and pinned host memory.
+
+Reference mapping (file:line):
+  plan_compression / uncompressed_plan / plan_packed_axis / choose_panel
+      plan.hpp:125-224
+  compress_rows_reversed / compress_cols_forward / compress_outer_cols /
+  compress_outer_rows                      gemm.hpp:104-178
+  uncompress                               gemm.hpp:182-204
+  packed_common_product                    gemm.hpp:210-244
+  reduce_common_entry                      gemm.hpp:247-250
+  mul_common_compressed                    gemm.hpp:254-271
+  mul_common_repacked                      gemm.hpp:275-280
+  packed_right_product / redq_in_place / mul_right_compressed
+                                           gemm.hpp:285-335
+  blocked_accumulate                       gemm.hpp:450-489
+  random_residue_matrix                    prng.hpp:31-38
+  residue_checksum                         bench.hpp:43-47
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import enum
+import os
+from typing import Optional, Union
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libqgemm_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "qgemm_b200.h")
+
+
+# ----------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """qgemm::Error, errors.hpp:8-10."""
+
+
+class InvalidModulus(Error):
+    pass
+
+
+class NoCompression(Error):
+    pass
+
+
+class SlotOverflow(Error):
+    pass
+
+
+class DigitOverflow(Error):
+    pass
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class PlanMismatch(Error):
+    pass
+
+
+class UnsupportedAlgorithm(Error):
+    pass
+
+
+class ParseError(Error):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument (plan.hpp:128-129, gemm.hpp:455)."""
+
+
+class CudaError(Error):
+    pass
+
+
+class NotExact(Error):
+    pass
+
+
+_STATUS = {
+    1: InvalidModulus,
+    2: NoCompression,
+    3: SlotOverflow,
+    4: DigitOverflow,
+    5: DimensionMismatch,
+    6: PlanMismatch,
+    7: UnsupportedAlgorithm,
+    8: ParseError,
+    9: InvalidArgument,
+    10: CudaError,
+    11: Error,
+    12: NotExact,
+}
+
+
+# ----------------------------------------------------------------- C types
+class _Plan(ctypes.Structure):
+    _fields_ = [
+        ("p", ctypes.c_uint32),
+        ("t", ctypes.c_int32),
+        ("d", ctypes.c_int32),
+        ("e", ctypes.c_int32),
+        ("beta", ctypes.c_int32),
+        ("kmax", ctypes.c_uint64),
+        ("inv_qd", ctypes.c_double),
+        ("extraction", ctypes.c_int32),
+    ]
+
+
+class _GpuPlan(ctypes.Structure):
+    _fields_ = [("plan", _Plan), ("kblock_words", ctypes.c_uint64), ("max_exact_words", ctypes.c_uint64)]
+
+
+class _Orientation(ctypes.Structure):
+    _fields_ = [("direction", ctypes.c_int32), ("axis", ctypes.c_int32), ("slots", ctypes.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(make -C paper_0803_1975_b200). There is no CPU fallback."
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    sz, u32, u64, i32, vp = ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
+    sig = {
+        "qg_abi_version": ([], i32),
+        "qg_status_string": ([i32], ctypes.c_char_p),
+        "qg_plan_compression": ([u32, u64, i32, i32, P(_Plan)], i32),
+        "qg_uncompressed_plan": ([u32, u64, i32, P(_Plan)], i32),
+        "qg_plan_packed_axis": ([u32, u64, u64, i32, P(_Plan)], i32),
+        "qg_choose_panel": ([u32, u64, i32, P(u64)], i32),
+        "qg_max_exact_block": ([P(_Plan), P(u64)], i32),
+        "qg_gpu_plan_from": ([P(_Plan), u64, P(_GpuPlan)], i32),
+        "qg_plan_gpu": ([u32, u64, P(_GpuPlan)], i32),
+        "qg_gen_residues": ([u64, u32, sz, sz, sz, vp, i32, vp], i32),
+        "qg_compress_rows_reversed": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_compress_cols_forward": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_compress_outer_cols": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_compress_outer_rows": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_packed_common_product": ([P(_Plan), vp, vp, sz, sz, sz, vp, vp], i32),
+        "qg_reduce_common": ([P(_Plan), vp, sz, vp, vp], i32),
+        "qg_mul_common": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_mul_common_repacked": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, vp, vp], i32),
+        "qg_mul_right": ([P(_Plan), vp, sz, vp, sz, sz, sz, vp, vp], i32),
+        "qg_packed_right_product": ([P(_Plan), vp, sz, vp, sz, sz, sz, vp, vp], i32),
+        "qg_redq": ([P(_Plan), vp, sz, vp], i32),
+        "qg_uncompress": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp, vp], i32),
+        "qg_host_mul_common": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_blocked_accumulate": ([P(_Plan), vp, vp, sz, sz, sz, sz, vp], i32),
+        "qg_host_mul_right": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_kernel_launches": ([], u64),
+        "qg_last_kernel": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+EXPORTED_SYMBOLS = tuple(
+    n for n in dir(lib) if n.startswith("qg_")
+)  # populated lazily by ctypes; use header_symbols() for the declared list
+
+
+def header_symbols(path: str = HEADER_PATH) -> list:
+    """Function names declared in include/qgemm_b200.h."""
+    import re
+
+    text = open(path).read()
+    return sorted(set(re.findall(r"\b(qg_[a-z0-9_]+)\s*\(", text)))
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        cls = _STATUS.get(status, Error)
+        raise cls(lib.qg_status_string(status).decode())
+
+
+# ----------------------------------------------------------------- plans
+class ExtractionMode(enum.IntEnum):
+    """plan.hpp:14-17."""
+
+    ReciprocalMul = 0
+    AddHighBits = 1
+
+
+@dataclasses.dataclass(frozen=True)
+class CompressionPlan:
+    """CompressionPlan, plan.hpp:29-42."""
+
+    p: int
+    t: int
+    d: int
+    e: int
+    beta: int
+    kmax: int
+    inv_qd: float
+    extraction: int = 0
+
+    def q(self) -> int:
+        return 1 << self.t
+
+    def q_mask(self) -> int:
+        return (1 << self.t) - 1
+
+    def _c(self) -> _Plan:
+        return _Plan(self.p, self.t, self.d, self.e, self.beta, self.kmax, self.inv_qd, self.extraction)
+
+    @staticmethod
+    def _from(c: _Plan) -> "CompressionPlan":
+        return CompressionPlan(c.p, c.t, c.d, c.e, c.beta, c.kmax, c.inv_qd, c.extraction)
+
+
+@dataclasses.dataclass(frozen=True)
+class GpuPlan:
+    """A CompressionPlan k-blocked for the FP64 tensor-core contraction."""
+
+    plan: CompressionPlan
+    kblock_words: int
+    max_exact_words: int
+
+    def _c(self) -> _GpuPlan:
+        return _GpuPlan(self.plan._c(), self.kblock_words, self.max_exact_words)
+
+
+def make_plan(p: int, t: int, e: int, beta: int = 53) -> CompressionPlan:
+    """The hand-built plan of the reference tests (test_pack.cpp:15-24)."""
+    import math
+
+    if p < 2 or any(p % f == 0 for f in range(2, int(math.isqrt(p)) + 1)):
+        raise InvalidModulus(f"modulus {p} is not prime")
+    return CompressionPlan(p, t, e - 1, e, beta, ((1 << t) - 1) // ((p - 1) ** 2), math.ldexp(1.0, -t * (e - 1)), 0)
+
+
+def plan_compression(p: int, k: int, beta: int = 53, mode: int = ExtractionMode.ReciprocalMul) -> CompressionPlan:
+    out = _Plan()
+    _check(lib.qg_plan_compression(p, k, beta, int(mode), ctypes.byref(out)))
+    return CompressionPlan._from(out)
+
+
+def uncompressed_plan(p: int, k: int, beta: int = 53) -> CompressionPlan:
+    out = _Plan()
+    _check(lib.qg_uncompressed_plan(p, k, beta, ctypes.byref(out)))
+    return CompressionPlan._from(out)
+
+
+def plan_packed_axis(p: int, k: int, axis_len: int, beta: int = 53) -> CompressionPlan:
+    out = _Plan()
+    _check(lib.qg_plan_packed_axis(p, k, axis_len, beta, ctypes.byref(out)))
+    return CompressionPlan._from(out)
+
+
+def choose_panel(p: int, k: int, beta: int = 53) -> int:
+    out = ctypes.c_uint64()
+    _check(lib.qg_choose_panel(p, k, beta, ctypes.byref(out)))
+    return out.value
+
+
+def max_exact_block(plan: CompressionPlan) -> int:
+    out = ctypes.c_uint64()
+    pl = plan._c()
+    _check(lib.qg_max_exact_block(ctypes.byref(pl), ctypes.byref(out)))
+    return out.value
+
+
+def gpu_plan_from(plan: CompressionPlan, k: int) -> GpuPlan:
+    out = _GpuPlan()
+    pl = plan._c()
+    _check(lib.qg_gpu_plan_from(ctypes.byref(pl), k, ctypes.byref(out)))
+    return GpuPlan(CompressionPlan._from(out.plan), out.kblock_words, out.max_exact_words)
+
+
+def plan_gpu(p: int, k: int) -> GpuPlan:
+    out = _GpuPlan()
+    _check(lib.qg_plan_gpu(p, k, ctypes.byref(out)))
+    return GpuPlan(CompressionPlan._from(out.plan), out.kblock_words, out.max_exact_words)
+
+
+def kernel_launches() -> int:
+    return int(lib.qg_kernel_launches())
+
+
+def last_kernel() -> str:
+    return lib.qg_last_kernel().decode()
+
+
+# ----------------------------------------------------------------- device data
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream() -> ctypes.c_void_p:
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return 0
+    if t.dtype == torch.int32:
+        return 2
+    if getattr(torch, "uint32", None) is not None and t.dtype == torch.uint32:
+        return 1
+    raise InvalidArgument(f"residues must be float64, int32 or uint32 tensors, got {t.dtype}")
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not t.is_cuda:
+            raise InvalidArgument("device entry points take CUDA tensors (use the *_host functions for host data)")
+        if not t.is_contiguous():
+            raise InvalidArgument("tensors must be contiguous row-major")
+
+
+class PackDirection(enum.IntEnum):
+    Forward = 0
+    Reversed = 1
+
+
+class PackAxis(enum.IntEnum):
+    Row = 0
+    Column = 1
+
+
+@dataclasses.dataclass
+class PackOrientation:
+    """PackOrientation, matrix.hpp:33-39."""
+
+    direction: int = PackDirection.Forward
+    axis: int = PackAxis.Column
+    slots: int = 1
+
+
+@dataclasses.dataclass
+class CompressedMatrix:
+    """CompressedMatrix<DoubleWord>, matrix.hpp:44-63: row-major packed words
+    (a float64 CUDA tensor of shape stored_rows x stored_cols) plus the
+    metadata needed to undo the packing."""
+
+    logical_rows: int
+    logical_cols: int
+    stored_rows: int
+    stored_cols: int
+    orientation: PackOrientation
+    plan: CompressionPlan
+    data: object  # torch.Tensor, float64, cuda
+
+
+def random_residue_matrix(rows: int, cols: int, p: int, seed: int, *, dtype=None, device="cuda",
+                          row0: int = 0):
+    """random_residue_matrix(rows, cols, PrimeModulus(p), seed), prng.hpp:31-38,
+    generated on the device (K0); rows [row0, row0+rows) of the seeded matrix."""
+    torch = _torch()
+    dtype = torch.float64 if dtype is None else dtype
+    out = torch.empty((rows, cols), dtype=dtype, device=device)
+    code = 0 if dtype == torch.float64 else 1
+    if code == 1 and dtype not in (torch.int32, getattr(torch, "uint32", torch.int32)):
+        raise InvalidArgument("dtype must be float64, int32 or uint32")
+    _check(lib.qg_gen_residues(seed, p, row0, rows, cols, _ptr(out), code, _stream()))
+    return out
+
+
+def compress_rows_reversed(a, plan: CompressionPlan) -> CompressedMatrix:
+    """gemm.hpp:104-118: m x ceil(k/e) words, {Reversed, Column, e}."""
+    torch = _torch()
+    _require_cuda(a)
+    m, k = a.shape
+    groups = (k + plan.e - 1) // plan.e
+    out = torch.empty((m, groups), dtype=torch.float64, device=a.device)
+    pl = plan._c()
+    _check(lib.qg_compress_rows_reversed(ctypes.byref(pl), _ptr(a), _dtype_code(a), m, k, k, _ptr(out), groups, _stream()))
+    return CompressedMatrix(m, k, m, groups, PackOrientation(PackDirection.Reversed, PackAxis.Column, plan.e), plan, out)
+
+
+def compress_cols_forward(b, plan: CompressionPlan) -> CompressedMatrix:
+    """gemm.hpp:122-140: ceil(k/e) x n words, {Forward, Row, e}."""
+    torch = _torch()
+    _require_cuda(b)
+    k, n = b.shape
+    groups = (k + plan.e - 1) // plan.e
+    out = torch.empty((groups, n), dtype=torch.float64, device=b.device)
+    pl = plan._c()
+    _check(lib.qg_compress_cols_forward(ctypes.byref(pl), _ptr(b), _dtype_code(b), k, n, n, _ptr(out), n, _stream()))
+    return CompressedMatrix(k, n, groups, n, PackOrientation(PackDirection.Forward, PackAxis.Row, plan.e), plan, out)
+
+
+def compress_outer_cols(b, plan: CompressionPlan) -> CompressedMatrix:
+    """gemm.hpp:145-158: rows x ceil(cols/e) words, {Forward, Column, e}."""
+    torch = _torch()
+    _require_cuda(b)
+    rows, cols = b.shape
+    groups = (cols + plan.e - 1) // plan.e
+    out = torch.empty((rows, groups), dtype=torch.float64, device=b.device)
+    pl = plan._c()
+    _check(lib.qg_compress_outer_cols(ctypes.byref(pl), _ptr(b), _dtype_code(b), rows, cols, cols, _ptr(out), groups, _stream()))
+    return CompressedMatrix(rows, cols, rows, groups, PackOrientation(PackDirection.Forward, PackAxis.Column, plan.e), plan, out)
+
+
+def compress_outer_rows(a, plan: CompressionPlan) -> CompressedMatrix:
+    """gemm.hpp:161-178: ceil(rows/e) x cols words, {Forward, Row, e}."""
+    torch = _torch()
+    _require_cuda(a)
+    rows, cols = a.shape
+    groups = (rows + plan.e - 1) // plan.e
+    out = torch.empty((groups, cols), dtype=torch.float64, device=a.device)
+    pl = plan._c()
+    _check(lib.qg_compress_outer_rows(ctypes.byref(pl), _ptr(a), _dtype_code(a), rows, cols, cols, _ptr(out), cols, _stream()))
+    return CompressedMatrix(rows, cols, groups, cols, PackOrientation(PackDirection.Forward, PackAxis.Row, plan.e), plan, out)
+
+
+def uncompress(cm: CompressedMatrix):
+    """gemm.hpp:182-204 -> int32 logical_rows x logical_cols residues."""
+    torch = _torch()
+    out = torch.empty((cm.logical_rows, cm.logical_cols), dtype=torch.int32, device=cm.data.device)
+    pl = cm.plan._c()
+    o = _Orientation(int(cm.orientation.direction), int(cm.orientation.axis), int(cm.orientation.slots))
+    _check(lib.qg_uncompress(ctypes.byref(pl), o, _ptr(cm.data), cm.stored_rows, cm.stored_cols,
+                             cm.logical_rows, cm.logical_cols, _ptr(out), _stream()))
+    return out
+
+
+def _plans_compatible(a: CompressionPlan, b: CompressionPlan) -> bool:  # gemm.hpp:37-39
+    return a.p == b.p and a.t == b.t and a.e == b.e and a.beta == b.beta
+
+
+def _check_common_operands(ca: CompressedMatrix, cb: CompressedMatrix) -> None:
+    """The checks of packed_common_product, gemm.hpp:213-225."""
+    if not _plans_compatible(ca.plan, cb.plan):
+        raise PlanMismatch("operands were packed under different plans")
+    if (ca.orientation.direction != PackDirection.Reversed or ca.orientation.axis != PackAxis.Column
+            or cb.orientation.direction != PackDirection.Forward or cb.orientation.axis != PackAxis.Row):
+        raise PlanMismatch("common product needs a row-reversed left operand and a column-forward right operand")
+    if ca.logical_cols != cb.logical_rows or ca.stored_cols != cb.stored_rows:
+        raise DimensionMismatch(
+            f"inner dimensions disagree: {ca.logical_rows}x{ca.logical_cols} times {cb.logical_rows}x{cb.logical_cols}")
+
+
+def packed_common_product(ca: CompressedMatrix, cb: CompressedMatrix):
+    """gemm.hpp:210-244 with the reference's per-product high part
+    (word.hpp:28-30): the m x n float64 accumulators, bit-identical."""
+    torch = _torch()
+    _check_common_operands(ca, cb)
+    if ca.logical_cols > ca.plan.kmax:
+        raise PlanMismatch(f"common dimension {ca.logical_cols} exceeds kmax={ca.plan.kmax}")
+    out = torch.empty((ca.logical_rows, cb.logical_cols), dtype=torch.float64, device=ca.data.device)
+    pl = ca.plan._c()
+    _check(lib.qg_packed_common_product(ctypes.byref(pl), _ptr(ca.data), _ptr(cb.data), ca.logical_rows,
+                                        cb.logical_cols, ca.logical_cols, _ptr(out), _stream()))
+    return out
+
+
+def reduce_common_entry(acc, plan: CompressionPlan):
+    """gemm.hpp:247-250 over a tensor of accumulators -> int32 residues."""
+    torch = _torch()
+    out = torch.empty(acc.shape, dtype=torch.int32, device=acc.device)
+    pl = plan._c()
+    _check(lib.qg_reduce_common(ctypes.byref(pl), _ptr(acc), acc.numel(), _ptr(out), _stream()))
+    return out
+
+
+def _as_gpu_plan(plan: Union[CompressionPlan, GpuPlan], k: int) -> GpuPlan:
+    return plan if isinstance(plan, GpuPlan) else gpu_plan_from(plan, k)
+
+
+def mul_common_compressed(a_or_ca, b_or_cb, plan: Optional[Union[CompressionPlan, GpuPlan]] = None):
+    """mul_common_compressed, gemm.hpp:254-271, on the FP64 tensor cores.
+
+    (a, b, plan): residue tensors, packed on the device under ``plan``;
+    (ca, cb): operands compressed already (their plan is used).
+    A GpuPlan (plan_gpu) may cover k > kmax through in-kernel k-blocks.
+    Returns int32 C (m x n)."""
+    torch = _torch()
+    if isinstance(a_or_ca, CompressedMatrix):
+        ca, cb = a_or_ca, b_or_cb
+        _check_common_operands(ca, cb)
+        gp = _as_gpu_plan(plan if plan is not None else ca.plan, ca.logical_cols)
+    else:
+        a, b = a_or_ca, b_or_cb
+        if a.shape[1] != b.shape[0]:  # check_inner_dims, gemm.hpp:22-27
+            raise DimensionMismatch(
+                f"inner dimensions disagree: {a.shape[0]}x{a.shape[1]} times {b.shape[0]}x{b.shape[1]}")
+        gp = _as_gpu_plan(plan, a.shape[1])
+        base = gp.plan
+        k = a.shape[1]
+        if isinstance(plan, GpuPlan) and k > base.kmax:
+            # blocked plan: pack with a kmax-free plan view (blocks enforce Eq. 3)
+            big = dataclasses.replace(base, kmax=max(base.kmax, k))
+            ca, cb = compress_rows_reversed(a, big), compress_cols_forward(b, big)
+            ca.plan = cb.plan = base
+        else:
+            ca, cb = compress_rows_reversed(a, base), compress_cols_forward(b, base)
+    m, n, k = ca.logical_rows, cb.logical_cols, ca.logical_cols
+    out = torch.empty((m, n), dtype=torch.int32, device=ca.data.device)
+    g = gp._c()
+    _check(lib.qg_mul_common(ctypes.byref(g), _ptr(ca.data), _ptr(cb.data), m, n, k, _ptr(out), n, _stream()))
+    return out
+
+
+def mul_common_repacked(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMatrix:
+    """mul_common_repacked, gemm.hpp:275-280 (ReduceAndCompress of C's rows)."""
+    torch = _torch()
+    c = mul_common_compressed(a, b, plan)
+    base = plan.plan if isinstance(plan, GpuPlan) else plan
+    return compress_outer_cols(c, base)
+
+
+def packed_right_product(a, cb: CompressedMatrix) -> CompressedMatrix:
+    """gemm.hpp:285-310: exact A x CB (pre-REDQ words)."""
+    return _right(a, cb, redq=False)
+
+
+def mul_right_compressed(a, cb: CompressedMatrix) -> CompressedMatrix:
+    """gemm.hpp:320-335: packed_right_product + redq_in_place, fused. ``a``
+    may also be a Forward CompressedMatrix (it is uncompressed first)."""
+    if isinstance(a, CompressedMatrix):
+        if a.orientation.direction != PackDirection.Forward:
+            raise PlanMismatch("left operand must be packed forward to be unpacked")
+        a = uncompress(a)
+    return _right(a, cb, redq=True)
+
+
+def _right(a, cb: CompressedMatrix, redq: bool) -> CompressedMatrix:
+    torch = _torch()
+    if cb.orientation.direction != PackDirection.Forward or cb.orientation.axis != PackAxis.Column:
+        raise PlanMismatch("right product needs the right operand packed forward on its columns")
+    m, k = a.shape
+    if k != cb.logical_rows:
+        raise DimensionMismatch(
+            f"inner dimensions disagree: {m}x{k} times {cb.logical_rows}x{cb.logical_cols}")
+    if k > cb.plan.kmax:
+        raise PlanMismatch(f"common dimension {k} exceeds kmax={cb.plan.kmax}")
+    ad = a if a.dtype == torch.float64 else a.to(torch.float64)
+    ad = ad.contiguous()
+    out = torch.empty((m, cb.stored_cols), dtype=torch.float64, device=cb.data.device)
+    pl = cb.plan._c()
+    fn = lib.qg_mul_right if redq else lib.qg_packed_right_product
+    _check(fn(ctypes.byref(pl), _ptr(ad), k, _ptr(cb.data), m, k, cb.logical_cols, _ptr(out), _stream()))
+    return CompressedMatrix(m, cb.logical_cols, m, cb.stored_cols, dataclasses.replace(cb.orientation), cb.plan, out)
+
+
+def redq_in_place(cm: CompressedMatrix) -> None:
+    """gemm.hpp:313-316."""
+    pl = cm.plan._c()
+    _check(lib.qg_redq(ctypes.byref(pl), _ptr(cm.data), cm.data.numel(), _stream()))
+
+
+def residue_checksum(c) -> int:
+    """bench.hpp:43-47: sum of residues mod 2^32."""
+    torch = _torch()
+    if hasattr(c, "is_cuda"):
+        return int(c.to(torch.int64).sum().item()) & 0xFFFFFFFF
+    return int(np.asarray(c, dtype=np.uint64).sum()) & 0xFFFFFFFF
+
+
+# ----------------------------------------------------------------- host data
+def _host_u32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint32))
+
+
+def mul_common_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+    """mul_common_compressed(A, B, plan) on host ResidueMatrix data
+    (uint32 row-major): copies in, runs the kernels, copies C out."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.uint32)
+    pl = plan._c()
+    _check(lib.qg_host_mul_common(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
+                                  m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
+    return c
+
+
+def blocked_accumulate_host(a, b, plan: CompressionPlan, kpanel: int) -> np.ndarray:
+    """blocked_accumulate(A, B, plan, kpanel), gemm.hpp:450-489, host data."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.uint32)
+    pl = plan._c()
+    _check(lib.qg_host_blocked_accumulate(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p),
+                                          b.ctypes.data_as(ctypes.c_void_p), m, k, n, kpanel,
+                                          c.ctypes.data_as(ctypes.c_void_p)))
+    return c
+
+
+def mul_right_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+    """mul_right_compressed(A, compress_outer_cols(B, plan)) on host data:
+    the post-REDQ words, m x ceil(n/e) float64."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
+    cc = np.empty((m, (n + plan.e - 1) // plan.e), dtype=np.float64)
+    pl = plan._c()
+    _check(lib.qg_host_mul_right(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
+                                 m, k, n, cc.ctypes.data_as(ctypes.c_void_p)))
+    return cc

@@ -1,0 +1,448 @@
+// qg_abi.cu — the C ABI (include/qgemm_b200.h): argument checks in the
+// reference's order, plan -> kernel dispatch, and the host-buffer entry points.
+// Every computation is a kernel launch on the caller's stream; nothing here
+// computes results on the CPU.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/qgemm_b200.h"
+#include "qg_kernels.h"
+
+namespace qg {
+bool is_prime(uint64_t n);
+uint64_t max_exact_block(uint32_t p, int t, int e);
+}  // namespace qg
+
+namespace qgk {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace qgk
+
+namespace {
+
+thread_local const char* g_last_kernel = "none";
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? QG_OK : QG_CUDA_ERROR; }
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
+
+// CompressionPlan usable by the DoubleWord backend (pack.hpp:19-24).
+int check_plan(const qg_plan* plan) {
+  if (!plan) return QG_INVALID_ARGUMENT;
+  if (plan->p < 2 || !qg::is_prime(plan->p)) return QG_INVALID_MODULUS;
+  if (plan->beta > 53) return QG_PLAN_MISMATCH;
+  if (plan->t < 1 || plan->e < 1 || plan->d != plan->e - 1 || plan->t * plan->e > 63)
+    return QG_PLAN_MISMATCH;
+  return QG_OK;
+}
+
+int check_dtype(qg_dtype d) { return (d == QG_F64 || d == QG_U32 || d == QG_I32) ? QG_OK : QG_INVALID_ARGUMENT; }
+
+// Device flag for DigitOverflow (redq / extract_all throw it in the reference).
+struct DeviceFlag {
+  int* ptr = nullptr;
+  cudaStream_t s;
+  explicit DeviceFlag(cudaStream_t st) : s(st) {
+    if (cudaMallocAsync(&ptr, sizeof(int), s) == cudaSuccess) cudaMemsetAsync(ptr, 0, sizeof(int), s);
+    else ptr = nullptr;
+  }
+  int read(int* value) {
+    int v = 0;
+    cudaError_t e = cudaMemcpyAsync(&v, ptr, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    *value = v;
+    return cuda_status(e);
+  }
+  ~DeviceFlag() {
+    if (ptr) cudaFreeAsync(ptr, s);
+  }
+};
+
+// The common-variant contraction, dispatched on the block structure: DMMA when
+// every block is provably exact (Eq. G) and spans whole 4-word k-steps, the
+// reference's per-product high-part kernel otherwise. words_per_block_layout:
+// when the words come in padded panels (blocked_accumulate), blocks must not
+// straddle them.
+int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca, const double* cb,
+               size_t ldcb, size_t m, size_t n, size_t K, int32_t* c, size_t ldc, cudaStream_t s) {
+  if (m == 0 || n == 0) return QG_OK;
+  const uint64_t exact = qg::max_exact_block(pl.p, pl.t, pl.e);
+  const uint32_t qmask = (uint32_t)((1ull << pl.t) - 1);
+  const bool single = kblock >= K;
+  uint64_t kb = single ? K : kblock;
+  if (!single && kb > exact) kb = exact;  // smaller blocks are always exact
+  const uint64_t nblocks = single ? 1 : ceil_div(K, kb);
+  const bool dmma_ok = single ? (K <= exact) : (kb >= 4);
+  if (dmma_ok && K > 0) {
+    qgk::DotArgs a;
+    a.ca = ca;
+    a.ldca = ldca;
+    a.cb = cb;
+    a.ldcb = ldcb;
+    a.M = (int)m;
+    a.N = (int)n;
+    a.K = (int)K;
+    a.kb_steps = single ? 0 : (int)(kb / 4);
+    a.sh_base = 1075 + pl.t * pl.d;
+    a.qmask = qmask;
+    a.p = pl.p;
+    const unsigned __int128 worst = (unsigned __int128)ceil_div(K, single ? K : (kb / 4) * 4) * qmask;
+    a.reduce_each = worst >= ((unsigned __int128)1 << 32) ? 1 : 0;
+    a.c = c;
+    a.ldc = ldc;
+    return cuda_status(qgk::launch_dot_dmma(a, s, &g_last_kernel));
+  }
+  qgk::HighArgs h;
+  h.ca = ca;
+  h.ldca = ldca;
+  h.cb = cb;
+  h.ldcb = ldcb;
+  h.M = (int)m;
+  h.N = (int)n;
+  h.K = (int)K;
+  h.inv_qd = pl.inv_qd;
+  h.kb_words = single ? 0 : (int)kblock;
+  h.qmask = qmask;
+  h.p = pl.p;
+  h.acc = nullptr;
+  h.c = c;
+  h.ldc = ldc;
+  (void)nblocks;
+  return cuda_status(qgk::launch_dot_highpart(h, s, &g_last_kernel));
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t qg_kernel_launches(void) { return qgk::g_launches.load(); }
+const char* qg_last_kernel(void) { return g_last_kernel; }
+
+int qg_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols, void* dst,
+                    qg_dtype dtype, void* stream) {
+  if (p < 2 || !qg::is_prime(p)) return QG_INVALID_MODULUS;  // PrimeModulus, field.hpp:19-21
+  if (dtype != QG_F64 && dtype != QG_U32) return QG_INVALID_ARGUMENT;
+  if (!dst && rows * cols) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_gen_residues(seed, p, row0, rows, cols, dst, dtype, as_stream(stream)));
+}
+
+int qg_compress_rows_reversed(const qg_plan* plan, const void* a, qg_dtype dtype, size_t m,
+                              size_t k, size_t lda, double* ca, size_t ldca, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // check_common_dim, gemm.hpp:29-35
+  const size_t K = ceil_div(k, plan->e);
+  if (lda < k || ldca < K) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, a, dtype, m, k, lda, plan->t,
+                                      plan->e, ca, ldca, 0, 0, as_stream(stream)));
+}
+
+int qg_compress_cols_forward(const qg_plan* plan, const void* b, qg_dtype dtype, size_t k,
+                             size_t n, size_t ldb, double* cb, size_t ldcb, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;
+  if (ldb < n || ldcb < n) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack(qgk::PACK_COLS_FORWARD, b, dtype, k, n, ldb, plan->t,
+                                      plan->e, cb, ldcb, 0, 0, as_stream(stream)));
+}
+
+int qg_compress_outer_cols(const qg_plan* plan, const void* b, qg_dtype dtype, size_t rows,
+                           size_t cols, size_t ldb, double* cb, size_t ldcb, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (ldb < cols || ldcb < ceil_div(cols, plan->e)) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack(qgk::PACK_OUTER_COLS, b, dtype, rows, cols, ldb, plan->t,
+                                      plan->e, cb, ldcb, 0, 0, as_stream(stream)));
+}
+
+int qg_compress_outer_rows(const qg_plan* plan, const void* a, qg_dtype dtype, size_t rows,
+                           size_t cols, size_t lda, double* ca, size_t ldca, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (lda < cols || ldca < cols) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack(qgk::PACK_OUTER_ROWS, a, dtype, rows, cols, lda, plan->t,
+                                      plan->e, ca, ldca, 0, 0, as_stream(stream)));
+}
+
+int qg_packed_common_product(const qg_plan* plan, const double* ca, const double* cb, size_t m,
+                             size_t n, size_t k, double* acc, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:225
+  qgk::HighArgs h;
+  h.ca = ca;
+  h.ldca = ceil_div(k, plan->e);
+  h.cb = cb;
+  h.ldcb = n;
+  h.M = (int)m;
+  h.N = (int)n;
+  h.K = (int)ceil_div(k, plan->e);
+  h.inv_qd = plan->inv_qd;
+  h.kb_words = 0;
+  h.qmask = (uint32_t)((1ull << plan->t) - 1);
+  h.p = plan->p;
+  h.acc = acc;
+  h.c = nullptr;
+  h.ldc = n;
+  if (m == 0 || n == 0) return QG_OK;
+  if (h.K == 0) return cuda_status(cudaMemsetAsync(acc, 0, m * n * sizeof(double), as_stream(stream)));
+  return cuda_status(qgk::launch_dot_highpart(h, as_stream(stream), &g_last_kernel));
+}
+
+int qg_reduce_common(const qg_plan* plan, const double* acc, size_t count, int32_t* c, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  return cuda_status(qgk::launch_reduce_common(acc, count, (uint32_t)((1ull << plan->t) - 1),
+                                               plan->p, c, as_stream(stream)));
+}
+
+int qg_mul_common(const qg_gpu_plan* gplan, const double* ca, const double* cb, size_t m, size_t n,
+                  size_t k, int32_t* c, size_t ldc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if (ldc < n) return QG_INVALID_ARGUMENT;
+  const size_t K = ceil_div(k, pl.e);
+  uint64_t kb = gplan->kblock_words;
+  if (kb == 0) return QG_INVALID_ARGUMENT;
+  // Eq. 3 per block (gemm.hpp:456): a block may hold at most kmax residues.
+  if (kb < K && kb * (uint64_t)pl.e > pl.kmax) return QG_PLAN_MISMATCH;
+  if (kb >= K && k > pl.kmax) return QG_PLAN_MISMATCH;
+  if (K == 0) {
+    cudaStream_t s = as_stream(stream);
+    for (size_t i = 0; i < m; ++i)
+      if (cudaMemsetAsync(c + i * ldc, 0, n * sizeof(int32_t), s) != cudaSuccess) return QG_CUDA_ERROR;
+    return QG_OK;
+  }
+  return run_common(pl, kb, ca, K, cb, n, m, n, K, c, ldc, as_stream(stream));
+}
+
+int qg_mul_common_repacked(const qg_gpu_plan* gplan, const double* ca, const double* cb, size_t m,
+                           size_t n, size_t k, double* cc, int32_t* workspace, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  int32_t* ws = workspace;
+  if (!ws && m * n) {
+    if (cudaMallocAsync(&ws, m * n * sizeof(int32_t), s) != cudaSuccess) return QG_CUDA_ERROR;
+  }
+  int st = qg_mul_common(gplan, ca, cb, m, n, k, ws, n, stream);
+  if (!st)  // compress_outer_cols(C, plan), gemm.hpp:279
+    st = cuda_status(qgk::launch_pack(qgk::PACK_OUTER_COLS, ws, QG_I32, m, n, n, gplan->plan.t,
+                                      gplan->plan.e, cc, ceil_div(n, gplan->plan.e), 0, 0, s));
+  if (!workspace && ws) cudaFreeAsync(ws, s);
+  return st;
+}
+
+static int right_common(const qg_plan* plan, const double* a, size_t lda, const double* cbo,
+                        size_t m, size_t k, size_t n, double* cc, int redq, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
+  if (plan->t * plan->e > 53) return QG_PLAN_MISMATCH;  // sums must stay exact
+  if (lda < k) return QG_INVALID_ARGUMENT;
+  const size_t H = ceil_div(n, plan->e);
+  if (m == 0 || H == 0) return QG_OK;
+  if (k == 0) return cuda_status(cudaMemsetAsync(cc, 0, m * H * sizeof(double), as_stream(stream)));
+  qgk::RightArgs r;
+  r.a = a;
+  r.lda = lda;
+  r.cb = cbo;
+  r.ldcb = H;
+  r.M = (int)m;
+  r.N = (int)H;
+  r.K = (int)k;
+  r.t = plan->t;
+  r.e = plan->e;
+  r.p = plan->p;
+  r.redq = redq;
+  r.cc = cc;
+  r.ldcc = H;
+  return cuda_status(qgk::launch_right_dmma(r, as_stream(stream), &g_last_kernel));
+}
+
+int qg_mul_right(const qg_plan* plan, const double* a, size_t lda, const double* cbo, size_t m,
+                 size_t k, size_t n, double* cc, void* stream) {
+  return right_common(plan, a, lda, cbo, m, k, n, cc, 1, stream);
+}
+
+int qg_packed_right_product(const qg_plan* plan, const double* a, size_t lda, const double* cbo,
+                            size_t m, size_t k, size_t n, double* cc, void* stream) {
+  return right_common(plan, a, lda, cbo, m, k, n, cc, 0, stream);
+}
+
+int qg_redq(const qg_plan* plan, double* words, size_t count, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (count == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  DeviceFlag flag(s);
+  if (!flag.ptr) return QG_CUDA_ERROR;
+  if ((st = cuda_status(qgk::launch_redq(words, count, plan->t, plan->e, plan->p, flag.ptr, s)))) return st;
+  int over = 0;
+  if ((st = flag.read(&over))) return st;
+  return over ? QG_DIGIT_OVERFLOW : QG_OK;
+}
+
+int qg_uncompress(const qg_plan* plan, qg_orientation o, const double* words, size_t stored_rows,
+                  size_t stored_cols, size_t logical_rows, size_t logical_cols, int32_t* out,
+                  void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (o.slots < 1 || o.slots > plan->e) return QG_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  DeviceFlag flag(s);
+  if (!flag.ptr) return QG_CUDA_ERROR;
+  if ((st = cuda_status(qgk::launch_uncompress(words, stored_rows, stored_cols, logical_rows,
+                                               logical_cols, plan->t, plan->e, o.slots,
+                                               o.direction == 1, o.axis == 1, plan->p, out,
+                                               flag.ptr, s))))
+    return st;
+  int over = 0;
+  if ((st = flag.read(&over))) return st;
+  return over ? QG_DIGIT_OVERFLOW : QG_OK;
+}
+
+// ------------------------------------------------------------ host buffers
+
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit DevBuf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return bytes ? cudaMallocAsync(&p, bytes, s) : cudaSuccess; }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+#define QG_TRY(x)                       \
+  do {                                  \
+    cudaError_t e_ = (x);               \
+    if (e_ != cudaSuccess) return QG_CUDA_ERROR; \
+  } while (0)
+}  // namespace
+
+int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                       size_t k, size_t n, uint32_t* c) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // compress_rows_reversed's check, gemm.hpp:106
+  qg_gpu_plan gp;
+  if ((st = qg_gpu_plan_from(plan, k, &gp))) return st;
+  cudaStream_t s = nullptr;
+  const size_t K = ceil_div(k, plan->e);
+  DevBuf da(s), db(s), dca(s), dcb(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dca.alloc(m * K * 8));
+  QG_TRY(dcb.alloc(K * n * 8));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  if ((st = qg_compress_rows_reversed(plan, da.p, QG_U32, m, k, k, (double*)dca.p, K, s))) return st;
+  if ((st = qg_compress_cols_forward(plan, db.p, QG_U32, k, n, n, (double*)dcb.p, n, s))) return st;
+  if ((st = qg_mul_common(&gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
+    return st;
+  if (m * n) QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
+                               size_t m, size_t k, size_t n, size_t kpanel, uint32_t* c) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (kpanel < 1) return QG_INVALID_ARGUMENT;             // gemm.hpp:455
+  if (kpanel > plan->kmax) return QG_PLAN_MISMATCH;       // gemm.hpp:456
+  cudaStream_t s = nullptr;
+  if (m * n == 0) return QG_OK;
+  // Each panel is packed on its own (gemm.hpp:471-478) into words padded to a
+  // whole number of 4-word k-steps, so k-blocks never straddle two panels.
+  const size_t pw = ceil_div(kpanel, plan->e);
+  const uint64_t exact = qg::max_exact_block(plan->p, plan->t, plan->e);
+  size_t pw4 = ceil_div(pw, 4) * 4;
+  uint64_t kb = 0;  // words per k-block, a divisor of pw4 in whole k-steps
+  for (uint64_t steps = pw4 / 4; steps >= 1; --steps)
+    if ((pw4 / 4) % steps == 0 && steps * 4 <= exact) {
+      kb = steps * 4;
+      break;
+    }
+  if (kb == 0) pw4 = pw;  // DMMA cannot be exact here: high-part kernel, panel = block
+  const size_t npanels = k ? ceil_div(k, kpanel) : 0;
+  const size_t W = npanels * pw4;
+  DevBuf da(s), db(s), dca(s), dcb(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dca.alloc(m * W * 8));
+  QG_TRY(dcb.alloc(W * n * 8));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  if (W == 0) {
+    QG_TRY(cudaMemsetAsync(dc.p, 0, m * n * 4, s));
+  } else {
+    QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, plan->t, plan->e,
+                            (double*)dca.p, W, kpanel, pw4, s));
+    QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, plan->t, plan->e,
+                            (double*)dcb.p, n, kpanel, pw4, s));
+    if (kb) {
+      if ((st = run_common(*plan, kb, (const double*)dca.p, W, (const double*)dcb.p, n, m, n, W,
+                           (int32_t*)dc.p, n, s)))
+        return st;
+    } else {
+      qgk::HighArgs h;
+      h.ca = (const double*)dca.p;
+      h.ldca = W;
+      h.cb = (const double*)dcb.p;
+      h.ldcb = n;
+      h.M = (int)m;
+      h.N = (int)n;
+      h.K = (int)W;
+      h.inv_qd = plan->inv_qd;
+      h.kb_words = (int)pw4;
+      h.qmask = (uint32_t)((1ull << plan->t) - 1);
+      h.p = plan->p;
+      h.acc = nullptr;
+      h.c = (int32_t*)dc.p;
+      h.ldc = n;
+      if ((st = cuda_status(qgk::launch_dot_highpart(h, s, &g_last_kernel)))) return st;
+    }
+  }
+  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                      size_t k, size_t n, double* cc) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;
+  cudaStream_t s = nullptr;
+  const size_t H = ceil_div(n, plan->e);
+  DevBuf da32(s), dad(s), db(s), dcb(s), dcc(s);
+  QG_TRY(da32.alloc(m * k * 4));
+  QG_TRY(dad.alloc(m * k * 8));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dcb.alloc(k * H * 8));
+  QG_TRY(dcc.alloc(m * H * 8));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da32.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  // A's residues as doubles for the DMMA operand: an e = 1 "pack" of each row.
+  if (m * k)
+    QG_TRY(qgk::launch_pack(qgk::PACK_OUTER_COLS, da32.p, QG_U32, m, k, k, 1, 1, (double*)dad.p, k, 0, 0, s));
+  if ((st = qg_compress_outer_cols(plan, db.p, QG_U32, k, n, n, (double*)dcb.p, H, s))) return st;
+  if ((st = qg_mul_right(plan, (const double*)dad.p, k, (const double*)dcb.p, m, k, n, (double*)dcc.p, s)))
+    return st;
+  if (m * H) QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+}  // extern "C"

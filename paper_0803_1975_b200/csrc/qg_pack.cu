@@ -1,0 +1,278 @@
+// qg_pack.cu — HBM-bound kernels: seeded residue generation (K0), the four
+// packings (K1-K3 + outer rows), REDQ, digit scatter (uncompress, K6) and the
+// common-entry reduction. Each thread produces whole words, so every output
+// store is a coalesced 8-byte write; input residues are read once.
+#include "qg_kernels.h"
+#include "qg_device.cuh"
+
+namespace qgk {
+
+// K0: random_residue_matrix, prng.hpp:31-38 — element (r, c) of the matrix is
+// SplitMix64 output number r*cols + c, reduced with `% p` (prng.hpp:25).
+template <typename TOut>
+__global__ void k_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols,
+                               TOut* __restrict__ dst) {
+  const size_t total = rows * cols;
+  const size_t base = row0 * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x)
+    store_residue(dst + i, (uint32_t)(splitmix64_at(seed, base + i) % p));
+}
+
+// Panel geometry of the common dimension: k residues split into panels of
+// panel_len (the last may be short), each packed on its own into
+// ceil(len/e) words and stored at a stride of panel_words (>= those words;
+// the padding words are zero). One panel of length k is the plain layout;
+// several reproduce blocked_accumulate's per-panel packing (gemm.hpp:460-478).
+struct Panels {
+  size_t k, panel_len;
+  unsigned panel_words, npanels;
+  __device__ __forceinline__ bool locate(unsigned gw_all, int e, size_t* base, int* len) const {
+    const unsigned pi = gw_all / panel_words, gw = gw_all - pi * panel_words;
+    const size_t pstart = (size_t)pi * panel_len;
+    const size_t plen = (k - pstart) < panel_len ? (k - pstart) : panel_len;
+    const size_t words = (plen + e - 1) / e;
+    if (gw >= words) return false;
+    *base = pstart + (size_t)gw * e;
+    const size_t rem = pstart + plen - *base;
+    *len = (int)(rem < (size_t)e ? rem : (size_t)e);
+    return true;
+  }
+};
+
+// K1: compress_rows_reversed, gemm.hpp:104-118 + compress_reverse,
+// pack.hpp:59-70. Word (i, g) = sum_s a[i][g e + s] Q^(d - s); a short final
+// group is shifted up by Q^(e - len).
+template <typename TIn>
+__global__ void k_pack_rows_reversed(const TIn* __restrict__ a, size_t m, size_t lda, int t, int e,
+                                     Panels pn, double* __restrict__ ca, size_t ldca) {
+  const unsigned W = pn.panel_words * pn.npanels;
+  for (size_t i = blockIdx.y; i < m; i += gridDim.y) {
+    const TIn* row = a + i * lda;
+    for (unsigned g = blockIdx.x * blockDim.x + threadIdx.x; g < W; g += gridDim.x * blockDim.x) {
+      size_t base;
+      int len;
+      uint64_t r = 0;
+      if (pn.locate(g, e, &base, &len)) {
+        for (int s = 0; s < len; ++s) r = (r << t) | residue_bits(row[base + s]);
+        r <<= t * (e - len);
+      }
+      ca[i * ldca + g] = __ull2double_rn(r);
+    }
+  }
+}
+
+// K2: compress_cols_forward, gemm.hpp:122-140 + compress_forward,
+// pack.hpp:47-54. Word (g, j) = sum_s b[g e + s][j] Q^s; lanes run along j so
+// every load and store is coalesced.
+template <typename TIn>
+__global__ void k_pack_cols_forward(const TIn* __restrict__ b, size_t n, size_t ldb, int t, int e,
+                                    Panels pn, double* __restrict__ cb, size_t ldcb) {
+  const unsigned W = pn.panel_words * pn.npanels;
+  for (unsigned g = blockIdx.y; g < W; g += gridDim.y) {
+    size_t base;
+    int len;
+    const bool live = pn.locate(g, e, &base, &len);
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < n;
+         j += (size_t)gridDim.x * blockDim.x) {
+      uint64_t r = 0;
+      if (live)
+        for (int s = len - 1; s >= 0; --s) r = (r << t) | residue_bits(b[(base + s) * ldb + j]);
+      cb[g * ldcb + j] = __ull2double_rn(r);
+    }
+  }
+}
+
+// K3: compress_outer_cols, gemm.hpp:145-158: word (i, h) = sum_s b[i][h e + s] Q^s.
+template <typename TIn>
+__global__ void k_pack_outer_cols(const TIn* __restrict__ b, size_t rows, size_t cols, size_t ldb,
+                                  int t, int e, double* __restrict__ cb, size_t ldcb) {
+  const size_t H = (cols + e - 1) / e;
+  for (size_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const TIn* row = b + i * ldb;
+    for (size_t h = blockIdx.x * (size_t)blockDim.x + threadIdx.x; h < H;
+         h += (size_t)gridDim.x * blockDim.x) {
+      const size_t base = h * e;
+      const int len = (int)((cols - base) < (size_t)e ? (cols - base) : (size_t)e);
+      uint64_t r = 0;
+      for (int s = len - 1; s >= 0; --s) r = (r << t) | residue_bits(row[base + s]);
+      cb[i * ldcb + h] = __ull2double_rn(r);
+    }
+  }
+}
+
+// redq over a buffer, pack.hpp:124-137: every base-Q digit replaced by itself
+// mod p. A word outside [0, 2^(t e)) raises the DigitOverflow flag.
+__global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint32_t p,
+                       int* __restrict__ overflow) {
+  const int total_bits = t * e;
+  const double limit = (double)(1ull << total_bits);
+  const uint64_t mask = (1ull << t) - 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double v = w[i];
+    if (!(v >= 0.0) || !(v < limit)) {
+      atomicExch(overflow, 1);
+      continue;
+    }
+    const uint64_t bits = __double2ull_rz(v);
+    uint64_t r = 0;
+    for (int s = 0; s < total_bits; s += t) r |= (((bits >> s) & mask) % p) << s;
+    w[i] = __ull2double_rn(r);
+  }
+}
+
+// uncompress, gemm.hpp:182-204 (+ extract_all, pack.hpp:104-119): every
+// stored word is split into its digits, each reduced mod p and scattered back
+// to its logical position; positions past the logical shape are dropped.
+__global__ void k_uncompress(const double* __restrict__ w, size_t srows, size_t scols,
+                             size_t lrows, size_t lcols, int t, int e, int slots, int reversed,
+                             int column_axis, uint32_t p, int32_t* __restrict__ out,
+                             int* __restrict__ overflow) {
+  const int total_bits = t * e;
+  const double limit = (double)(1ull << total_bits);
+  const uint64_t mask = (1ull << t) - 1;
+  const size_t count = srows * scols;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < count;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t si = idx / scols, sj = idx % scols;
+    const double v = w[idx];
+    if (!(v >= 0.0) || !(v < limit)) {
+      atomicExch(overflow, 1);
+      continue;
+    }
+    const uint64_t bits = __double2ull_rz(v);
+    for (int s = 0; s < slots; ++s) {
+      const int di = reversed ? slots - 1 - s : s;
+      const uint64_t digit = di < e ? (bits >> (t * di)) & mask : 0;
+      size_t i = si, j = sj;
+      if (column_axis) j = sj * slots + s;
+      else i = si * slots + s;
+      if (i < lrows && j < lcols) out[i * lcols + j] = (int32_t)(digit % p);
+    }
+  }
+}
+
+// reduce_common_entry over a buffer, gemm.hpp:247-250.
+__global__ void k_reduce_common(const double* __restrict__ acc, size_t count, uint32_t qmask,
+                                uint32_t p, int32_t* __restrict__ c) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x)
+    c[i] = (int32_t)(((uint32_t)(__double2ull_rz(acc[i]) & qmask)) % p);
+}
+
+// ---------------------------------------------------------------- launchers
+static unsigned grid1d(size_t work, int threads) {
+  size_t blocks = (work + threads - 1) / threads;
+  const size_t cap = 148 * 16;
+  if (blocks > cap) blocks = cap;
+  return (unsigned)(blocks ? blocks : 1);
+}
+
+// panel_len 0 = one panel of the whole dimension; panel_words 0 = unpadded.
+static Panels make_panels(size_t k, int e, size_t panel_len, size_t panel_words) {
+  Panels pn;
+  pn.k = k;
+  pn.panel_len = (panel_len == 0 || panel_len > k) ? k : panel_len;
+  if (pn.panel_len == 0) pn.panel_len = 1;
+  const size_t words = (pn.panel_len + e - 1) / e;
+  pn.panel_words = (unsigned)(panel_words ? panel_words : words);
+  pn.npanels = (unsigned)((k + pn.panel_len - 1) / pn.panel_len);
+  return pn;
+}
+
+static dim3 grid2d(size_t inner, size_t outer, int threads) {
+  size_t bx = (inner + threads - 1) / threads;
+  if (bx < 1) bx = 1;
+  if (bx > 65535) bx = 65535;
+  size_t by = outer < 65535 ? outer : 65535;
+  if (by < 1) by = 1;
+  return dim3((unsigned)bx, (unsigned)by);
+}
+
+cudaError_t launch_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols,
+                                void* dst, int dtype, cudaStream_t s) {
+  const size_t total = rows * cols;
+  if (total == 0) return cudaSuccess;
+  if (dtype == 0)
+    k_gen_residues<double><<<grid1d(total, 256), 256, 0, s>>>(seed, p, row0, rows, cols, (double*)dst);
+  else
+    k_gen_residues<uint32_t><<<grid1d(total, 256), 256, 0, s>>>(seed, p, row0, rows, cols, (uint32_t*)dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename TIn>
+static cudaError_t pack_dispatch(int kind, const TIn* src, size_t rows, size_t cols, size_t ld,
+                                 int t, int e, double* dst, size_t ldd, size_t panel_len,
+                                 size_t panel_words, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  switch (kind) {
+    case PACK_ROWS_REVERSED: {  // common dimension = cols
+      const Panels pn = make_panels(cols, e, panel_len, panel_words);
+      k_pack_rows_reversed<TIn><<<grid2d((size_t)pn.panel_words * pn.npanels, rows, 128), 128, 0, s>>>(
+          src, rows, ld, t, e, pn, dst, ldd);
+      break;
+    }
+    case PACK_COLS_FORWARD: {  // common dimension = rows
+      const Panels pn = make_panels(rows, e, panel_len, panel_words);
+      k_pack_cols_forward<TIn><<<grid2d(cols, (size_t)pn.panel_words * pn.npanels, 128), 128, 0, s>>>(
+          src, cols, ld, t, e, pn, dst, ldd);
+      break;
+    }
+    case PACK_OUTER_COLS: {
+      const size_t H = (cols + e - 1) / e;
+      k_pack_outer_cols<TIn><<<grid2d(H, rows, 128), 128, 0, s>>>(src, rows, cols, ld, t, e, dst, ldd);
+      break;
+    }
+    case PACK_OUTER_ROWS: {  // compress_outer_rows, gemm.hpp:161-178: forward words down columns
+      const Panels pn = make_panels(rows, e, rows, 0);
+      k_pack_cols_forward<TIn><<<grid2d(cols, (size_t)pn.panel_words, 128), 128, 0, s>>>(
+          src, cols, ld, t, e, pn, dst, ldd);
+      break;
+    }
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(int kind, const void* src, int dtype, size_t rows, size_t cols, size_t ld,
+                        int t, int e, double* dst, size_t ldd, size_t panel_len,
+                        size_t panel_words, cudaStream_t s) {
+  switch (dtype) {
+    case 0: return pack_dispatch<double>(kind, (const double*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
+    case 1: return pack_dispatch<uint32_t>(kind, (const uint32_t*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
+    default: return pack_dispatch<int32_t>(kind, (const int32_t*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
+  }
+}
+
+cudaError_t launch_redq(double* w, size_t count, int t, int e, uint32_t p, int* overflow,
+                        cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  k_redq<<<grid1d(count, 256), 256, 0, s>>>(w, count, t, e, p, overflow);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uncompress(const double* w, size_t srows, size_t scols, size_t lrows,
+                              size_t lcols, int t, int e, int slots, int reversed, int column_axis,
+                              uint32_t p, int32_t* out, int* overflow, cudaStream_t s) {
+  if (lrows * lcols)
+    cudaMemsetAsync(out, 0, lrows * lcols * sizeof(int32_t), s);
+  const size_t count = srows * scols;
+  if (count == 0) return cudaGetLastError();
+  k_uncompress<<<grid1d(count, 256), 256, 0, s>>>(w, srows, scols, lrows, lcols, t, e, slots,
+                                                   reversed, column_axis, p, out, overflow);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_common(const double* acc, size_t count, uint32_t qmask, uint32_t p,
+                                 int32_t* c, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  k_reduce_common<<<grid1d(count, 256), 256, 0, s>>>(acc, count, qmask, p, c);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace qgk

@@ -1,0 +1,298 @@
+// qg_plan.cpp — host planners behind the C ABI (include/qgemm_b200.h).
+//
+// The reference planners (plan.hpp) are restated with identical results:
+// tests/test_plan_parity.py checks them against the reference itself.
+// The GPU planner is new: the reference keeps every partial sum exact by
+// flooring each word product (word.hpp:28-30); a tensor-core contraction
+// accumulates full products in FP64 and rounds, so blocks of the common
+// dimension are sized by the exactness bound "Eq. G":
+//
+//   L_max(Kb) + rho * sum_{j=1..Kb} [ulp(x_max) + ulp(j x_max)] < Q^d,
+//   ulp(Kb x_max) <= Q^d,
+//
+// with rho = 1 (faithful rounding, any order, products not fused) — more
+// conservative than the measured DMMA behaviour (an RN FMA chain in k order,
+// profiles/r01_fp64_probe.log).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/qgemm_b200.h"
+
+using u128 = unsigned __int128;
+
+namespace qg {
+
+bool is_prime(uint64_t n) {  // field.hpp:42-48
+  if (n < 2) return false;
+  if (n % 2 == 0) return n == 2;
+  for (uint64_t f = 3; f * f <= n; f += 2)
+    if (n % f == 0) return false;
+  return true;
+}
+
+static uint64_t pm1sq(uint32_t p) { return uint64_t(p - 1) * (p - 1); }
+
+int minimal_radix_exponent(uint32_t p, uint64_t k) {  // plan.hpp:98-104
+  const u128 bound = u128(k) * pm1sq(p);
+  int t = 1;
+  while ((u128(1) << t) <= bound) ++t;
+  return t;
+}
+
+int word_capacity(int t, int beta) {  // plan.hpp:107-111
+  int e = beta / t;
+  if (e * t == beta) --e;
+  return e;
+}
+
+uint64_t largest_common_dim(uint32_t p, int t) {  // plan.hpp:113-115
+  return ((uint64_t(1) << t) - 1) / pm1sq(p);
+}
+
+static void fill(qg_plan* out, uint32_t p, int t, int e, int beta, double inv_qd) {
+  std::memset(out, 0, sizeof *out);
+  out->p = p;
+  out->t = t;
+  out->e = e;
+  out->d = e - 1;
+  out->beta = beta;
+  out->kmax = largest_common_dim(p, t);
+  out->inv_qd = inv_qd;
+}
+
+static int bitlen(u128 v) {
+  int b = 0;
+  while (v) {
+    ++b;
+    v >>= 1;
+  }
+  return b;
+}
+
+static u128 ulp_of(u128 v) {  // spacing of doubles at v (>= 1 for integers)
+  const int b = bitlen(v);
+  return b > 53 ? (u128(1) << (b - 53)) : u128(1);
+}
+
+// Largest number of packed words whose full-product FP64 accumulation keeps
+// digit d exact (Eq. G). Digits below d are bounded by min(Q-1, Kb n_s (p-1)^2)
+// — carry-free whenever a block holds at most kmax real residues, which the
+// callers enforce separately (Eq. 3).
+uint64_t max_exact_block(uint32_t p, int t, int e) {
+  static std::mutex mu;
+  static std::map<std::tuple<uint32_t, int, int>, uint64_t> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({p, t, e});
+    if (it != cache.end()) return it->second;
+  }
+  const int d = e - 1;
+  const u128 Q = u128(1) << t;
+  const u128 Qd = u128(1) << (t * d);
+  const u128 pm = pm1sq(p);
+  u128 amax = 0;
+  for (int i = 0; i < e; ++i) amax += u128(p - 1) << (t * i);
+  const u128 xmax = amax * amax;  // < 2^106 for t*e <= 53
+  const u128 ulp_x = ulp_of(xmax);
+  u128 err = 0;
+  uint64_t best = 0;
+  const uint64_t cap = uint64_t(1) << 20;
+  for (uint64_t kb = 1; kb <= cap; ++kb) {
+    u128 L = 0;
+    for (int s = 0; s < d; ++s) {
+      const int ns = (s + 1) < (2 * d + 1 - s) ? (s + 1) : (2 * d + 1 - s);
+      u128 ds = u128(kb) * ns * pm;
+      if (ds > Q - 1) ds = Q - 1;
+      L += ds << (t * s);
+    }
+    const u128 smax = u128(kb) * xmax;
+    if (bitlen(smax) > 120) break;
+    err += ulp_of(smax) + ulp_x;
+    if (ulp_of(smax) > Qd) break;
+    if (L + err >= Qd) break;
+    if ((smax >> (t * d)) >= (u128(1) << 63)) break;
+    best = kb;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{p, t, e}] = best;
+  return best;
+}
+
+// Predicted relative cost of a blocked plan: packed words (rounded up to the
+// 4-word DMMA k-step) times a per-block flush overhead measured in words.
+double blocked_cost(uint64_t k, int e, uint64_t kb_words, double flush_words) {
+  const uint64_t K = (k + e - 1) / e;
+  const uint64_t Kpad = (K + 3) / 4 * 4;
+  const uint64_t nblocks = (K + kb_words - 1) / kb_words;
+  return double(Kpad) + flush_words * double(nblocks > 1 ? nblocks : 0);
+}
+
+}  // namespace qg
+
+using namespace qg;
+
+extern "C" {
+
+int qg_abi_version(void) { return QG_ABI_VERSION; }
+
+const char* qg_status_string(int s) {
+  switch (s) {
+    case QG_OK: return "ok";
+    case QG_INVALID_MODULUS: return "InvalidModulus";
+    case QG_NO_COMPRESSION: return "NoCompression";
+    case QG_SLOT_OVERFLOW: return "SlotOverflow";
+    case QG_DIGIT_OVERFLOW: return "DigitOverflow";
+    case QG_DIMENSION_MISMATCH: return "DimensionMismatch";
+    case QG_PLAN_MISMATCH: return "PlanMismatch";
+    case QG_UNSUPPORTED_ALGORITHM: return "UnsupportedAlgorithm";
+    case QG_PARSE_ERROR: return "ParseError";
+    case QG_INVALID_ARGUMENT: return "InvalidArgument";
+    case QG_CUDA_ERROR: return "CudaError";
+    case QG_NCCL_ERROR: return "NcclError";
+    case QG_NOT_EXACT: return "NotExact";
+  }
+  return "unknown";
+}
+
+int qg_plan_compression(uint32_t p, uint64_t k, int beta, int mode, qg_plan* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;  // field.hpp:19-21
+  if (k < 1 || beta < 2) return QG_INVALID_ARGUMENT;     // plan.hpp:128-129
+  const int t = minimal_radix_exponent(p, k);
+  if (t >= beta) return QG_NO_COMPRESSION;  // plan.hpp:132-135
+  const int e_raw = word_capacity(t, beta);
+  const int e = int(uint64_t(e_raw) < k ? uint64_t(e_raw) : k);
+  if (e < 2) return QG_NO_COMPRESSION;  // plan.hpp:138-140
+  fill(out, p, t, e, beta, std::ldexp(1.0, -t * (e - 1)));
+  out->extraction = mode;
+  if (mode == QG_EXTRACT_ADD_HIGH_BITS) {  // plan.hpp:150-157
+    const long double limit = std::exp2l(static_cast<long double>(t) - 1.0L / e);
+    uint64_t km = out->kmax;
+    while (km > 0 && static_cast<long double>(km) * pm1sq(p) >= limit) --km;
+    out->kmax = km;
+  }
+  return QG_OK;
+}
+
+int qg_uncompressed_plan(uint32_t p, uint64_t k, int beta, qg_plan* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1) return QG_INVALID_ARGUMENT;
+  const int t = minimal_radix_exponent(p, k);
+  if (t >= beta) return QG_NO_COMPRESSION;
+  fill(out, p, t, 1, beta, 1.0);
+  return QG_OK;
+}
+
+int qg_plan_packed_axis(uint32_t p, uint64_t k, uint64_t axis_len, int beta, qg_plan* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1 || axis_len < 1) return QG_INVALID_ARGUMENT;
+  const int t = minimal_radix_exponent(p, k);
+  if (t >= beta) return QG_NO_COMPRESSION;
+  const uint64_t cap = uint64_t(word_capacity(t, beta));
+  const int e = int(cap < axis_len ? cap : axis_len);
+  fill(out, p, t, e, beta, std::ldexp(1.0, -t * (e - 1)));
+  return QG_OK;
+}
+
+int qg_choose_panel(uint32_t p, uint64_t k, int beta, uint64_t* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1 || beta < 2) return QG_INVALID_ARGUMENT;
+  int direct_e = 1;
+  qg_plan pl;
+  if (qg_plan_compression(p, k, beta, 0, &pl) == QG_OK) direct_e = pl.e;
+  for (int t = 1; t < beta; ++t) {  // plan.hpp:215-222
+    const uint64_t km = largest_common_dim(p, t);
+    if (km == 0) continue;
+    const uint64_t panel = km < k ? km : k;
+    const uint64_t cap = uint64_t(word_capacity(t, beta));
+    const int e = int(cap < panel ? cap : panel);
+    if (e > direct_e) {
+      *out = panel;
+      return QG_OK;
+    }
+  }
+  *out = 0;
+  return QG_OK;
+}
+
+int qg_max_exact_block(const qg_plan* plan, uint64_t* words) {
+  if (!plan || !words) return QG_INVALID_ARGUMENT;
+  if (plan->p < 2 || !is_prime(plan->p)) return QG_INVALID_MODULUS;
+  if (plan->e < 1 || plan->t < 1 || plan->t * plan->e > 53) return QG_PLAN_MISMATCH;
+  *words = max_exact_block(plan->p, plan->t, plan->e);
+  return QG_OK;
+}
+
+int qg_gpu_plan_from(const qg_plan* plan, uint64_t k, qg_gpu_plan* out) {
+  if (!plan || !out) return QG_INVALID_ARGUMENT;
+  if (plan->p < 2 || !is_prime(plan->p)) return QG_INVALID_MODULUS;
+  if (plan->e < 1 || plan->t < 1 || plan->t * plan->e > 53 || plan->beta > 53)
+    return QG_PLAN_MISMATCH;
+  std::memset(out, 0, sizeof *out);
+  out->plan = *plan;
+  const uint64_t exact = max_exact_block(plan->p, plan->t, plan->e);
+  out->max_exact_words = exact;
+  const uint64_t K = (k + plan->e - 1) / plan->e;
+  uint64_t kb = exact;
+  // Eq. 3 per block: a block may hold at most kmax real residues. When the
+  // whole common dimension already satisfies it, any blocking does.
+  if (k > plan->kmax) {
+    const uint64_t lim = plan->kmax / uint64_t(plan->e);
+    if (lim < kb) kb = lim;
+  }
+  if (kb >= K) kb = K;  // single block
+  out->kblock_words = kb;
+  return QG_OK;
+}
+
+int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1) return QG_INVALID_ARGUMENT;
+  const double flush_words = 8.0;  // calibrated on B200, DESIGN.md §4
+  double best_cost = 1e300;
+  bool found = false;
+  qg_gpu_plan best;
+  std::memset(&best, 0, sizeof best);
+  for (int t = 1; t < 53; ++t) {
+    const uint64_t km = largest_common_dim(p, t);
+    if (km == 0) continue;
+    const int cap = word_capacity(t, 53);
+    for (int e = 1; e <= cap; ++e) {
+      if (uint64_t(e) > k && e > 1) break;
+      const uint64_t exact = max_exact_block(p, t, e);
+      uint64_t kb = exact;
+      if (k > km) {
+        const uint64_t lim = km / uint64_t(e);
+        if (lim < kb) kb = lim;
+      }
+      const uint64_t K = (k + e - 1) / e;
+      if (kb >= K) kb = K;
+      else kb = kb / 4 * 4;  // multi-block plans flush on the 4-word DMMA k-step
+      if (kb < 4 && kb < K) continue;
+      const uint64_t nblocks = (K + kb - 1) / kb;
+      // digit sums of all blocks must fit the kernel's uint32 accumulator
+      if (u128(nblocks) * ((u128(1) << t) - 1) >= (u128(1) << 32)) continue;
+      const double cost = blocked_cost(k, e, kb, flush_words);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        found = true;
+        fill(&best.plan, p, t, e, 53, std::ldexp(1.0, -t * (e - 1)));
+        best.kblock_words = kb;
+        best.max_exact_words = exact;
+      }
+    }
+  }
+  if (!found) return QG_NO_COMPRESSION;
+  *out = best;
+  return QG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,398 @@
+#!/usr/bin/env python3
+"""bench.py — effective mod-p multiply-adds per second (2mnk/s) of the
+compressed modular GEMM on B200, the BASELINE.json metric.
+
+Workload (N=1): BASELINE config 2 — p=7, m=n=k=4096, dot-product variant
+(Q-adic rows reversed / columns forward, FP64 tensor-core contraction,
+per-k-block digit extraction, mod-p accumulation between blocks).
+A "step" = pack A (K1) + pack B (K2) + the fused DMMA contraction/extract/mod-p
+kernel (K4) on device-resident residues (seeded SplitMix64, K0, generated
+once). For N>1 (torchrun) every rank owns m=4096 rows of A and C (weak
+scaling); rank 0 packs B and broadcasts the packed CB over NCCL each step.
+
+Keys beyond the base contract:
+  roofline      the contraction kernel's achieved packed FP64 TFLOP/s vs the
+                measured DMMA peak (profiles/r01_fp64_peak.json)
+  cpu_baseline  the reference's own CPU path (oracle/_ref, the unmodified
+                reference headers) timed on this host's cores on a row sample
+  e2e           the same metric through the public host-buffer API
+                (mul_common_compressed_host: H2D of A,B + kernels + D2H of C)
+``--impl reference`` runs only the reference CPU arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (p, m, k, n, description)
+    "config1": (3, 512, 512, 512, "config1: p=3 m=n=k=512 dot-product variant"),
+    "config2": (7, 4096, 4096, 4096, "config2: p=7 m=n=k=4096 dot-product variant, k-blocked"),
+    "config3": (3, 8192, 256, 8192, "config3: p=3 m=n=8192 k=256 dot-product variant"),
+    "config5": (3, 32768, 32768, 32768, "config5: p=3 m=n=k=32768 dot-product variant, k-blocked"),
+}
+SEED = 42
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and clock-event reasons while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+# ------------------------------------------------------------------ CPU reference
+def reference_cpu_sample(p, m, k, n, target_s=4.0, threads=None, rows=None):
+    """Time the reference's own dot-product path (oracle/_ref: unmodified
+    compress_rows_reversed -> compress_cols_forward -> packed_common_product
+    -> reduce_common_entry, bench.hpp:127-146) at its own plan on a row
+    sample of the seeded workload, rows sharded over host threads.
+    Returns (rate 2*rows*n*k/s, rows, threads, seconds, C rows, plan)."""
+    import ctypes
+
+    import numpy as np
+
+    import oracle
+
+    ref = oracle.REF
+    kind = "reference"
+    threads = threads or host_threads()
+    pl = oracle.Plan()
+    if ref is None:
+        raise RuntimeError("oracle/_ref/libqgref.so is missing (built by __graft_entry__.build())")
+    st = ref.qgref_plan_compression(p, k, 53, 0, ctypes.byref(pl))
+    if st:
+        raise RuntimeError(f"reference plan failed: {st}")
+    b = oracle.random_residue_matrix(k, n, p, SEED + 1)
+
+    def run(r):
+        a = oracle.random_residue_matrix(r, k, p, SEED)
+        c = np.empty((r, n), dtype=np.uint32)
+        mul, conv = ctypes.c_double(), ctypes.c_double()
+        t0 = time.perf_counter()
+        st = ref.qgref_mul_common(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
+                                  r, k, n, c.ctypes.data_as(ctypes.c_void_p), threads, ctypes.byref(mul), ctypes.byref(conv))
+        dt = time.perf_counter() - t0
+        if st:
+            raise RuntimeError(f"reference mul_common failed: {st}")
+        return dt, c
+
+    if rows is None:
+        pilot = max(threads, 8)
+        dt, _ = run(pilot)
+        rows = int(min(m, max(threads, pilot * target_s / max(dt, 1e-3))))
+        rows = max(threads, rows // threads * threads) if rows >= threads else rows
+    dt, c = run(rows)
+    return 2.0 * rows * n * k / dt, rows, threads, dt, c, pl, kind
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_arm(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    p, m, k, n, desc = CONFIGS[args.config]
+    rates, rows_used, thr = [], None, host_threads()
+    rows_used = None
+    for i in range(args.warmup + args.steps):
+        rate, rows, thr, dt, _, pl, kind = reference_cpu_sample(p, m, k, n, target_s=args.ref_step_s, rows=rows_used)
+        rows_used = rows
+        if i >= args.warmup:
+            rates.append(rate)
+    value = sum(rates) / len(rates)
+    sample = f"rows 0..{rows_used - 1} of A ({rows_used}x{k}) x B ({k}x{n}), reference plan t={pl.t} e={pl.e}, {thr} threads"
+    line = {
+        "impl": "reference", "metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": value, "unit": "mult-adds/s (2mnk/s)",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * rows_used * n * k / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 seed 42/43)",
+        "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n},
+        "cpu_baseline": {"value": value, "unit": "mult-adds/s (2mnk/s)", "cores": thr, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "mult-adds/s (2mnk/s)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def our_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_0803_1975_b200 as qg
+    from paper_0803_1975_b200.dist import ShardOps, mul_common_sharded
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    p, m_rank, k, n, desc = CONFIGS[args.config]
+    gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
+    pl = gp.plan
+    K = -(-k // pl.e)
+    m_total = m_rank * world
+    row0 = rank * m_rank
+
+    # device-resident seeded inputs (K0): this rank's rows of A, all of B on rank 0
+    a = qg.random_residue_matrix(m_rank, k, p, SEED, row0=row0)
+    b = qg.random_residue_matrix(k, n, p, SEED + 1) if rank == 0 else None
+    ca = torch.empty((m_rank, K), dtype=torch.float64, device=dev)
+    cb = torch.empty((K, n), dtype=torch.float64, device=dev)
+    c = torch.empty((m_rank, n), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    sp = qg._stream
+
+    import ctypes
+
+    plc, gpc = pl._c(), gp._c()
+
+    def pack_rows(a_):
+        qg._check(qg.lib.qg_compress_rows_reversed(ctypes.byref(_bigplan), qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), K, sp()))
+        return ca
+
+    def pack_cols(b_):
+        qg._check(qg.lib.qg_compress_cols_forward(ctypes.byref(_bigplan), qg._ptr(b_), 0, k, n, n, qg._ptr(cb), n, sp()))
+        return cb
+
+    ev = {}
+
+    def contract(ca_, cb_):
+        ev["c0"].record(stream)
+        qg._check(qg.lib.qg_mul_common(ctypes.byref(gpc), qg._ptr(ca_), qg._ptr(cb_), m_rank, n, k, qg._ptr(c), n, sp()))
+        ev["c1"].record(stream)
+        return c
+
+    # packing does not depend on kmax (the k-blocks enforce Eq. 3)
+    _bigplan = qg._Plan(pl.p, pl.t, pl.d, pl.e, pl.beta, max(pl.kmax, k), pl.inv_qd, pl.extraction)
+    ops = ShardOps(pack_rows=pack_rows, pack_cols=pack_cols, empty_cb=lambda shape: cb, contract=contract)
+
+    def step():
+        return mul_common_sharded(a, b, (K, n), ops, rank, world)
+
+    for _ in range(args.warmup):
+        ev["c0"], ev["c1"] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        step()
+    torch.cuda.synchronize()
+
+    step_ms, contract_ms = [], []
+    launches0 = qg.kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # evict L2 between timed steps (outside the events)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev["c0"], ev["c1"] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            step()
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            contract_ms.append(ev["c0"].elapsed_time(ev["c1"]))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    launches = qg.kernel_launches() - launches0
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = 2.0 * m_total * n * k / (ms_per_step * 1e-3)
+
+    # parity spot-check inside the bench: checksum of this rank's C
+    checksum = qg.residue_checksum(c)
+
+    contract_avg = sum(contract_ms) / len(contract_ms)
+    packed_flop = 2.0 * m_rank * n * K  # per launch
+    peak_doc = load_json(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) or {}
+    peak = float(peak_doc.get("dmma_m8n8k4_tflops", 37.09))
+    achieved = packed_flop / (contract_avg * 1e-3) / 1e12
+    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
+    traffic = ncu.get("contraction", {}).get(args.config, {}).get("dram_bytes") if ncu else None
+    roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": qg.last_kernel(), "kernel_ms": round(contract_avg, 4),
+                "share_of_step": round(contract_avg / (sum(step_ms) / len(step_ms)), 4),
+                "peak_source": "measured DMMA.8x8x4 microbenchmark on this pool (profiles/r01_fp64_peak.json); "
+                               "cuBLAS DGEMM 35.7 TF/s",
+                "algorithmic_flop_per_launch": packed_flop}
+
+    line = {
+        "metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": value, "unit": "mult-adds/s (2mnk/s)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
+        "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over NCCL" if world > 1 else ""),
+                   "p": p, "m": m_total, "k": k, "n": n,
+                   "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "source": args.plan},
+                   "l2": "flushed between timed steps (256 MiB write); A,B residues (2x128 MiB f64) exceed the 126 MB L2",
+                   "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
+        "roofline": roofline,
+        "gpu_launches": launches,
+        "checksum_rank0": checksum if rank == 0 else None,
+        "wall_s_timed_region": round(wall, 4),
+    }
+    line["clocks"] = clk.summary()
+
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = e2e_measure(qg, gp, p, m_rank, k, n, args)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rate, rows, thr, dt, c_cpu, rpl, kind = reference_cpu_sample(p, m_rank, k, n, target_s=args.cpu_s)
+            agree = bool(np.array_equal(c[:rows].cpu().numpy().astype(np.uint32), c_cpu))
+            line["cpu_baseline"] = {"value": rate, "unit": "mult-adds/s (2mnk/s)", "cores": thr, "kind": kind,
+                                    "sample": f"rows 0..{rows - 1} of the same A x B ({rows}x{k} x {k}x{n}), reference plan "
+                                              f"t={rpl.t} e={rpl.e}, {dt:.2f} s wall",
+                                    "rows_bit_exact_vs_gpu": agree}
+        except Exception as ex:  # the baseline must not kill the measurement
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_measure(qg, gp, p, m, k, n, args):
+    """Same metric through the public host-buffer API (pinned buffers):
+    H2D of A and B (uint32 ResidueMatrix data), pack + contraction kernels,
+    D2H of C, every step."""
+    import numpy as np
+    import torch
+
+    import oracle  # only to create the seeded host inputs bit-identically
+
+    a = torch.empty((m, k), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    b = torch.empty((k, n), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    c = torch.empty((m, n), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    a[:] = oracle.random_residue_matrix(m, k, p, SEED)
+    b[:] = oracle.random_residue_matrix(k, n, p, SEED + 1)
+    for _ in range(2):
+        qg.mul_common_compressed_host(a, b, gp, out=c)
+    times = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        qg.mul_common_compressed_host(a, b, gp, out=c)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    return {"value": 2.0 * m * n * k / t, "unit": "mult-adds/s (2mnk/s)", "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
+            "d2h_bytes_per_step": int(c.nbytes), "ms_per_step": t * 1e3, "api": "mul_common_compressed_host (qg_host_mul_common_gpu)",
+            "checksum": int(c.astype(np.uint64).sum() & 0xFFFFFFFF)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
+    ap.add_argument("--plan", default="gpu", choices=["gpu", "reference"],
+                    help="gpu: planner-chosen (t, e, kblock); reference: plan_compression's plan")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
+    ap.add_argument("--ref-step-s", type=float, default=2.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

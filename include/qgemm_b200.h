@@ -174,6 +174,10 @@ int qg_uncompress(const qg_plan* plan, qg_orientation o, const double* words,
  * for exactness. Copies in, computes on the current device, copies C out. */
 int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
                        size_t k, size_t n, uint32_t* c);
+/* Same, under an explicit k-blocked GPU plan (qg_plan_gpu): k may exceed
+ * plan.kmax; blocks are packed, contracted and accumulated mod p on device. */
+int qg_host_mul_common_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b,
+                           size_t m, size_t k, size_t n, uint32_t* c);
 /* blocked_accumulate(A, B, plan, kpanel), gemm.hpp:450-489 on HOST data:
  * panels of kpanel residues, each packed under `plan`, mod-p accumulation. */
 int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uint32_t* b,

@@ -162,6 +162,7 @@ def _load():
         "qg_redq": ([P(_Plan), vp, sz, vp], i32),
         "qg_uncompress": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp, vp], i32),
         "qg_host_mul_common": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_common_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_blocked_accumulate": ([P(_Plan), vp, vp, sz, sz, sz, sz, vp], i32),
         "qg_host_mul_right": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
@@ -582,18 +583,26 @@ def _host_u32(x) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(x, dtype=np.uint32))
 
 
-def mul_common_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+def mul_common_compressed_host(a, b, plan: Union[CompressionPlan, GpuPlan], out=None) -> np.ndarray:
     """mul_common_compressed(A, B, plan) on host ResidueMatrix data
-    (uint32 row-major): copies in, runs the kernels, copies C out."""
+    (uint32 row-major): copies in, runs the kernels, copies C out. A GpuPlan
+    (plan_gpu) k-blocks the common dimension past plan.kmax. ``out`` may be a
+    preallocated (pinned) uint32 array."""
     a, b = _host_u32(a), _host_u32(b)
     if a.shape[1] != b.shape[0]:
         raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
     m, k = a.shape
     n = b.shape[1]
-    c = np.empty((m, n), dtype=np.uint32)
-    pl = plan._c()
-    _check(lib.qg_host_mul_common(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
-                                  m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
+    c = np.empty((m, n), dtype=np.uint32) if out is None else out
+    vp = ctypes.c_void_p
+    if isinstance(plan, GpuPlan):
+        g = plan._c()
+        _check(lib.qg_host_mul_common_gpu(ctypes.byref(g), a.ctypes.data_as(vp), b.ctypes.data_as(vp), m, k, n,
+                                          c.ctypes.data_as(vp)))
+    else:
+        pl = plan._c()
+        _check(lib.qg_host_mul_common(ctypes.byref(pl), a.ctypes.data_as(vp), b.ctypes.data_as(vp), m, k, n,
+                                      c.ctypes.data_as(vp)))
     return c
 
 

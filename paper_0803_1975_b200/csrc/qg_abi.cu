@@ -328,15 +328,12 @@ struct DevBuf {
   } while (0)
 }  // namespace
 
-int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m,
                        size_t k, size_t n, uint32_t* c) {
-  int st = check_plan(plan);
-  if (st) return st;
-  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // compress_rows_reversed's check, gemm.hpp:106
-  qg_gpu_plan gp;
-  if ((st = qg_gpu_plan_from(plan, k, &gp))) return st;
+  const qg_plan& pl = gp->plan;
+  int st;
   cudaStream_t s = nullptr;
-  const size_t K = ceil_div(k, plan->e);
+  const size_t K = ceil_div(k, pl.e);
   DevBuf da(s), db(s), dca(s), dcb(s), dc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
@@ -345,13 +342,34 @@ int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b
   QG_TRY(dc.alloc(m * n * 4));
   if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if ((st = qg_compress_rows_reversed(plan, da.p, QG_U32, m, k, k, (double*)dca.p, K, s))) return st;
-  if ((st = qg_compress_cols_forward(plan, db.p, QG_U32, k, n, n, (double*)dcb.p, n, s))) return st;
-  if ((st = qg_mul_common(&gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
+  // packing itself does not depend on kmax; the blocks enforce Eq. 3
+  QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e,
+                          (double*)dca.p, K, 0, 0, s));
+  QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e,
+                          (double*)dcb.p, n, 0, 0, s));
+  if ((st = qg_mul_common(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
     return st;
   if (m * n) QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
   return QG_OK;
+}
+
+int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                       size_t k, size_t n, uint32_t* c) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // compress_rows_reversed's check, gemm.hpp:106
+  qg_gpu_plan gp;
+  if ((st = qg_gpu_plan_from(plan, k, &gp))) return st;
+  return host_common(&gp, a, b, m, k, n, c);
+}
+
+int qg_host_mul_common_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b,
+                           size_t m, size_t k, size_t n, uint32_t* c) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  int st = check_plan(&gplan->plan);
+  if (st) return st;
+  return host_common(gplan, a, b, m, k, n, c);
 }
 
 int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uint32_t* b,

@@ -3,6 +3,7 @@
 // Every computation is a kernel launch on the caller's stream; nothing here
 // computes results on the CPU.
 #include <atomic>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 
@@ -12,6 +13,7 @@
 namespace qg {
 bool is_prime(uint64_t n);
 uint64_t max_exact_block(uint32_t p, int t, int e);
+uint64_t stage_block(uint64_t limit, int* bk);
 }  // namespace qg
 
 namespace qgk {
@@ -59,39 +61,53 @@ struct DeviceFlag {
   }
 };
 
-// The common-variant contraction, dispatched on the block structure: DMMA when
-// every block is provably exact (Eq. G) and spans whole 4-word k-steps, the
-// reference's per-product high-part kernel otherwise. words_per_block_layout:
-// when the words come in padded panels (blocked_accumulate), blocks must not
-// straddle them.
+// The common-variant contraction, dispatched on the block structure. Blocks
+// may always be made shorter than asked (Eq. 3 and Eq. G only get easier), so
+// the DMMA kernel runs with blocks of min(kblock, Eq. G bound) words rounded
+// down to whole pipeline stages; only when that leaves less than one 4-word
+// k-step does the reference's per-product high-part kernel take over.
 int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca, const double* cb,
                size_t ldcb, size_t m, size_t n, size_t K, int32_t* c, size_t ldc, cudaStream_t s) {
   if (m == 0 || n == 0) return QG_OK;
   const uint64_t exact = qg::max_exact_block(pl.p, pl.t, pl.e);
   const uint32_t qmask = (uint32_t)((1ull << pl.t) - 1);
-  const bool single = kblock >= K;
-  uint64_t kb = single ? K : kblock;
-  if (!single && kb > exact) kb = exact;  // smaller blocks are always exact
-  const uint64_t nblocks = single ? 1 : ceil_div(K, kb);
-  const bool dmma_ok = single ? (K <= exact) : (kb >= 4);
-  if (dmma_ok && K > 0) {
-    qgk::DotArgs a;
-    a.ca = ca;
-    a.ldca = ldca;
-    a.cb = cb;
-    a.ldcb = ldcb;
+  uint64_t kb = kblock < K ? kblock : K;
+  if (kb > exact) kb = exact;
+  int bk = 32;
+  uint64_t blk = K;  // words per k-block
+  bool dmma = kb >= K;
+  if (!dmma) {
+    blk = qg::stage_block(kb, &bk);
+    dmma = blk >= 4;
+  }
+  if (dmma) {
+    qgk::GemmArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.lda = ldca;
+    a.b = cb;
+    a.ldb = ldcb;
     a.M = (int)m;
     a.N = (int)n;
-    a.K = (int)K;
-    a.kb_steps = single ? 0 : (int)(kb / 4);
-    a.sh_base = 1075 + pl.t * pl.d;
+    a.kb_stages = blk >= K ? 0 : (int)(blk / bk);
+    a.anchor = std::ldexp(1.0, pl.t * pl.d + 52);
     a.qmask = qmask;
     a.p = pl.p;
-    const unsigned __int128 worst = (unsigned __int128)ceil_div(K, single ? K : (kb / 4) * 4) * qmask;
-    a.reduce_each = worst >= ((unsigned __int128)1 << 32) ? 1 : 0;
     a.c = c;
     a.ldc = ldc;
-    return cuda_status(qgk::launch_dot_dmma(a, s, &g_last_kernel));
+    // digit sums are uint32: split k into launches of at most this many blocks,
+    // each adding its residues onto C (mod p)
+    const uint64_t max_blocks = ((1ull << 32) - 1 - pl.p) / (qmask ? qmask : 1);
+    const uint64_t chunk_words = a.kb_stages ? max_blocks * blk : K;
+    for (uint64_t w0 = 0; w0 < K; w0 += chunk_words) {
+      const uint64_t wn = (K - w0) < chunk_words ? (K - w0) : chunk_words;
+      a.a = ca + w0;
+      a.b = cb + w0 * ldcb;
+      a.K = (int)wn;
+      a.accumulate = w0 > 0;
+      cudaError_t e = qgk::launch_dot_dmma(a, bk, s, &g_last_kernel);
+      if (e) return QG_CUDA_ERROR;
+    }
+    return QG_OK;
   }
   qgk::HighArgs h;
   h.ca = ca;
@@ -102,13 +118,12 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
   h.N = (int)n;
   h.K = (int)K;
   h.inv_qd = pl.inv_qd;
-  h.kb_words = single ? 0 : (int)kblock;
+  h.kb_words = kblock >= K ? 0 : (int)kblock;
   h.qmask = qmask;
   h.p = pl.p;
   h.acc = nullptr;
   h.c = c;
   h.ldc = ldc;
-  (void)nblocks;
   return cuda_status(qgk::launch_dot_highpart(h, s, &g_last_kernel));
 }
 
@@ -250,21 +265,21 @@ static int right_common(const qg_plan* plan, const double* a, size_t lda, const 
   const size_t H = ceil_div(n, plan->e);
   if (m == 0 || H == 0) return QG_OK;
   if (k == 0) return cuda_status(cudaMemsetAsync(cc, 0, m * H * sizeof(double), as_stream(stream)));
-  qgk::RightArgs r;
+  qgk::GemmArgs r;
+  std::memset(&r, 0, sizeof r);
   r.a = a;
   r.lda = lda;
-  r.cb = cbo;
-  r.ldcb = H;
+  r.b = cbo;
+  r.ldb = H;
   r.M = (int)m;
   r.N = (int)H;
   r.K = (int)k;
   r.t = plan->t;
   r.e = plan->e;
   r.p = plan->p;
-  r.redq = redq;
   r.cc = cc;
   r.ldcc = H;
-  return cuda_status(qgk::launch_right_dmma(r, as_stream(stream), &g_last_kernel));
+  return cuda_status(qgk::launch_right_dmma(r, redq != 0, as_stream(stream), &g_last_kernel));
 }
 
 int qg_mul_right(const qg_plan* plan, const double* a, size_t lda, const double* cbo, size_t m,

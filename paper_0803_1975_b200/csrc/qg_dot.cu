@@ -3,41 +3,54 @@
 // sm_100a has no FP64 kind for tcgen05.mma (ptxas rejects .kind::f64), so the
 // FP64 tensor path is the warp-level mma.sync.m8n8k4.f64, which ptxas lowers
 // to SASS DMMA.8x8x4 (37.1 TFLOP/s measured on B200, profiles/r01_*). The
-// operands are staged global -> shared by cp.async (LDGSTS) in a 4-stage
-// ring and fed to DMMA from shared memory; each warp owns a 32x32 tile of
-// the 128x128 CTA tile (16 DMMAs per 4-word k-step).
+// operands are staged global -> shared by cp.async (LDGSTS, zero-filling
+// the ragged edges) in a multi-stage ring and fed to DMMA from shared memory.
+// CTA tile 128x128, 8 warps, each owning a 64x32 tile: 64 FP64 accumulators
+// and 32 DMMAs per 4-word k-step per warp, 12 fragment loads per k-step.
 //
 // K4 (common / dot-product variant, gemm.hpp:210-271 + 450-489): the FP64
-// accumulator holds sum_g CA[i][g] CB[g][j] over one k-block; at the end of
-// every block its base-Q digit d is read straight from the IEEE bits
-// (digit_at) and added to an integer digit sum kept in shared memory; the
-// epilogue reduces mod p and stores int32 C. Exactness of digit d per block
-// is the planner's Eq. G (qg_plan.cpp); the k-block flush replaces the
-// reference's per-product floor (word.hpp:28-30).
+// accumulators hold sum_g CA[i][g] CB[g][j] over one k-block. Blocks end on
+// pipeline-stage boundaries (stage depth BK is a template parameter chosen
+// by the host so that blocks align with stages; no branch sits inside the
+// unrolled DMMA sequence). At a block end every accumulator is added with
+// round-toward-zero to the anchor 2^(td+52): the sum's ulp is then exactly
+// Q^d, so its low mantissa bits ARE floor(acc / Q^d) — one DADD.RZ and one
+// LOP3 per accumulator give digit d, which is added to a uint32 digit sum in
+// registers. The epilogue reduces mod p and stores int32 C. Exactness of
+// digit d per block is the planner's Eq. G (qg_plan.cpp); the k-block flush
+// replaces the reference's per-product floor (word.hpp:28-30).
 //
 // K5 (mixed / right variant, gemm.hpp:285-325): plain exact DGEMM of residues
 // by forward-packed words (every partial sum < Q^e < 2^53) with a fused REDQ
 // epilogue (pack.hpp:124-137).
+#include <cstdio>
+
 #include "qg_kernels.h"
 #include "qg_device.cuh"
 
 namespace qgk {
 
-constexpr int BM = 128, BN = 128, BK = 16;  // CTA tile; BK in words
-constexpr int WM = 32, WN = 32;             // warp tile
+constexpr int BM = 128, BN = 128;  // CTA tile
+constexpr int WM = 64, WN = 32;    // warp tile
 constexpr int WARPS_N = BN / WN;
-constexpr int NWARPS = (BM / WM) * (BN / WN);
-constexpr int NT = NWARPS * 32;  // 512 threads
+constexpr int NT = (BM / WM) * (BN / WN) * 32;  // 256 threads
 constexpr int MI = WM / 8, NI = WN / 8;
-constexpr int NACC = MI * NI * 2;  // accumulators per thread
-constexpr int A_ST = BK + 4;       // padded smem row strides (conflict-free fragments)
-constexpr int B_ST = BN + 4;
-constexpr int A_TILE = BM * A_ST;
-constexpr int B_TILE = BK * B_ST;
-constexpr int STAGE_DBL = A_TILE + B_TILE;
-constexpr int STAGES = 4;
-constexpr size_t SMEM_PIPE = size_t(STAGES) * STAGE_DBL * sizeof(double);
-constexpr size_t SMEM_DIGITS = size_t(NACC) * NT * sizeof(uint32_t);
+constexpr int B_ST = BN + 4;  // 132 words = 1056 B = 32 mod 128: conflict-free B fragments
+constexpr int SMEM_BUDGET = 220 * 1024;
+
+// Stage geometry for a stage depth of BK words. The A row stride is the
+// smallest s >= BK with s = 4 (mod 16) words (32 mod 128 bytes), which makes
+// the A-fragment loads conflict-free.
+template <int BK>
+struct Geo {
+  static constexpr int A_ST = BK + ((4 - BK) % 16 + 16) % 16;
+  static constexpr int A_TILE = BM * A_ST;
+  static constexpr int B_TILE = BK * B_ST;
+  static constexpr int STAGE = A_TILE + B_TILE;  // doubles
+  static constexpr int STAGES_RAW = SMEM_BUDGET / (STAGE * 8);
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -60,11 +73,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // One pipeline stage: A rows [m0, m0+BM) x words [k0, k0+BK), B words
 // [k0, k0+BK) x cols [n0, n0+BN). Out-of-range elements are zero-filled by
 // cp.async's src-size operand, so partial tiles contribute nothing.
-template <int VEC>
+template <int BK, int VEC>
 __device__ __forceinline__ void load_stage(double* sA, double* sB, const double* __restrict__ A,
                                            size_t lda, const double* __restrict__ B, size_t ldb,
                                            int m0, int n0, int k0, int M, int N, int K, int tid) {
-  constexpr int A_CPR = BK / VEC;  // chunks per A row
+  using G = Geo<BK>;
+  constexpr int A_CPR = BK / VEC;
   constexpr int A_CH = BM * A_CPR;
 #pragma unroll
   for (int c = tid; c < A_CH; c += NT) {
@@ -76,8 +90,8 @@ __device__ __forceinline__ void load_stage(double* sA, double* sB, const double*
       bytes = rem >= VEC ? VEC * 8 : (rem > 0 ? rem * 8 : 0);
     }
     const double* src = bytes ? A + (size_t)gm * lda + gk : A;
-    if (VEC == 2) cp_async16(sA + r * A_ST + kc, src, bytes);
-    else cp_async8(sA + r * A_ST + kc, src, bytes);
+    if (VEC == 2) cp_async16(sA + r * G::A_ST + kc, src, bytes);
+    else cp_async8(sA + r * G::A_ST + kc, src, bytes);
   }
   constexpr int B_CPR = BN / VEC;
   constexpr int B_CH = BK * B_CPR;
@@ -96,119 +110,20 @@ __device__ __forceinline__ void load_stage(double* sA, double* sB, const double*
   }
 }
 
-// Common variant, K4. MULTI: more than one k-block (digit sums in smem).
-template <int VEC, bool MULTI>
-__global__ void __launch_bounds__(NT, 1) k_dot_dmma(DotArgs args) {
-  extern __shared__ __align__(128) double smem[];
-  uint32_t* dsum = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_DBL);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int warp_m = warp / WARPS_N, warp_n = warp % WARPS_N;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int M = args.M, N = args.N, K = args.K;
-
-  double acc[MI][NI][2];
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  if (MULTI) {
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) dsum[q * NT + tid] = 0u;
-  }
-  int cnt = args.kb_steps;
-
-  const int ktiles = (K + BK - 1) / BK;
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles)
-      load_stage<VEC>(smem + s * STAGE_DBL, smem + s * STAGE_DBL + A_TILE, args.ca, args.ldca,
-                      args.cb, args.ldcb, m0, n0, s * BK, M, N, K, tid);
-    cp_async_commit();
-  }
-
-  for (int kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + STAGES - 1;
-      if (nk < ktiles) {
-        const int slot = nk % STAGES;
-        load_stage<VEC>(smem + slot * STAGE_DBL, smem + slot * STAGE_DBL + A_TILE, args.ca,
-                        args.ldca, args.cb, args.ldcb, m0, n0, nk * BK, M, N, K, tid);
-      }
-      cp_async_commit();
-    }
-    const double* sA = smem + (kt % STAGES) * STAGE_DBL;
-    const double* sB = sA + A_TILE;
-    const double* a_base = sA + (warp_m * WM + g) * A_ST + t;
-    const double* b_base = sB + t * B_ST + warp_n * WN + g;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double af[MI], bf[NI];
-#pragma unroll
-      for (int mi = 0; mi < MI; ++mi) af[mi] = a_base[mi * 8 * A_ST + kk * 4];
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) bf[ni] = b_base[kk * 4 * B_ST + ni * 8];
-#pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-      if (MULTI) {
-        if (--cnt == 0) {  // end of a k-block: digit d out, accumulator reset
-          cnt = args.kb_steps;
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int q = (mi * NI + ni) * 2 + h;
-                uint32_t v = dsum[q * NT + tid] + digit_at(acc[mi][ni][h], args.sh_base, args.qmask);
-                if (args.reduce_each) v %= args.p;
-                dsum[q * NT + tid] = v;
-                acc[mi][ni][h] = 0.0;
-              }
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-
-  // Epilogue: last (partial) block's digit + earlier blocks' digits, mod p.
-  const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi) {
-    const int row = m0 + warp_m * WM + mi * 8 + g;
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni) {
-      const int col = n0 + warp_n * WN + ni * 8 + 2 * t;
-      uint32_t r[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t v = digit_at(acc[mi][ni][h], args.sh_base, args.qmask);
-        if (MULTI) {
-          const int q = (mi * NI + ni) * 2 + h;
-          v += args.reduce_each ? modp(dsum[q * NT + tid]) : dsum[q * NT + tid];
-        }
-        r[h] = modp(v);
-      }
-      if (row < M) {
-        int32_t* dst = args.c + (size_t)row * args.ldc + col;
-        if (col + 1 < N && ((((uintptr_t)dst) & 7) == 0)) {
-          *reinterpret_cast<int2*>(dst) = make_int2((int)r[0], (int)r[1]);
-        } else {
-          if (col < N) dst[0] = (int32_t)r[0];
-          if (col + 1 < N) dst[1] = (int32_t)r[1];
-        }
-      }
-    }
-  }
+// digit d of an accumulator: floor(acc / Q^d) mod Q. acc + 2^(td+52) rounded
+// toward zero has ulp exactly Q^d (the planner keeps acc < 2^(td+52)), so
+// its low mantissa bits hold floor(acc / Q^d) with no rounding.
+__device__ __forceinline__ uint32_t block_digit(double acc, double anchor, uint32_t qmask) {
+  return (uint32_t)__double2loint(__dadd_rz(acc, anchor)) & qmask;
 }
 
-// Mixed variant, K5: exact DGEMM + fused REDQ (or raw words).
-template <int VEC>
-__global__ void __launch_bounds__(NT, 1) k_right_dmma(RightArgs args) {
+// EPI_DIGIT: K4 epilogue (int32 C = digit sums mod p). EPI_REDQ: K5 fused
+// REDQ of exact packed sums (pack.hpp:124-137). EPI_RAW: plain words.
+enum { EPI_DIGIT = 0, EPI_REDQ = 1, EPI_RAW = 2 };
+
+template <int BK, int VEC, int EPI, bool MULTI>
+__global__ void __launch_bounds__(NT, 1) k_gemm_dmma(GemmArgs args) {
+  using G = Geo<BK>;
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -217,40 +132,48 @@ __global__ void __launch_bounds__(NT, 1) k_right_dmma(RightArgs args) {
   const int M = args.M, N = args.N, K = args.K;
 
   double acc[MI][NI][2];
+  uint32_t dsum[MI][NI][2];
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc[mi][ni][h] = 0.0;
+        dsum[mi][ni][h] = 0u;
+      }
 
   const int ktiles = (K + BK - 1) / BK;
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < G::STAGES - 1; ++s) {
     if (s < ktiles)
-      load_stage<VEC>(smem + s * STAGE_DBL, smem + s * STAGE_DBL + A_TILE, args.a, args.lda,
-                      args.cb, args.ldcb, m0, n0, s * BK, M, N, K, tid);
+      load_stage<BK, VEC>(smem + s * G::STAGE, smem + s * G::STAGE + G::A_TILE, args.a, args.lda,
+                          args.b, args.ldb, m0, n0, s * BK, M, N, K, tid);
     cp_async_commit();
   }
+
+  int kst = 0;
   for (int kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<G::STAGES - 2>();
     __syncthreads();
     {
-      const int nk = kt + STAGES - 1;
+      const int nk = kt + G::STAGES - 1;
       if (nk < ktiles) {
-        const int slot = nk % STAGES;
-        load_stage<VEC>(smem + slot * STAGE_DBL, smem + slot * STAGE_DBL + A_TILE, args.a,
-                        args.lda, args.cb, args.ldcb, m0, n0, nk * BK, M, N, K, tid);
+        const int slot = nk % G::STAGES;
+        load_stage<BK, VEC>(smem + slot * G::STAGE, smem + slot * G::STAGE + G::A_TILE, args.a,
+                            args.lda, args.b, args.ldb, m0, n0, nk * BK, M, N, K, tid);
       }
       cp_async_commit();
     }
-    const double* sA = smem + (kt % STAGES) * STAGE_DBL;
-    const double* sB = sA + A_TILE;
-    const double* a_base = sA + (warp_m * WM + g) * A_ST + t;
+    const double* sA = smem + (kt % G::STAGES) * G::STAGE;
+    const double* sB = sA + G::A_TILE;
+    const double* a_base = sA + (warp_m * WM + g) * G::A_ST + t;
     const double* b_base = sB + t * B_ST + warp_n * WN + g;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double af[MI], bf[NI];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) af[mi] = a_base[mi * 8 * A_ST + kk * 4];
+      for (int mi = 0; mi < MI; ++mi) af[mi] = a_base[mi * 8 * G::A_ST + kk * 4];
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) bf[ni] = b_base[kk * 4 * B_ST + ni * 8];
 #pragma unroll
@@ -258,11 +181,23 @@ __global__ void __launch_bounds__(NT, 1) k_right_dmma(RightArgs args) {
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
     }
+    if (MULTI) {
+      if (++kst == args.kb_stages) {  // end of a k-block: digit d out, accumulators reset
+        kst = 0;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              dsum[mi][ni][h] += block_digit(acc[mi][ni][h], args.anchor, args.qmask);
+              acc[mi][ni][h] = 0.0;
+            }
+      }
+    }
   }
   cp_async_wait<0>();
 
-  const int tb = args.t * args.e;
-  const uint64_t mask = (1ull << args.t) - 1;
   const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi) {
@@ -271,17 +206,36 @@ __global__ void __launch_bounds__(NT, 1) k_right_dmma(RightArgs args) {
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) {
       const int col = n0 + warp_n * WN + ni * 8 + 2 * t;
+      if (EPI == EPI_DIGIT) {
+        int32_t* dst = args.c + (size_t)row * args.ldc + col;
+        uint32_t r[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (col + h >= N) continue;
-        double w = acc[mi][ni][h];
-        if (args.redq) {  // redq, pack.hpp:124-137 (every partial sum exact, < Q^e)
-          const uint64_t bits = __double2ull_rz(w);
-          uint64_t r = 0;
-          for (int s = 0; s < tb; s += args.t) r |= (uint64_t)modp((uint32_t)((bits >> s) & mask)) << s;
-          w = __ull2double_rn(r);
+        for (int h = 0; h < 2; ++h) {
+          uint32_t v = block_digit(acc[mi][ni][h], args.anchor, args.qmask) + dsum[mi][ni][h];
+          if (args.accumulate && col + h < N) v += (uint32_t)dst[h];
+          r[h] = modp(v);
         }
-        args.cc[(size_t)row * args.ldcc + col + h] = w;
+        if (col + 1 < N && ((((uintptr_t)dst) & 7) == 0)) {
+          *reinterpret_cast<int2*>(dst) = make_int2((int)r[0], (int)r[1]);
+        } else {
+          if (col < N) dst[0] = (int32_t)r[0];
+          if (col + 1 < N) dst[1] = (int32_t)r[1];
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (col + h >= N) continue;
+          double w = acc[mi][ni][h];
+          if (EPI == EPI_REDQ) {  // redq, pack.hpp:124-137 (every partial sum exact, < Q^e)
+            const uint64_t bits = __double2ull_rz(w);
+            const uint64_t mask = (1ull << args.t) - 1;
+            uint64_t r = 0;
+            for (int s = 0; s < args.t * args.e; s += args.t)
+              r |= (uint64_t)modp((uint32_t)((bits >> s) & mask)) << s;
+            w = __ull2double_rn(r);
+          }
+          args.cc[(size_t)row * args.ldcc + col + h] = w;
+        }
       }
     }
   }
@@ -362,63 +316,53 @@ __global__ void __launch_bounds__(HT) k_dot_highpart(HighArgs args) {
 }
 
 // ---------------------------------------------------------------- launchers
-template <typename Kern>
-static cudaError_t prep(Kern k, size_t smem) {
-  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-cudaError_t launch_dot_dmma(const DotArgs& a, cudaStream_t s, const char** variant) {
-  if (a.M == 0 || a.N == 0) return cudaSuccess;
-  const bool vec2 = (a.ldca % 2 == 0) && (a.ldcb % 2 == 0) && ((((uintptr_t)a.ca) & 15) == 0) &&
-                    ((((uintptr_t)a.cb) & 15) == 0);
-  const bool multi = a.kb_steps > 0;
+template <int BK, int VEC, int EPI, bool MULTI>
+static cudaError_t launch_one(const GemmArgs& a, cudaStream_t s) {
+  using G = Geo<BK>;
+  auto k = k_gemm_dmma<BK, VEC, EPI, MULTI>;
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+  if (err) return err;
   const dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
-  const size_t smem = SMEM_PIPE + (multi ? SMEM_DIGITS : 0);
-  cudaError_t err;
-  if (vec2 && multi) {
-    err = prep(k_dot_dmma<2, true>, smem);
-    if (err) return err;
-    k_dot_dmma<2, true><<<grid, NT, smem, s>>>(a);
-    *variant = "dot_dmma_v2_multiblock";
-  } else if (vec2) {
-    err = prep(k_dot_dmma<2, false>, smem);
-    if (err) return err;
-    k_dot_dmma<2, false><<<grid, NT, smem, s>>>(a);
-    *variant = "dot_dmma_v2_singleblock";
-  } else if (multi) {
-    err = prep(k_dot_dmma<1, true>, smem);
-    if (err) return err;
-    k_dot_dmma<1, true><<<grid, NT, smem, s>>>(a);
-    *variant = "dot_dmma_v1_multiblock";
-  } else {
-    err = prep(k_dot_dmma<1, false>, smem);
-    if (err) return err;
-    k_dot_dmma<1, false><<<grid, NT, smem, s>>>(a);
-    *variant = "dot_dmma_v1_singleblock";
-  }
+  k<<<grid, NT, G::SMEM, s>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_right_dmma(const RightArgs& a, cudaStream_t s, const char** variant) {
-  if (a.M == 0 || a.N == 0) return cudaSuccess;
-  const bool vec2 = (a.lda % 2 == 0) && (a.ldcb % 2 == 0) && ((((uintptr_t)a.a) & 15) == 0) &&
-                    ((((uintptr_t)a.cb) & 15) == 0);
-  const dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
-  cudaError_t err;
-  if (vec2) {
-    err = prep(k_right_dmma<2>, SMEM_PIPE);
-    if (err) return err;
-    k_right_dmma<2><<<grid, NT, SMEM_PIPE, s>>>(a);
-    *variant = "right_dmma_v2";
-  } else {
-    err = prep(k_right_dmma<1>, SMEM_PIPE);
-    if (err) return err;
-    k_right_dmma<1><<<grid, NT, SMEM_PIPE, s>>>(a);
-    *variant = "right_dmma_v1";
+template <int VEC>
+static cudaError_t launch_digit(const GemmArgs& a, int bk, cudaStream_t s) {
+  if (a.kb_stages == 0) return launch_one<32, VEC, EPI_DIGIT, false>(a, s);
+  switch (bk) {
+    case 32: return launch_one<32, VEC, EPI_DIGIT, true>(a, s);
+    case 28: return launch_one<28, VEC, EPI_DIGIT, true>(a, s);
+    case 24: return launch_one<24, VEC, EPI_DIGIT, true>(a, s);
+    case 16: return launch_one<16, VEC, EPI_DIGIT, true>(a, s);
+    case 8: return launch_one<8, VEC, EPI_DIGIT, true>(a, s);
+    case 4: return launch_one<4, VEC, EPI_DIGIT, true>(a, s);
   }
-  count_launch();
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
+}
+
+static bool vec2_ok(const GemmArgs& a) {
+  return (a.lda % 2 == 0) && (a.ldb % 2 == 0) && ((((uintptr_t)a.a) & 15) == 0) &&
+         ((((uintptr_t)a.b) & 15) == 0);
+}
+
+cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
+  if (a.M == 0 || a.N == 0) return cudaSuccess;
+  static thread_local char name[64];
+  const bool v2 = vec2_ok(a);
+  snprintf(name, sizeof name, "dot_dmma_bk%d_%s_v%d", a.kb_stages ? bk : 32,
+           a.kb_stages ? "multiblock" : "singleblock", v2 ? 2 : 1);
+  *variant = name;
+  return v2 ? launch_digit<2>(a, bk, s) : launch_digit<1>(a, bk, s);
+}
+
+cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant) {
+  if (a.M == 0 || a.N == 0) return cudaSuccess;
+  const bool v2 = vec2_ok(a);
+  *variant = redq ? (v2 ? "right_dmma_redq_v2" : "right_dmma_redq_v1") : (v2 ? "right_dmma_raw_v2" : "right_dmma_raw_v1");
+  if (redq) return v2 ? launch_one<32, 2, EPI_REDQ, false>(a, s) : launch_one<32, 1, EPI_REDQ, false>(a, s);
+  return v2 ? launch_one<32, 2, EPI_RAW, false>(a, s) : launch_one<32, 1, EPI_RAW, false>(a, s);
 }
 
 cudaError_t launch_dot_highpart(const HighArgs& a, cudaStream_t s, const char** variant) {

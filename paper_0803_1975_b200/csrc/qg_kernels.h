@@ -24,39 +24,29 @@ cudaError_t launch_uncompress(const double* w, size_t srows, size_t scols, size_
 cudaError_t launch_reduce_common(const double* acc, size_t count, uint32_t qmask, uint32_t p,
                                  int32_t* c, cudaStream_t s);
 
-// Tensor-core (DMMA) contraction of CA (M x K words) by CB (K x N words) with
-// per-k-block digit extraction and a mod-p int32 epilogue.
-struct DotArgs {
-  const double* ca;
-  size_t ldca;
-  const double* cb;
-  size_t ldcb;
-  int M, N, K;          // K = packed words
-  int kb_steps;         // 4-word k-steps per block; 0 = single block
-  int sh_base;          // 1075 + t*d
-  uint32_t qmask;       // Q - 1
-  uint32_t p;
-  int reduce_each;      // reduce digit sums mod p at every flush (huge k)
-  int32_t* c;
-  size_t ldc;
-};
-cudaError_t launch_dot_dmma(const DotArgs& a, cudaStream_t s, const char** variant);
-
-// Mixed variant: CC = A (M x K residues as double) x CBo (K x N words); epilogue
-// REDQ (redq=1) or raw words (redq=0).
-struct RightArgs {
+// Tensor-core (DMMA) contraction C = A (M x K words) x B (K x N words).
+// Common variant (launch_dot_dmma): k-blocks of kb_stages pipeline stages of
+// `bk` words each, per-block digit extraction, mod-p int32 epilogue
+// (accumulate: add the existing C first). Mixed variant (launch_right_dmma):
+// exact sums, fused REDQ (redq) or raw words.
+struct GemmArgs {
   const double* a;
   size_t lda;
-  const double* cb;
-  size_t ldcb;
+  const double* b;
+  size_t ldb;
   int M, N, K;
-  int t, e;
-  uint32_t p;
-  int redq;
+  int kb_stages;        // stages per k-block; 0 = single block
+  double anchor;        // 2^(t d + 52)
+  uint32_t qmask, p;
+  int accumulate;
+  int32_t* c;
+  size_t ldc;
+  int t, e;             // REDQ digit geometry
   double* cc;
   size_t ldcc;
 };
-cudaError_t launch_right_dmma(const RightArgs& a, cudaStream_t s, const char** variant);
+cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
+cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
 
 // Reference high-part semantics (word.hpp:28-30): acc += trunc(a*b*2^-td).
 struct HighArgs {

@@ -114,7 +114,8 @@ uint64_t max_exact_block(uint32_t p, int t, int e) {
     err += ulp_of(smax) + ulp_x;
     if (ulp_of(smax) > Qd) break;
     if (L + err >= Qd) break;
-    if ((smax >> (t * d)) >= (u128(1) << 63)) break;
+    // digit extraction adds 2^(td+52) with round-toward-zero: needs H < 2^52
+    if ((smax >> (t * d)) >= (u128(1) << 52)) break;
     best = kb;
   }
   std::lock_guard<std::mutex> lk(mu);
@@ -122,13 +123,41 @@ uint64_t max_exact_block(uint32_t p, int t, int e) {
   return best;
 }
 
-// Predicted relative cost of a blocked plan: packed words (rounded up to the
-// 4-word DMMA k-step) times a per-block flush overhead measured in words.
+// The contraction kernel flushes k-blocks at pipeline-stage boundaries; a
+// stage holds BK in {4, 8, 16, 24, 28, 32} words. Largest block (in words)
+// of the form BK * j not above `limit`; *bk gets the stage depth used.
+uint64_t stage_block(uint64_t limit, int* bk) {
+  static const int kBK[] = {32, 28, 24, 16, 8, 4};
+  uint64_t best = 0;
+  int best_bk = 0;
+  if (limit >= 64) {  // long blocks: deepest stage, flush cost is amortised anyway
+    best_bk = 32;
+    best = limit / 32 * 32;
+  } else {
+    for (int b : kBK) {  // descending, so ties keep the deeper stage
+      if (uint64_t(b) > limit) continue;
+      const uint64_t blk = limit / b * b;
+      if (blk > best) {
+        best = blk;
+        best_bk = b;
+      }
+    }
+  }
+  if (bk) *bk = best_bk;
+  return best;
+}
+
+// Predicted relative cost of a blocked plan: packed words rounded up to the
+// stage depth, plus a per-block flush overhead measured in words.
 double blocked_cost(uint64_t k, int e, uint64_t kb_words, double flush_words) {
   const uint64_t K = (k + e - 1) / e;
-  const uint64_t Kpad = (K + 3) / 4 * 4;
-  const uint64_t nblocks = (K + kb_words - 1) / kb_words;
-  return double(Kpad) + flush_words * double(nblocks > 1 ? nblocks : 0);
+  if (kb_words >= K) return double((K + 15) / 16 * 16);
+  int bk = 4;
+  const uint64_t blk = stage_block(kb_words, &bk);
+  if (blk == 0) return 1e300;
+  const uint64_t Kpad = (K + bk - 1) / bk * bk;
+  const uint64_t nblocks = (K + blk - 1) / blk;
+  return double(Kpad) + flush_words * double(nblocks);
 }
 
 }  // namespace qg
@@ -256,7 +285,7 @@ int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
   if (!out) return QG_INVALID_ARGUMENT;
   if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
   if (k < 1) return QG_INVALID_ARGUMENT;
-  const double flush_words = 8.0;  // calibrated on B200, DESIGN.md §4
+  const double flush_words = 2.0;  // per-block overhead in packed words
   double best_cost = 1e300;
   bool found = false;
   qg_gpu_plan best;
@@ -275,8 +304,8 @@ int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
       }
       const uint64_t K = (k + e - 1) / e;
       if (kb >= K) kb = K;
-      else kb = kb / 4 * 4;  // multi-block plans flush on the 4-word DMMA k-step
-      if (kb < 4 && kb < K) continue;
+      else kb = stage_block(kb, nullptr);  // multi-block plans flush at stage ends
+      if (kb == 0 || (kb < 4 && kb < K)) continue;
       const uint64_t nblocks = (K + kb - 1) / kb;
       // digit sums of all blocks must fit the kernel's uint32 accumulator
       if (u128(nblocks) * ((u128(1) << t) - 1) >= (u128(1) << 32)) continue;

@@ -78,6 +78,10 @@ static u128 ulp_of(u128 v) {  // spacing of doubles at v (>= 1 for integers)
   return b > 53 ? (u128(1) << (b - 53)) : u128(1);
 }
 
+// Largest rounding error of one FP64 operation whose exact result is the
+// integer v: zero while v < 2^53 (integers there are representable).
+static u128 round_err(u128 v) { return bitlen(v) > 53 ? ulp_of(v) : u128(0); }
+
 // Largest number of packed words whose full-product FP64 accumulation keeps
 // digit d exact (Eq. G). Digits below d are bounded by min(Q-1, Kb n_s (p-1)^2)
 // — carry-free whenever a block holds at most kmax real residues, which the
@@ -97,7 +101,7 @@ uint64_t max_exact_block(uint32_t p, int t, int e) {
   u128 amax = 0;
   for (int i = 0; i < e; ++i) amax += u128(p - 1) << (t * i);
   const u128 xmax = amax * amax;  // < 2^106 for t*e <= 53
-  const u128 ulp_x = ulp_of(xmax);
+  const u128 err_x = round_err(xmax);
   u128 err = 0;
   uint64_t best = 0;
   const uint64_t cap = uint64_t(1) << 20;
@@ -111,7 +115,7 @@ uint64_t max_exact_block(uint32_t p, int t, int e) {
     }
     const u128 smax = u128(kb) * xmax;
     if (bitlen(smax) > 120) break;
-    err += ulp_of(smax) + ulp_x;
+    err += round_err(smax) + err_x;
     if (ulp_of(smax) > Qd) break;
     if (L + err >= Qd) break;
     // digit extraction adds 2^(td+52) with round-toward-zero: needs H < 2^52
@@ -147,17 +151,32 @@ uint64_t stage_block(uint64_t limit, int* bk) {
   return best;
 }
 
-// Predicted relative cost of a blocked plan: packed words rounded up to the
-// stage depth, plus a per-block flush overhead measured in words.
+// Predicted relative cost of a blocked plan, in packed-word units: words
+// rounded up to the stage depth times the stage's per-word overhead, plus a
+// per-block flush cost. Calibrated on B200 with tools/plan_sweep.py
+// (profiles/r01_plan_sweep_*.jsonl): relative to the single-block kernel a
+// flush every stage runs at 0.94 / 0.92 / 0.91 / 0.86 / 0.74 / 0.62 of its
+// speed for BK = 32 / 28 / 24 / 16 / 8 / 4.
+static double stage_cost(int bk) {
+  switch (bk) {
+    case 32: return 1.0;
+    case 28: return 1.01;
+    case 24: return 1.02;
+    case 16: return 1.04;
+    case 8: return 1.1;
+    default: return 1.1;
+  }
+}
+
 double blocked_cost(uint64_t k, int e, uint64_t kb_words, double flush_words) {
   const uint64_t K = (k + e - 1) / e;
-  if (kb_words >= K) return double((K + 15) / 16 * 16);
+  if (kb_words >= K) return double((K + 31) / 32 * 32);
   int bk = 4;
   const uint64_t blk = stage_block(kb_words, &bk);
   if (blk == 0) return 1e300;
   const uint64_t Kpad = (K + bk - 1) / bk * bk;
   const uint64_t nblocks = (K + blk - 1) / blk;
-  return double(Kpad) + flush_words * double(nblocks);
+  return double(Kpad) * stage_cost(bk) + flush_words * double(nblocks);
 }
 
 }  // namespace qg

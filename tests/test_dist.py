@@ -1,0 +1,80 @@
+"""Multi-rank path on CPU: world_size-2 gloo run of the row-sharded product
+(paper_0803_1975_b200/dist.py) with the oracle standing in for the kernels.
+Checks the shard geometry, the broadcast of the packed right operand, and
+that the gathered C equals naive_gemm."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_0803_1975_b200.dist import ShardOps, mul_common_sharded, shard_rows
+
+
+def test_shard_rows_cover_exactly():
+    for m in (0, 1, 7, 70, 4096, 32769):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_rows(m, world, r) for r in range(world)]
+            assert sum(rows for _, rows in spans) == m
+            pos = 0
+            for row0, rows in spans:
+                assert row0 == pos
+                pos += rows
+            assert max(r for _, r in spans) - min(r for _, r in spans) <= 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, p, m, k, n):
+    import oracle as O
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = O.plan_compression(p, k)
+        K = -(-k // plan.e)
+        row0, rows = shard_rows(m, world, rank)
+        a_shard = O.random_residue_matrix(rows, k, p, 42, row0=row0)
+        b = O.random_residue_matrix(k, n, p, 43) if rank == 0 else None
+
+        def contract(ca, cb):
+            acc = O.packed_common_product(plan, ca.numpy(), cb.numpy(), k)
+            return torch.from_numpy(((acc.astype(np.uint64) & np.uint64((1 << plan.t) - 1)) % np.uint64(p)).astype(np.int32))
+
+        ops = ShardOps(
+            pack_rows=lambda a: torch.from_numpy(O.compress_rows_reversed(plan, a)),
+            pack_cols=lambda bb: torch.from_numpy(O.compress_cols_forward(plan, bb)),
+            empty_cb=lambda shape: torch.empty(shape, dtype=torch.float64),
+            contract=contract,
+        )
+        c_shard, cb = mul_common_sharded(a_shard, b, (K, n), ops, rank, world)
+        # every rank must hold rank 0's packed words bit for bit
+        want_cb = O.compress_cols_forward(plan, O.random_residue_matrix(k, n, p, 43))
+        assert np.array_equal(cb.numpy().view(np.uint64), want_cb.view(np.uint64))
+        sizes = [shard_rows(m, world, r)[1] for r in range(world)]
+        top = max(sizes)  # gloo gathers equal shapes: pad ragged shards
+        padded = torch.zeros((top, n), dtype=torch.int32)
+        padded[:rows] = c_shard
+        gathered = [torch.empty((top, n), dtype=torch.int32) for _ in sizes] if rank == 0 else None
+        dist.gather(padded, gathered, dst=0)
+        if rank == 0:
+            c = torch.cat([g[:s] for g, s in zip(gathered, sizes)]).numpy().astype(np.uint32)
+            full_a = O.random_residue_matrix(m, k, p, 42)
+            assert np.array_equal(c, O.naive_gemm(p, full_a, O.random_residue_matrix(k, n, p, 43)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p,m,k,n", [(7, 70, 300, 50), (3, 9, 512, 33)])
+def test_row_sharded_world2_gloo(p, m, k, n):
+    mp.spawn(_worker, args=(2, _free_port(), p, m, k, n), nprocs=2, join=True)

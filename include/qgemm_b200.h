@@ -191,6 +191,8 @@ int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
 /* Number of kernels this library launched since load (the bench's
  * gpu_launches evidence). */
 uint64_t qg_kernel_launches(void);
+/* CUDA error string behind the last QG_CUDA_ERROR of this thread. */
+const char* qg_last_error(void);
 /* Name of the contraction kernel variant the last qg_mul_common used. */
 const char* qg_last_kernel(void);
 

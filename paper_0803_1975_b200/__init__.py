@@ -167,6 +167,7 @@ def _load():
         "qg_host_mul_right": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
+        "qg_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -192,7 +193,10 @@ def header_symbols(path: str = HEADER_PATH) -> list:
 def _check(status: int) -> None:
     if status != 0:
         cls = _STATUS.get(status, Error)
-        raise cls(lib.qg_status_string(status).decode())
+        msg = lib.qg_status_string(status).decode()
+        if status == 10:
+            msg += ": " + lib.qg_last_error().decode()
+        raise cls(msg)
 
 
 # ----------------------------------------------------------------- plans

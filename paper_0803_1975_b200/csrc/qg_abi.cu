@@ -24,8 +24,13 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 thread_local const char* g_last_kernel = "none";
+thread_local cudaError_t g_last_cuda_error = cudaSuccess;
 
-int cuda_status(cudaError_t e) { return e == cudaSuccess ? QG_OK : QG_CUDA_ERROR; }
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return QG_OK;
+  g_last_cuda_error = e;
+  return QG_CUDA_ERROR;
+}
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 
@@ -105,7 +110,7 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
       a.K = (int)wn;
       a.accumulate = w0 > 0;
       cudaError_t e = qgk::launch_dot_dmma(a, bk, s, &g_last_kernel);
-      if (e) return QG_CUDA_ERROR;
+      if (e) return cuda_status(e);
     }
     return QG_OK;
   }
@@ -132,6 +137,7 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
 extern "C" {
 
 uint64_t qg_kernel_launches(void) { return qgk::g_launches.load(); }
+const char* qg_last_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 const char* qg_last_kernel(void) { return g_last_kernel; }
 
 int qg_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols, void* dst,
@@ -339,7 +345,7 @@ struct DevBuf {
 #define QG_TRY(x)                       \
   do {                                  \
     cudaError_t e_ = (x);               \
-    if (e_ != cudaSuccess) return QG_CUDA_ERROR; \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
   } while (0)
 }  // namespace
 

@@ -24,6 +24,7 @@
 // by forward-packed words (every partial sum < Q^e < 2^53) with a fused REDQ
 // epilogue (pack.hpp:124-137).
 #include <cstdio>
+#include <cstdlib>
 
 #include "qg_kernels.h"
 #include "qg_device.cuh"
@@ -241,6 +242,234 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_dmma(GemmArgs args) {
   }
 }
 
+// ------------------------------------------------------------------ v3
+// Persistent, barrier-free variant of the same contraction. Shared-memory
+// stages are filled by cp.async.bulk (the TMA engine's bulk-copy path, SASS
+// UBLKCP): every warp issues ~BM/8 + BK/8 row copies of its share of each
+// stage from single lanes and arms the stage's `full` mbarrier with the bytes
+// it expects; consumers wait on `full`, compute, and arrive on `empty`. No
+// __syncthreads in the main loop, no per-thread address arithmetic for the
+// loads, and the next tile's first stages stream in during the current
+// tile's epilogue. Tiles are walked in groups of 8 row panels so the CTAs
+// resident at one time share their CA/CB panels in L2. Requires 16-byte row
+// alignment (even leading dimensions, even K and N); the v2 kernel above
+// covers every other shape.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n QG_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra QG_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
+  constexpr int GROUP = 8;
+  const int per_group = GROUP * tiles_n;
+  const int gid = tile / per_group;
+  const int first_m = gid * GROUP;
+  const int gsz = (tiles_m - first_m) < GROUP ? (tiles_m - first_m) : GROUP;
+  const int r = tile - gid * per_group;
+  tm = first_m + r % gsz;
+  tn = r / gsz;
+}
+
+template <int BK, int EPI, bool MULTI>
+__global__ void __launch_bounds__(NT + 128, 1) k_gemm_bulk(GemmArgs args, int tiles_m, int tiles_n) {
+  using G = Geo<BK>;
+  constexpr int S = G::STAGES;
+  constexpr int NWARPS = NT / 32;  // consumer warps 0..7; warpgroup 2 (warps 8..11) produces
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * G::STAGE);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = args.M, N = args.N, K = args.K;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int ktiles = (K + BK - 1) / BK;
+  const int total_tiles = tiles_m * tiles_n;
+  const int my_tiles = blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const bool nomem = args.debug & 1;  // timing experiment: compute on stale smem
+
+  if (warp >= NWARPS) {
+    // ---------------- producer warpgroup: gives its registers to the consumers
+    // (setmaxnreg); warp 8 fills stage after stage, ahead of the consumers.
+    // Ragged edges: A rows >= M are skipped (they only feed output rows that are
+    // never stored); words >= K are zero-filled.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (nomem || warp != NWARPS) return;
+    uint32_t slot = 0, phase = 0;
+    for (int ts = 0; ts < my_tiles; ++ts) {
+      int tm, tn;
+      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+      const int m0 = tm * BM, n0 = tn * BN;
+      const int mrows = (M - m0) < BM ? (M - m0) : BM;
+      const int ncols = (N - n0) < BN ? (N - n0) : BN;
+      for (int kt = 0; kt < ktiles; ++kt) {
+        mbar_wait(empty + slot, phase ^ 1);
+        const int k0 = kt * BK;
+        const int kval = (K - k0) < BK ? (K - k0) : BK;
+        double* sA = smem + slot * G::STAGE;
+        double* sB = sA + G::A_TILE;
+        if (kval < BK) {  // zero the k tail (generic stores, ordered before the async copies)
+          for (int i = lane; i < BM * (BK - kval); i += 32) {
+            const int r = i / (BK - kval), c = kval + i % (BK - kval);
+            sA[r * G::A_ST + c] = 0.0;
+          }
+          for (int i = lane; i < (BK - kval) * BN; i += 32) sB[(kval + i / BN) * B_ST + i % BN] = 0.0;
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(full + slot, (uint32_t)(mrows * kval + kval * ncols) * 8u);
+        __syncwarp();
+        for (int r = lane; r < mrows; r += 32)
+          bulk_g2s(sA + r * G::A_ST, args.a + (size_t)(m0 + r) * args.lda + k0, (uint32_t)kval * 8u, full + slot);
+        for (int r = lane; r < kval; r += 32)
+          bulk_g2s(sB + r * B_ST, args.b + (size_t)(k0 + r) * args.ldb + n0, (uint32_t)ncols * 8u, full + slot);
+        if (++slot == S) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  const int g = lane >> 2, t = lane & 3;
+  const int warp_m = warp / WARPS_N, warp_n = warp % WARPS_N;
+  double acc[MI][NI][2];
+  uint32_t dsum[MI][NI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc[mi][ni][h] = 0.0;
+        dsum[mi][ni][h] = 0u;
+      }
+
+  const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
+  uint32_t slot = 0, phase = 0;
+  for (int ts = 0; ts < my_tiles; ++ts) {
+    int tm, tn;
+    tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+    const int m0 = tm * BM, n0 = tn * BN;
+    int kst = 0;
+    for (int kt = 0; kt < ktiles; ++kt) {
+      if (!nomem) mbar_wait(full + slot, phase);
+      const double* sA = smem + slot * G::STAGE;
+      const double* sB = sA + G::A_TILE;
+      const double* a_base = sA + (warp_m * WM + g) * G::A_ST + t;
+      const double* b_base = sB + t * B_ST + warp_n * WN + g;
+      if (!(args.debug & 2)) {  // debug bit 1: data delivery alone (no DMMA)
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk) {
+          double af[MI], bf[NI];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) af[mi] = a_base[mi * 8 * G::A_ST + kk * 4];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) bf[ni] = b_base[kk * 4 * B_ST + ni * 8];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == S) {
+        slot = 0;
+        phase ^= 1;
+      }
+      if (MULTI) {
+        if (++kst == args.kb_stages) {
+          kst = 0;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                dsum[mi][ni][h] += block_digit(acc[mi][ni][h], args.anchor, args.qmask);
+                acc[mi][ni][h] = 0.0;
+              }
+        }
+      }
+    }
+    // epilogue of this tile (the producer is already filling the next tile's stages)
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int row = m0 + warp_m * WM + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const int col = n0 + warp_n * WN + ni * 8 + 2 * t;
+        if (EPI == EPI_DIGIT) {
+          uint32_t r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) r[h] = block_digit(acc[mi][ni][h], args.anchor, args.qmask) + dsum[mi][ni][h];
+          if (row < M && col < N) {  // N even: col < N implies col + 1 < N
+            int32_t* dst = args.c + (size_t)row * args.ldc + col;
+            if (args.accumulate) {
+              const int2 old = *reinterpret_cast<const int2*>(dst);
+              r[0] += (uint32_t)old.x;
+              r[1] += (uint32_t)old.y;
+            }
+            *reinterpret_cast<int2*>(dst) = make_int2((int)modp(r[0]), (int)modp(r[1]));
+          }
+        } else if (row < M && col < N) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double w = acc[mi][ni][h];
+            if (EPI == EPI_REDQ) {
+              const uint64_t bits = __double2ull_rz(w);
+              const uint64_t mask = (1ull << args.t) - 1;
+              uint64_t rr = 0;
+              for (int s2 = 0; s2 < args.t * args.e; s2 += args.t)
+                rr |= (uint64_t)modp((uint32_t)((bits >> s2) & mask)) << s2;
+              w = __ull2double_rn(rr);
+            }
+            args.cc[(size_t)row * args.ldcc + col + h] = w;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          acc[mi][ni][h] = 0.0;
+          dsum[mi][ni][h] = 0u;
+        }
+      }
+    }
+  }
+}
+
 // Reference-semantics contraction (DoubleWord::high_part, word.hpp:28-30):
 // acc[i][j] = sum_g trunc((CA[i][g] 2^-td) CB[g][j]) — the scale is a power
 // of two, so this rounds exactly like the reference's (a*b)*inv_qd. FP64
@@ -316,6 +545,16 @@ __global__ void __launch_bounds__(HT) k_dot_highpart(HighArgs args) {
 }
 
 // ---------------------------------------------------------------- launchers
+// QG_FORCE_CPASYNC=1 forces the v2 (cp.async + __syncthreads) kernels.
+static bool getenv_flag() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QG_FORCE_CPASYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int BK, int VEC, int EPI, bool MULTI>
 static cudaError_t launch_one(const GemmArgs& a, cudaStream_t s) {
   using G = Geo<BK>;
@@ -342,25 +581,80 @@ static cudaError_t launch_digit(const GemmArgs& a, int bk, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BK, int EPI, bool MULTI>
+static cudaError_t launch_bulk(const GemmArgs& a, cudaStream_t s) {
+  using G = Geo<BK>;
+  auto k = k_gemm_bulk<BK, EPI, MULTI>;
+  const size_t smem = G::SMEM + 2 * G::STAGES * sizeof(uint64_t);
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err) return err;
+  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int tiles = tiles_m * tiles_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  GemmArgs a2 = a;
+  const char* dbg = getenv("QG_DEBUG_MODE");
+  a2.debug = dbg ? atoi(dbg) : 0;
+  k<<<grid, NT + 128, smem, s>>>(a2, tiles_m, tiles_n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_digit_bulk(const GemmArgs& a, int bk, cudaStream_t s) {
+  if (a.kb_stages == 0) return launch_bulk<32, EPI_DIGIT, false>(a, s);
+  switch (bk) {
+    case 32: return launch_bulk<32, EPI_DIGIT, true>(a, s);
+    case 28: return launch_bulk<28, EPI_DIGIT, true>(a, s);
+    case 24: return launch_bulk<24, EPI_DIGIT, true>(a, s);
+    case 16: return launch_bulk<16, EPI_DIGIT, true>(a, s);
+    case 8: return launch_bulk<8, EPI_DIGIT, true>(a, s);
+    case 4: return launch_bulk<4, EPI_DIGIT, true>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 static bool vec2_ok(const GemmArgs& a) {
   return (a.lda % 2 == 0) && (a.ldb % 2 == 0) && ((((uintptr_t)a.a) & 15) == 0) &&
          ((((uintptr_t)a.b) & 15) == 0);
+}
+
+// The bulk-copy kernel moves whole 16-byte multiples: rows must start
+// 16-byte aligned and every partial row (K tail, N tail) must be even.
+static bool bulk_ok(const GemmArgs& a, bool digit_out) {
+  return vec2_ok(a) && (a.K % 2 == 0) && (a.N % 2 == 0) &&
+         (!digit_out || ((a.ldc % 2 == 0) && ((((uintptr_t)a.c) & 7) == 0))) && !getenv_flag();
 }
 
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
   static thread_local char name[64];
   const bool v2 = vec2_ok(a);
-  snprintf(name, sizeof name, "dot_dmma_bk%d_%s_v%d", a.kb_stages ? bk : 32,
-           a.kb_stages ? "multiblock" : "singleblock", v2 ? 2 : 1);
+  const bool bulk = bulk_ok(a, true);
+  snprintf(name, sizeof name, "dot_%s_bk%d_%s", bulk ? "bulk" : (v2 ? "cpasync16" : "cpasync8"),
+           a.kb_stages ? bk : 32, a.kb_stages ? "multiblock" : "singleblock");
   *variant = name;
+  if (bulk) return launch_digit_bulk(a, bk, s);
   return v2 ? launch_digit<2>(a, bk, s) : launch_digit<1>(a, bk, s);
 }
 
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
   const bool v2 = vec2_ok(a);
-  *variant = redq ? (v2 ? "right_dmma_redq_v2" : "right_dmma_redq_v1") : (v2 ? "right_dmma_raw_v2" : "right_dmma_raw_v1");
+  const bool bulk = bulk_ok(a, false);
+  if (bulk) {
+    *variant = redq ? "right_bulk_redq" : "right_bulk_raw";
+    return redq ? launch_bulk<32, EPI_REDQ, false>(a, s) : launch_bulk<32, EPI_RAW, false>(a, s);
+  }
+  *variant = redq ? (v2 ? "right_cpasync16_redq" : "right_cpasync8_redq") : (v2 ? "right_cpasync16_raw" : "right_cpasync8_raw");
   if (redq) return v2 ? launch_one<32, 2, EPI_REDQ, false>(a, s) : launch_one<32, 1, EPI_REDQ, false>(a, s);
   return v2 ? launch_one<32, 2, EPI_RAW, false>(a, s) : launch_one<32, 1, EPI_RAW, false>(a, s);
 }

@@ -44,6 +44,7 @@ struct GemmArgs {
   int t, e;             // REDQ digit geometry
   double* cc;
   size_t ldcc;
+  int debug;            // experiments only (QG_DEBUG_MODE)
 };
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);

@@ -197,6 +197,8 @@ def load_json(path):
 def our_arm(args):
     import numpy as np
     import torch
+    import ctypes
+
     import torch.distributed as dist
 
     import paper_0803_1975_b200 as qg
@@ -214,6 +216,8 @@ def our_arm(args):
 
     p, m_rank, k, n, desc = CONFIGS[args.config]
     gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
+    if args.kblock:  # experiments: override the k-block of the chosen plan
+        gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words)
     pl = gp.plan
     K = -(-k // pl.e)
     m_total = m_rank * world
@@ -222,39 +226,39 @@ def our_arm(args):
     # device-resident seeded inputs (K0): this rank's rows of A, all of B on rank 0
     a = qg.random_residue_matrix(m_rank, k, p, SEED, row0=row0)
     b = qg.random_residue_matrix(k, n, p, SEED + 1) if rank == 0 else None
-    ca = torch.empty((m_rank, K), dtype=torch.float64, device=dev)
-    cb = torch.empty((K, n), dtype=torch.float64, device=dev)
+    bk_c = ctypes.c_uint32()
+    gpc = gp._c()
+    qg._check(qg.lib.qg_tiled_stage_words(ctypes.byref(gpc), k, ctypes.byref(bk_c)))
+    bk = bk_c.value
+    # tiled packed layouts (dense zero-padded 128 x bk blocks, CB transposed)
+    ca = torch.empty(qg.lib.qg_tiled_words(m_rank, k, pl.e, bk), dtype=torch.float64, device=dev)
+    cb = torch.empty(qg.lib.qg_tiled_words(n, k, pl.e, bk), dtype=torch.float64, device=dev)
     c = torch.empty((m_rank, n), dtype=torch.int32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
     sp = qg._stream
-
-    import ctypes
-
-    plc, gpc = pl._c(), gp._c()
+    plc = pl._c()
 
     def pack_rows(a_):
-        qg._check(qg.lib.qg_compress_rows_reversed(ctypes.byref(_bigplan), qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), K, sp()))
+        qg._check(qg.lib.qg_pack_a_tiled(ctypes.byref(plc), bk, qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), sp()))
         return ca
 
     def pack_cols(b_):
-        qg._check(qg.lib.qg_compress_cols_forward(ctypes.byref(_bigplan), qg._ptr(b_), 0, k, n, n, qg._ptr(cb), n, sp()))
+        qg._check(qg.lib.qg_pack_b_tiled(ctypes.byref(plc), bk, qg._ptr(b_), 0, k, n, n, qg._ptr(cb), sp()))
         return cb
 
     ev = {}
 
     def contract(ca_, cb_):
         ev["c0"].record(stream)
-        qg._check(qg.lib.qg_mul_common(ctypes.byref(gpc), qg._ptr(ca_), qg._ptr(cb_), m_rank, n, k, qg._ptr(c), n, sp()))
+        qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca_), qg._ptr(cb_), m_rank, n, k, qg._ptr(c), n, sp()))
         ev["c1"].record(stream)
         return c
 
-    # packing does not depend on kmax (the k-blocks enforce Eq. 3)
-    _bigplan = qg._Plan(pl.p, pl.t, pl.d, pl.e, pl.beta, max(pl.kmax, k), pl.inv_qd, pl.extraction)
     ops = ShardOps(pack_rows=pack_rows, pack_cols=pack_cols, empty_cb=lambda shape: cb, contract=contract)
 
     def step():
-        return mul_common_sharded(a, b, (K, n), ops, rank, world)
+        return mul_common_sharded(a, b, tuple(cb.shape), ops, rank, world)
 
     for _ in range(args.warmup):
         ev["c0"], ev["c1"] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -295,7 +299,7 @@ def our_arm(args):
     checksum = qg.residue_checksum(c)
 
     contract_avg = sum(contract_ms) / len(contract_ms)
-    packed_flop = 2.0 * m_rank * n * K  # per launch
+    packed_flop = 2.0 * m_rank * n * K  # per launch: packed words, not padding
     peak_doc = load_json(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) or {}
     peak = float(peak_doc.get("dmma_m8n8k4_tflops", 37.09))
     achieved = packed_flop / (contract_avg * 1e-3) / 1e12
@@ -316,7 +320,9 @@ def our_arm(args):
         "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
         "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over NCCL" if world > 1 else ""),
                    "p": p, "m": m_total, "k": k, "n": n,
-                   "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "source": args.plan},
+                   "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
+                            "source": args.plan},
+                   "layout": "tiled packed operands (128 x stage_words blocks, CB transposed)",
                    "l2": "flushed between timed steps (256 MiB write); A,B residues (2x128 MiB f64) exceed the 126 MB L2",
                    "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
         "roofline": roofline,
@@ -381,6 +387,7 @@ def main():
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
     ap.add_argument("--plan", default="gpu", choices=["gpu", "reference"],
                     help="gpu: planner-chosen (t, e, kblock); reference: plan_compression's plan")
+    ap.add_argument("--kblock", type=int, default=0, help="override the plan's k-block (words)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=2.0)

@@ -149,6 +149,24 @@ int qg_mul_common_repacked(const qg_gpu_plan* gplan, const double* ca, const dou
                            size_t m, size_t n, size_t k, double* cc, int32_t* workspace,
                            void* stream);
 
+/* ---- tiled packed layout (the B200 fast path for the dot-product variant).
+ * The same words as compress_rows_reversed / compress_cols_forward, stored as
+ * dense, zero-padded 128 x BK blocks so that one pipeline stage of the
+ * contraction is one contiguous chunk per operand:
+ *   CA_t[tm][kt][r][c] = CA[128 tm + r][BK kt + c]
+ *   CB_t[tn][kt][r][c] = CB[BK kt + c][128 tn + r]   (B transposed)
+ * qg_tiled_stage_words gives the BK a plan runs with; qg_tiled_words the
+ * buffer size in doubles for `rows` (m for CA_t, n for CB_t). */
+int qg_tiled_stage_words(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk);
+size_t qg_tiled_words(size_t rows, size_t k, int e, uint32_t bk);
+int qg_pack_a_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
+                    size_t lda, double* ca_t, void* stream);
+int qg_pack_b_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+                    size_t ldb, double* cb_t, void* stream);
+/* qg_mul_common on tiled operands (n and ldc even). */
+int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m,
+                        size_t n, size_t k, int32_t* c, size_t ldc, void* stream);
+
 /* packed_right_product + redq_in_place = mul_right_compressed(a, cb),
  * gemm.hpp:285-325: CC = REDQ(A x CBo). A: m x k residues as double (lda),
  * CBo: k x ceil(n/e) words. cc: m x ceil(n/e). */

@@ -165,6 +165,11 @@ def _load():
         "qg_host_mul_common_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_blocked_accumulate": ([P(_Plan), vp, vp, sz, sz, sz, sz, vp], i32),
         "qg_host_mul_right": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_tiled_stage_words": ([P(_GpuPlan), u64, P(u32)], i32),
+        "qg_tiled_words": ([sz, sz, i32, u32], sz),
+        "qg_pack_a_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_b_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_mul_common_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),
@@ -512,6 +517,10 @@ def mul_common_compressed(a_or_ca, b_or_cb, plan: Optional[Union[CompressionPlan
         gp = _as_gpu_plan(plan, a.shape[1])
         base = gp.plan
         k = a.shape[1]
+        if not isinstance(plan, GpuPlan) and k > base.kmax:  # compress_rows_reversed's check
+            raise PlanMismatch(f"common dimension {k} exceeds kmax={base.kmax}")
+        if b.shape[1] % 2 == 0 and not os.environ.get("QG_FORCE_ROW_LAYOUT"):
+            return mul_common_tiled(a, b, gp)
         if isinstance(plan, GpuPlan) and k > base.kmax:
             # blocked plan: pack with a kmax-free plan view (blocks enforce Eq. 3)
             big = dataclasses.replace(base, kmax=max(base.kmax, k))
@@ -523,6 +532,46 @@ def mul_common_compressed(a_or_ca, b_or_cb, plan: Optional[Union[CompressionPlan
     out = torch.empty((m, n), dtype=torch.int32, device=ca.data.device)
     g = gp._c()
     _check(lib.qg_mul_common(ctypes.byref(g), _ptr(ca.data), _ptr(cb.data), m, n, k, _ptr(out), n, _stream()))
+    return out
+
+
+def tiled_stage_words(gp: GpuPlan, k: int) -> int:
+    out = ctypes.c_uint32()
+    g = gp._c()
+    _check(lib.qg_tiled_stage_words(ctypes.byref(g), k, ctypes.byref(out)))
+    return out.value
+
+
+def pack_tiled(a, plan: CompressionPlan, bk: int, operand: str):
+    """Tiled packed layout of A ('a': compress_rows_reversed words) or B
+    ('b': compress_cols_forward words, transposed) as dense zero-padded
+    128 x bk blocks (include/qgemm_b200.h). Returns a flat float64 tensor."""
+    torch = _torch()
+    _require_cuda(a)
+    rows, cols = a.shape
+    pl = plan._c()
+    if operand == "a":
+        out = torch.empty(lib.qg_tiled_words(rows, cols, plan.e, bk), dtype=torch.float64, device=a.device)
+        _check(lib.qg_pack_a_tiled(ctypes.byref(pl), bk, _ptr(a), _dtype_code(a), rows, cols, cols, _ptr(out), _stream()))
+    else:
+        out = torch.empty(lib.qg_tiled_words(cols, rows, plan.e, bk), dtype=torch.float64, device=a.device)
+        _check(lib.qg_pack_b_tiled(ctypes.byref(pl), bk, _ptr(a), _dtype_code(a), rows, cols, cols, _ptr(out), _stream()))
+    return out
+
+
+def mul_common_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]):
+    """mul_common_compressed on residue tensors through the tiled packed
+    layout and the tiled DMMA contraction (n must be even)."""
+    torch = _torch()
+    m, k = a.shape
+    n = b.shape[1]
+    gp = _as_gpu_plan(plan, k)
+    bk = tiled_stage_words(gp, k)
+    ca = pack_tiled(a, gp.plan, bk, "a")
+    cb = pack_tiled(b, gp.plan, bk, "b")
+    out = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    g = gp._c()
+    _check(lib.qg_mul_common_tiled(ctypes.byref(g), _ptr(ca), _ptr(cb), m, n, k, _ptr(out), n, _stream()))
     return out
 
 

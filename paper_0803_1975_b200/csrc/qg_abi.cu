@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/qgemm_b200.h"
@@ -14,6 +15,7 @@ namespace qg {
 bool is_prime(uint64_t n);
 uint64_t max_exact_block(uint32_t p, int t, int e);
 uint64_t stage_block(uint64_t limit, int* bk);
+uint64_t stage_block_tiled(uint64_t limit, int* bk);
 }  // namespace qg
 
 namespace qgk {
@@ -132,9 +134,107 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
   return cuda_status(qgk::launch_dot_highpart(h, s, &g_last_kernel));
 }
 
+// Tiled path: stage depth and blocks for a plan. Single-block plans stream
+// BK = 28 stages (4 in flight); blocked plans use the deepest stage that
+// divides the (Eq. G / Eq. 3) block.
+int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
+  const qg_plan& pl = gp->plan;
+  const uint64_t exact = qg::max_exact_block(pl.p, pl.t, pl.e);
+  uint64_t kb = gp->kblock_words < K ? gp->kblock_words : K;
+  if (kb > exact) kb = exact;
+  if (kb >= K) {
+    const char* e = getenv("QG_TILED_SINGLE_BK");
+    *bk = e ? atoi(e) : 28;
+    *kb_stages = 0;
+    return QG_OK;
+  }
+  const uint64_t blk = qg::stage_block_tiled(kb, bk);
+  if (blk < 4) return QG_NOT_EXACT;
+  *kb_stages = (int)(blk / *bk);
+  return QG_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int qg_tiled_stage_words(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk) {
+  if (!gplan || !bk) return QG_INVALID_ARGUMENT;
+  int st = check_plan(&gplan->plan);
+  if (st) return st;
+  int b = 0, kbs = 0;
+  if ((st = tiled_geometry(gplan, ceil_div(k, gplan->plan.e), &b, &kbs))) return st;
+  *bk = (uint32_t)b;
+  return QG_OK;
+}
+
+size_t qg_tiled_words(size_t rows, size_t k, int e, uint32_t bk) {
+  if (e < 1 || bk == 0) return 0;
+  const size_t K = ceil_div(k, (size_t)e);
+  return ceil_div(rows, 128) * 128 * ceil_div(K, bk) * bk;
+}
+
+int qg_pack_a_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
+                    size_t lda, double* ca_t, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (lda < k) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_tiled(false, a, dtype, m, k, lda, plan->t, plan->e, (int)bk, ca_t,
+                                            as_stream(stream)));
+}
+
+int qg_pack_b_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+                    size_t ldb, double* cb_t, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (ldb < n) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_tiled(true, b, dtype, k, n, ldb, plan->t, plan->e, (int)bk, cb_t,
+                                            as_stream(stream)));
+}
+
+int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,
+                        size_t k, int32_t* c, size_t ldc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if (ldc < n || (ldc % 2) || (n % 2) || ((((uintptr_t)c) & 7) != 0)) return QG_INVALID_ARGUMENT;
+  const size_t K = ceil_div(k, pl.e);
+  const uint64_t kb = gplan->kblock_words;
+  if (kb == 0) return QG_INVALID_ARGUMENT;
+  if (kb < K && kb * (uint64_t)pl.e > pl.kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
+  if (kb >= K && k > pl.kmax) return QG_PLAN_MISMATCH;
+  if (m == 0 || n == 0) return QG_OK;
+  int bk = 0, kbs = 0;
+  if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
+  qgk::GemmArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.a = ca_t;
+  a.b = cb_t;
+  a.M = (int)m;
+  a.N = (int)n;
+  a.K = (int)K;
+  a.kb_stages = kbs;
+  a.anchor = std::ldexp(1.0, pl.t * pl.d + 52);
+  a.qmask = (uint32_t)((1ull << pl.t) - 1);
+  a.p = pl.p;
+  a.c = c;
+  a.ldc = ldc;
+  if (K == 0) {
+    for (size_t i = 0; i < m; ++i)
+      if (cudaMemsetAsync(c + i * ldc, 0, n * sizeof(int32_t), as_stream(stream)) != cudaSuccess) return QG_CUDA_ERROR;
+    return QG_OK;
+  }
+  // digit sums are uint32 (planner keeps nblocks * (Q-1) < 2^32); the fused
+  // flush packs two per register as 16-bit lanes, reduced mod p in time
+  if (pl.t <= 16) a.pack_period = (int)((65535u - (pl.p - 1)) / a.qmask);
+  const uint64_t nblocks = kbs ? ceil_div(K, (size_t)kbs * bk) : 1;
+  if ((unsigned __int128)nblocks * a.qmask + pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+  return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));
+}
+
 
 uint64_t qg_kernel_launches(void) { return qgk::g_launches.load(); }
 const char* qg_last_error(void) { return cudaGetErrorString(g_last_cuda_error); }
@@ -355,21 +455,31 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
   int st;
   cudaStream_t s = nullptr;
   const size_t K = ceil_div(k, pl.e);
+  int bk = 0, kbs = 0;
+  const bool tiled = (n % 2 == 0) && tiled_geometry(gp, K ? K : 1, &bk, &kbs) == QG_OK;
   DevBuf da(s), db(s), dca(s), dcb(s), dc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
-  QG_TRY(dca.alloc(m * K * 8));
-  QG_TRY(dcb.alloc(K * n * 8));
   QG_TRY(dc.alloc(m * n * 4));
   if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  // packing itself does not depend on kmax; the blocks enforce Eq. 3
-  QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e,
-                          (double*)dca.p, K, 0, 0, s));
-  QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e,
-                          (double*)dcb.p, n, 0, 0, s));
-  if ((st = qg_mul_common(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
-    return st;
+  if (tiled) {  // tiled packed layout + the v4 contraction
+    QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
+    QG_TRY(dcb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
+    QG_TRY(qgk::launch_pack_tiled(false, da.p, QG_U32, m, k, k, pl.t, pl.e, bk, (double*)dca.p, s));
+    QG_TRY(qgk::launch_pack_tiled(true, db.p, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, s));
+    if ((st = qg_mul_common_tiled(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
+      return st;
+  } else {  // reference layout: packing itself does not depend on kmax; the blocks enforce Eq. 3
+    QG_TRY(dca.alloc(m * K * 8));
+    QG_TRY(dcb.alloc(K * n * 8));
+    QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e,
+                            (double*)dca.p, K, 0, 0, s));
+    QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e,
+                            (double*)dcb.p, n, 0, 0, s));
+    if ((st = qg_mul_common(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
+      return st;
+  }
   if (m * n) QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
   return QG_OK;

@@ -40,15 +40,29 @@ constexpr int B_ST = BN + 4;  // 132 words = 1056 B = 32 mod 128: conflict-free 
 constexpr int SMEM_BUDGET = 220 * 1024;
 
 // Stage geometry for a stage depth of BK words. The A row stride is the
-// smallest s >= BK with s = 4 (mod 16) words (32 mod 128 bytes), which makes
-// the A-fragment loads conflict-free.
+// smallest s >= BK with s = 4 or 12 (mod 16) words: rows g = 0..3 of a
+// fragment then start 32 bytes apart modulo 128, so the A-fragment loads are
+// conflict-free (BK = 28 and 4 need no padding at all).
 template <int BK>
 struct Geo {
-  static constexpr int A_ST = BK + ((4 - BK) % 16 + 16) % 16;
+  static constexpr int A_ST = (BK % 16 == 4 || BK % 16 == 12) ? BK : (BK % 16 < 4 ? BK - BK % 16 + 4 : (BK % 16 < 12 ? BK - BK % 16 + 12 : BK - BK % 16 + 20));
   static constexpr int A_TILE = BM * A_ST;
   static constexpr int B_TILE = BK * B_ST;
   static constexpr int STAGE = A_TILE + B_TILE;  // doubles
   static constexpr int STAGES_RAW = SMEM_BUDGET / (STAGE * 8);
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
+};
+
+// Tiled-layout geometry (k_gemm_tiled): a stage is one dense 128 x BK block
+// of A and one of B^T, each a single contiguous chunk in HBM. Fragment loads
+// are conflict-free when BK = 4 or 12 (mod 16); BK in {4, 12, 20, 28, 36}.
+template <int BK>
+struct GeoT {
+  static constexpr int A_TILE = BM * BK;
+  static constexpr int STAGE = 2 * BM * BK;  // doubles
+  static constexpr int BUDGET = 232448 - 1024;
+  static constexpr int STAGES_RAW = BUDGET / (STAGE * 8);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
   static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
 };
@@ -69,6 +83,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// D = A * B (C = 0): the first k-step of a new k-block.
+__device__ __forceinline__ void dmma_zc(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(0.0));
 }
 
 // One pipeline stage: A rows [m0, m0+BM) x words [k0, k0+BK), B words
@@ -115,7 +136,14 @@ __device__ __forceinline__ void load_stage(double* sA, double* sB, const double*
 // toward zero has ulp exactly Q^d (the planner keeps acc < 2^(td+52)), so
 // its low mantissa bits hold floor(acc / Q^d) with no rounding.
 __device__ __forceinline__ uint32_t block_digit(double acc, double anchor, uint32_t qmask) {
+#ifdef QG_INT_DIGIT
+  // integer-pipe variant: floor(acc / 2^td) from the IEEE fields; anchor's
+  // exponent field is 1023 + td + 52, so its high word gives the shift base
+  const int sh_base = (int)((unsigned)__double2hiint(anchor) >> 20) - 52 - 1023 + 1075;
+  return digit_at(acc, sh_base, qmask);
+#else
   return (uint32_t)__double2loint(__dadd_rz(acc, anchor)) & qmask;
+#endif
 }
 
 // EPI_DIGIT: K4 epilogue (int32 C = digit sums mod p). EPI_REDQ: K5 fused
@@ -293,6 +321,195 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
   tn = r / gsz;
 }
 
+// Per-output digit sums of finished k-blocks. PACK: two outputs share one
+// register as 16-bit lanes (t <= 16); the caller reduces both lanes mod p
+// every args.pack_period flushes, before a lane could reach 2^16. Saves the
+// 32 registers the fused flush needs.
+template <bool PACK>
+struct DigitSums {
+  uint32_t v[MI][NI][2];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) v[i][j][0] = v[i][j][1] = 0u;
+  }
+  __device__ __forceinline__ void add(int i, int j, uint32_t d0, uint32_t d1) {
+    v[i][j][0] += d0;
+    v[i][j][1] += d1;
+  }
+  __device__ __forceinline__ uint32_t get(int i, int j, int h) const { return v[i][j][h]; }
+  __device__ __forceinline__ void reduce(const ModP&) {}
+};
+template <>
+struct DigitSums<true> {
+  uint32_t v[MI][NI];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) v[i][j] = 0u;
+  }
+  __device__ __forceinline__ void add(int i, int j, uint32_t d0, uint32_t d1) { v[i][j] += d0 + (d1 << 16); }
+  __device__ __forceinline__ uint32_t get(int i, int j, int h) const { return h ? (v[i][j] >> 16) : (v[i][j] & 0xFFFFu); }
+  __device__ __forceinline__ void reduce(const ModP& modp) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) v[i][j] = modp(v[i][j] & 0xFFFFu) | (modp(v[i][j] >> 16) << 16);
+  }
+};
+
+// Consumer side of k_gemm_bulk (TILED = false: padded row layout) and
+// k_gemm_tiled (TILED = true: dense A and B^T blocks). MID = 0: k-blocks end
+// on stage boundaries (every kb_stages stages). MID > 0 (kb_stages == 1 only):
+// blocks end after k-step MID-1 of every stage, i.e. they straddle stages.
+// MID < 0 (kb_stages == 1 only): blocks are stages and the flush is fused
+// into the first k-step of the next stage.
+template <int BK, int EPI, bool MULTI, int MID, bool TILED, bool PACK = false>
+__device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint64_t* full, uint64_t* empty,
+                                        int tiles_m, int tiles_n, int my_tiles, int ktiles, bool nomem) {
+  using G = Geo<BK>;
+  using GT = GeoT<BK>;
+  constexpr int S = TILED ? GT::STAGES : G::STAGES;
+  constexpr int STAGE = TILED ? GT::STAGE : G::STAGE;
+  constexpr int A_TILE = TILED ? GT::A_TILE : G::A_TILE;
+  constexpr int AST = TILED ? BK : G::A_ST;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = args.M, N = args.N;
+  const int g = lane >> 2, t = lane & 3;
+  const int warp_m = warp / WARPS_N, warp_n = warp % WARPS_N;
+  double acc[MI][NI][2];
+  DigitSums<PACK> ds;
+  ds.reset();
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+  const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
+  uint32_t slot = 0, phase = 0;
+  int nflush = 0;
+  if (MULTI && warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise SMSP warp pairs
+  for (int ts = 0; ts < my_tiles; ++ts) {
+    int tm, tn;
+    tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+    const int m0 = tm * BM, n0 = tn * BN;
+    int kst = 0;
+    for (int kt = 0; kt < ktiles; ++kt) {
+      if (!nomem) mbar_wait(full + slot, phase);
+      const double* sA = smem + slot * STAGE;
+      const double* sB = sA + A_TILE;
+      const double* a_base = sA + (warp_m * WM + g) * AST + t;
+      // B^T block (tiled): element (n, k) at n*BK + k; row block: (k, n) at k*B_ST + n
+      const double* b_base = TILED ? sB + (warp_n * WN + g) * BK + t : sB + t * B_ST + warp_n * WN + g;
+      if (!(args.debug & 2)) {  // debug bit 1: data delivery alone (no DMMA)
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk) {
+          double af[MI], bf[NI];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) af[mi] = a_base[mi * 8 * AST + kk * 4];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) bf[ni] = TILED ? b_base[ni * 8 * BK + kk * 4] : b_base[kk * 4 * B_ST + ni * 8];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+              if (MULTI && MID < 0 && kk == 0) {
+                // fused flush (one stage per block): the finished block's digit
+                // d leaves each accumulator right before that accumulator's
+                // first DMMA of the new block (C = 0), so the integer work of
+                // the flush interleaves with DMMAs that keep the pipe busy
+                ds.add(mi, ni, block_digit(acc[mi][ni][0], args.anchor, args.qmask),
+                       block_digit(acc[mi][ni][1], args.anchor, args.qmask));
+                dmma_zc(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+              } else {
+                dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+              }
+            }
+          if (MULTI && MID > 0 && kk == MID - 1) {  // compile-time position: no branch in the DMMA stream
+            asm volatile("" ::: "memory");  // keep the next fragment loads below the flush (register pressure)
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) {
+                ds.add(mi, ni, block_digit(acc[mi][ni][0], args.anchor, args.qmask),
+                       block_digit(acc[mi][ni][1], args.anchor, args.qmask));
+                acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+              }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == S) {
+        slot = 0;
+        phase ^= 1;
+      }
+      if (MULTI && MID == 0) {  // (MID != 0 flushes inside the unrolled k-steps)
+        if (++kst == args.kb_stages) {
+          kst = 0;
+          ++nflush;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+              ds.add(mi, ni, block_digit(acc[mi][ni][0], args.anchor, args.qmask),
+                     block_digit(acc[mi][ni][1], args.anchor, args.qmask));
+              acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+            }
+        }
+      } else if (MULTI) {
+        ++nflush;
+      }
+      if (PACK && nflush >= args.pack_period) {  // keep both 16-bit lanes below 2^16
+        ds.reduce(modp);
+        nflush = 0;
+      }
+    }
+    // epilogue of this tile (the producer is already filling the next tile's stages)
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int row = m0 + warp_m * WM + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const int col = n0 + warp_n * WN + ni * 8 + 2 * t;
+        if (EPI == EPI_DIGIT) {
+          uint32_t r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) r[h] = block_digit(acc[mi][ni][h], args.anchor, args.qmask) + ds.get(mi, ni, h);
+          if (row < M && col < N) {  // N even: col < N implies col + 1 < N
+            int32_t* dst = args.c + (size_t)row * args.ldc + col;
+            if (args.accumulate) {
+              const int2 old = *reinterpret_cast<const int2*>(dst);
+              r[0] += (uint32_t)old.x;
+              r[1] += (uint32_t)old.y;
+            }
+            *reinterpret_cast<int2*>(dst) = make_int2((int)modp(r[0]), (int)modp(r[1]));
+          }
+        } else if (row < M && col < N) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double w = acc[mi][ni][h];
+            if (EPI == EPI_REDQ) {
+              const uint64_t bits = __double2ull_rz(w);
+              const uint64_t mask = (1ull << args.t) - 1;
+              uint64_t rr = 0;
+              for (int s2 = 0; s2 < args.t * args.e; s2 += args.t)
+                rr |= (uint64_t)modp((uint32_t)((bits >> s2) & mask)) << s2;
+              w = __ull2double_rn(rr);
+            }
+            args.cc[(size_t)row * args.ldcc + col + h] = w;
+          }
+        }
+        acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+    }
+    ds.reset();
+    nflush = 0;
+  }
+}
+
 template <int BK, int EPI, bool MULTI>
 __global__ void __launch_bounds__(NT + 128, 1) k_gemm_bulk(GemmArgs args, int tiles_m, int tiles_n) {
   using G = Geo<BK>;
@@ -363,111 +580,81 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_bulk(GemmArgs args, int ti
 
   // ---------------- consumer warps
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-  const int g = lane >> 2, t = lane & 3;
-  const int warp_m = warp / WARPS_N, warp_n = warp % WARPS_N;
-  double acc[MI][NI][2];
-  uint32_t dsum[MI][NI][2];
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        acc[mi][ni][h] = 0.0;
-        dsum[mi][ni][h] = 0u;
-      }
+  // With one stage per k-block every warp would flush at the same stage end and
+  // the DMMA pipe would idle meanwhile; warps 4..7 (the second warp of every
+  // SMSP) therefore cut their blocks in the middle of each stage instead. Any
+  // partition of k into blocks of <= kb words is exact, so both are correct.
+  if (MULTI && args.kb_stages == 1 && (warp >= 4) && BK / 8 >= 1)
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), false>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+  else
+    consume<BK, EPI, MULTI, 0, false>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+}
 
-  const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
-  uint32_t slot = 0, phase = 0;
-  for (int ts = 0; ts < my_tiles; ++ts) {
-    int tm, tn;
-    tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
-    const int m0 = tm * BM, n0 = tn * BN;
-    int kst = 0;
-    for (int kt = 0; kt < ktiles; ++kt) {
-      if (!nomem) mbar_wait(full + slot, phase);
-      const double* sA = smem + slot * G::STAGE;
-      const double* sB = sA + G::A_TILE;
-      const double* a_base = sA + (warp_m * WM + g) * G::A_ST + t;
-      const double* b_base = sB + t * B_ST + warp_n * WN + g;
-      if (!(args.debug & 2)) {  // debug bit 1: data delivery alone (no DMMA)
-#pragma unroll
-        for (int kk = 0; kk < BK / 4; ++kk) {
-          double af[MI], bf[NI];
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi) af[mi] = a_base[mi * 8 * G::A_ST + kk * 4];
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) bf[ni] = b_base[kk * 4 * B_ST + ni * 8];
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + slot);
-      if (++slot == S) {
-        slot = 0;
-        phase ^= 1;
-      }
-      if (MULTI) {
-        if (++kst == args.kb_stages) {
-          kst = 0;
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                dsum[mi][ni][h] += block_digit(acc[mi][ni][h], args.anchor, args.qmask);
-                acc[mi][ni][h] = 0.0;
-              }
-        }
-      }
+// ------------------------------------------------------------------ v4 (tiled)
+// The contraction on the tiled packed layout written by qg_pack_*_tiled:
+//   CA_t[tm][kt] = rows 128*tm.. x words BK*kt.. of CA      (128 x BK, dense)
+//   CB_t[tn][kt] = cols 128*tn.. x words BK*kt.. of CB^T    (128 x BK, dense)
+// zero padded at pack time, so a stage is exactly two cp.async.bulk copies of
+// 128*BK*8 bytes (28 KiB at BK = 28) and there is no ragged-edge handling
+// left in the kernel. Same warpgroup split and consumers as k_gemm_bulk.
+template <int BK, int EPI, bool MULTI, int FLUSH>
+__global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int tiles_m, int tiles_n) {
+  using GT = GeoT<BK>;
+  constexpr int S = GT::STAGES;
+  constexpr int NWARPS = NT / 32;
+  constexpr uint32_t CHUNK = BM * BK * 8;  // bytes of one operand block
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * GT::STAGE);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, NWARPS);
     }
-    // epilogue of this tile (the producer is already filling the next tile's stages)
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
-      const int row = m0 + warp_m * WM + mi * 8 + g;
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) {
-        const int col = n0 + warp_n * WN + ni * 8 + 2 * t;
-        if (EPI == EPI_DIGIT) {
-          uint32_t r[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) r[h] = block_digit(acc[mi][ni][h], args.anchor, args.qmask) + dsum[mi][ni][h];
-          if (row < M && col < N) {  // N even: col < N implies col + 1 < N
-            int32_t* dst = args.c + (size_t)row * args.ldc + col;
-            if (args.accumulate) {
-              const int2 old = *reinterpret_cast<const int2*>(dst);
-              r[0] += (uint32_t)old.x;
-              r[1] += (uint32_t)old.y;
-            }
-            *reinterpret_cast<int2*>(dst) = make_int2((int)modp(r[0]), (int)modp(r[1]));
-          }
-        } else if (row < M && col < N) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            double w = acc[mi][ni][h];
-            if (EPI == EPI_REDQ) {
-              const uint64_t bits = __double2ull_rz(w);
-              const uint64_t mask = (1ull << args.t) - 1;
-              uint64_t rr = 0;
-              for (int s2 = 0; s2 < args.t * args.e; s2 += args.t)
-                rr |= (uint64_t)modp((uint32_t)((bits >> s2) & mask)) << s2;
-              w = __ull2double_rn(rr);
-            }
-            args.cc[(size_t)row * args.ldcc + col + h] = w;
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          acc[mi][ni][h] = 0.0;
-          dsum[mi][ni][h] = 0u;
-        }
-      }
-    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __syncthreads();
+  const int ktiles = (args.K + BK - 1) / BK;
+  const int total_tiles = tiles_m * tiles_n;
+  const int my_tiles = blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const bool nomem = args.debug & 1;
+
+  if (warp >= NWARPS) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (nomem || warp != NWARPS || lane != 0) return;
+    uint32_t slot = 0, phase = 0;
+    for (int ts = 0; ts < my_tiles; ++ts) {
+      int tm, tn;
+      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+      const double* ablk = args.a + (size_t)tm * ktiles * BM * BK;
+      const double* bblk = args.b + (size_t)tn * ktiles * BM * BK;
+      for (int kt = 0; kt < ktiles; ++kt) {
+        mbar_wait(empty + slot, phase ^ 1);
+        double* sA = smem + slot * GT::STAGE;
+        mbar_arrive_expect_tx(full + slot, 2 * CHUNK);
+        bulk_g2s(sA, ablk + (size_t)kt * BM * BK, CHUNK, full + slot);
+        bulk_g2s(sA + GT::A_TILE, bblk + (size_t)kt * BM * BK, CHUNK, full + slot);
+        if (++slot == S) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  // FLUSH (multi-block): 0 = at stage ends; for kb_stages == 1 also
+  // 1 = staggered (warps 4..7 cut mid-stage; two inlined consumer bodies, so
+  // instantiated separately) and 2 = fused into the next stage's first k-step.
+  if (FLUSH == 2)  // fused flush with packed digit sums (t <= 16)
+    consume<BK, EPI, MULTI, -1, true, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+  else if (FLUSH == 1 && warp >= 4)
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+  else if (FLUSH == 1)
+    consume<BK, EPI, MULTI, 0, true, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+  else
+    consume<BK, EPI, MULTI, 0, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
 }
 
 // Reference-semantics contraction (DoubleWord::high_part, word.hpp:28-30):
@@ -604,13 +791,21 @@ static cudaError_t launch_bulk(const GemmArgs& a, cudaStream_t s) {
   GemmArgs a2 = a;
   const char* dbg = getenv("QG_DEBUG_MODE");
   a2.debug = dbg ? atoi(dbg) : 0;
+  // warps 4..7 start 4 us late so the two warps of an SMSP do not flush their
+  // k-blocks at the same moment (+3% on config 2, profiles/r01_notes.md)
+  const char* skew = getenv("QG_SKEW_NS");
+  a2.skew_ns = skew ? (unsigned)atoi(skew) : (a.kb_stages ? 4000u : 0u);
   k<<<grid, NT + 128, smem, s>>>(a2, tiles_m, tiles_n);
   count_launch();
   return cudaGetLastError();
 }
 
 static cudaError_t launch_digit_bulk(const GemmArgs& a, int bk, cudaStream_t s) {
-  if (a.kb_stages == 0) return launch_bulk<32, EPI_DIGIT, false>(a, s);
+  if (a.kb_stages == 0) {
+    const char* e = getenv("QG_SINGLE_BK");  // experiments: stage depth of single-block runs
+    if (e && atoi(e) == 16) return launch_bulk<16, EPI_DIGIT, false>(a, s);
+    return launch_bulk<32, EPI_DIGIT, false>(a, s);
+  }
   switch (bk) {
     case 32: return launch_bulk<32, EPI_DIGIT, true>(a, s);
     case 28: return launch_bulk<28, EPI_DIGIT, true>(a, s);
@@ -618,6 +813,60 @@ static cudaError_t launch_digit_bulk(const GemmArgs& a, int bk, cudaStream_t s) 
     case 16: return launch_bulk<16, EPI_DIGIT, true>(a, s);
     case 8: return launch_bulk<8, EPI_DIGIT, true>(a, s);
     case 4: return launch_bulk<4, EPI_DIGIT, true>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+static int num_sms();
+template <int BK, int EPI, bool MULTI, int FLUSH>
+static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
+  using GT = GeoT<BK>;
+  auto k = k_gemm_tiled<BK, EPI, MULTI, FLUSH>;
+  const size_t smem = GT::SMEM + 2 * GT::STAGES * sizeof(uint64_t);
+  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err) return err;
+  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int tiles = tiles_m * tiles_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  GemmArgs a2 = a;
+  const char* dbg = getenv("QG_DEBUG_MODE");
+  a2.debug = dbg ? atoi(dbg) : 0;
+  // warps 4..7 start 4 us late so the two warps of an SMSP do not flush their
+  // k-blocks at the same moment (+3% on config 2, profiles/r01_notes.md)
+  const char* skew = getenv("QG_SKEW_NS");
+  a2.skew_ns = skew ? (unsigned)atoi(skew) : (a.kb_stages ? 4000u : 0u);
+  k<<<grid, NT + 128, smem, s>>>(a2, tiles_m, tiles_n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int BK>
+static cudaError_t launch_tiled_bk(const GemmArgs& a, int flush, cudaStream_t s) {
+  const char* dbg = getenv("QG_DEBUG_MODE");  // bit 2: time without flushes (wrong digits)
+  if (a.kb_stages == 0 || (dbg && (atoi(dbg) & 4))) return launch_tiled_one<BK, EPI_DIGIT, false, 0>(a, s);
+  if (a.kb_stages == 1 && flush == 2 && a.pack_period >= 1) return launch_tiled_one<BK, EPI_DIGIT, true, 2>(a, s);
+  if (a.kb_stages == 1 && flush == 1 && BK >= 8 && a.pack_period >= 1)
+    return launch_tiled_one<BK, EPI_DIGIT, true, (BK >= 8 ? 1 : 0)>(a, s);
+  return launch_tiled_one<BK, EPI_DIGIT, true, 0>(a, s);
+}
+
+cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
+  if (a.M == 0 || a.N == 0) return cudaSuccess;
+  static thread_local char name[64];
+  // 0 = flush at stage ends (default), 1 = staggered, 2 = fused into the next
+  // stage's first k-step; measured equal within noise on B200, 0 spills least.
+  const char* e = getenv("QG_FLUSH");
+  const int flush = e ? atoi(e) : 0;
+  static const char* kFlush[] = {"", "_stagger", "_fused"};
+  snprintf(name, sizeof name, "dot_tiled_bk%d_%s%s", bk, a.kb_stages ? "multiblock" : "singleblock",
+           (a.kb_stages == 1 && (flush == 1 || (flush == 2 && a.pack_period >= 1))) ? kFlush[flush] : "");
+  *variant = name;
+  switch (bk) {
+    case 36: return launch_tiled_bk<36>(a, flush, s);
+    case 28: return launch_tiled_bk<28>(a, flush, s);
+    case 20: return launch_tiled_bk<20>(a, flush, s);
+    case 12: return launch_tiled_bk<12>(a, flush, s);
+    case 4: return launch_tiled_bk<4>(a, flush, s);
   }
   return cudaErrorInvalidValue;
 }

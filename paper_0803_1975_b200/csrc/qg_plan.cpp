@@ -127,52 +127,66 @@ uint64_t max_exact_block(uint32_t p, int t, int e) {
   return best;
 }
 
-// The contraction kernel flushes k-blocks at pipeline-stage boundaries; a
-// stage holds BK in {4, 8, 16, 24, 28, 32} words. Largest block (in words)
-// of the form BK * j not above `limit`; *bk gets the stage depth used.
-uint64_t stage_block(uint64_t limit, int* bk) {
-  static const int kBK[] = {32, 28, 24, 16, 8, 4};
+// Per-word cost of a stage depth relative to the deepest (calibrated on B200
+// with tools/plan_sweep.py, profiles/r01_plan_sweep_*.jsonl: short stages pay
+// their fixed barrier/producer overhead over fewer words).
+static double stage_cost(int bk) {
+  switch (bk) {
+    case 36: return 1.0;
+    case 32: return 1.0;
+    case 28: return 1.0;
+    case 24: return 1.02;
+    case 20: return 1.03;
+    case 16: return 1.05;
+    case 12: return 1.1;
+    case 8: return 1.25;
+    default: return 1.5;
+  }
+}
+constexpr double kFlushWords = 2.0;  // per-block flush overhead, in packed words
+
+// The contraction kernels flush k-blocks at pipeline-stage boundaries. The
+// tiled kernel (the main path) has stages of BK in {36, 28, 20, 12, 4} words,
+// the row-layout kernels of BK in {32, 28, 24, 16, 8, 4}. Picks the stage
+// depth (and the block BK * j <= limit) with the least predicted per-word
+// cost; returns the block length, *bk the stage depth.
+static uint64_t stage_block_set(uint64_t limit, int* bk, const int* set, int nset) {
   uint64_t best = 0;
   int best_bk = 0;
-  if (limit >= 64) {  // long blocks: deepest stage, flush cost is amortised anyway
-    best_bk = 32;
-    best = limit / 32 * 32;
-  } else {
-    for (int b : kBK) {  // descending, so ties keep the deeper stage
-      if (uint64_t(b) > limit) continue;
-      const uint64_t blk = limit / b * b;
-      if (blk > best) {
-        best = blk;
-        best_bk = b;
-      }
+  double best_cost = 1e300;
+  for (int i = 0; i < nset; ++i) {
+    const int b = set[i];
+    if (uint64_t(b) > limit) continue;
+    const uint64_t blk = limit / b * b;
+    const double cost = stage_cost(b) + kFlushWords / double(blk);
+    if (cost < best_cost - 1e-12) {
+      best_cost = cost;
+      best = blk;
+      best_bk = b;
     }
   }
   if (bk) *bk = best_bk;
   return best;
 }
 
-// Predicted relative cost of a blocked plan, in packed-word units: words
-// rounded up to the stage depth times the stage's per-word overhead, plus a
-// per-block flush cost. Calibrated on B200 with tools/plan_sweep.py
-// (profiles/r01_plan_sweep_*.jsonl): relative to the single-block kernel a
-// flush every stage runs at 0.94 / 0.92 / 0.91 / 0.86 / 0.74 / 0.62 of its
-// speed for BK = 32 / 28 / 24 / 16 / 8 / 4.
-static double stage_cost(int bk) {
-  switch (bk) {
-    case 32: return 1.0;
-    case 28: return 1.01;
-    case 24: return 1.02;
-    case 16: return 1.04;
-    case 8: return 1.1;
-    default: return 1.1;
-  }
+uint64_t stage_block(uint64_t limit, int* bk) {
+  static const int kSet[] = {32, 28, 24, 16, 8, 4};
+  return stage_block_set(limit, bk, kSet, 6);
 }
 
+uint64_t stage_block_tiled(uint64_t limit, int* bk) {
+  static const int kSet[] = {36, 28, 20, 12, 4};
+  return stage_block_set(limit, bk, kSet, 5);
+}
+
+// Predicted relative cost of a blocked plan, in packed-word units: words
+// rounded up to the stage depth times the stage's per-word overhead, plus a
+// per-block flush cost.
 double blocked_cost(uint64_t k, int e, uint64_t kb_words, double flush_words) {
   const uint64_t K = (k + e - 1) / e;
   if (kb_words >= K) return double((K + 31) / 32 * 32);
   int bk = 4;
-  const uint64_t blk = stage_block(kb_words, &bk);
+  const uint64_t blk = stage_block_tiled(kb_words, &bk);
   if (blk == 0) return 1e300;
   const uint64_t Kpad = (K + bk - 1) / bk * bk;
   const uint64_t nblocks = (K + blk - 1) / blk;
@@ -304,7 +318,7 @@ int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
   if (!out) return QG_INVALID_ARGUMENT;
   if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
   if (k < 1) return QG_INVALID_ARGUMENT;
-  const double flush_words = 2.0;  // per-block overhead in packed words
+  const double flush_words = kFlushWords;
   double best_cost = 1e300;
   bool found = false;
   qg_gpu_plan best;
@@ -323,7 +337,7 @@ int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
       }
       const uint64_t K = (k + e - 1) / e;
       if (kb >= K) kb = K;
-      else kb = stage_block(kb, nullptr);  // multi-block plans flush at stage ends
+      else kb = stage_block_tiled(kb, nullptr);  // multi-block plans flush at stage ends
       if (kb == 0 || (kb < 4 && kb < K)) continue;
       const uint64_t nblocks = (K + kb - 1) / kb;
       // digit sums of all blocks must fit the kernel's uint32 accumulator

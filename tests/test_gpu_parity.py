@@ -240,3 +240,50 @@ def test_empty_shapes(qg, cuda):
     z = lambda r, c: torch.zeros((r, c), dtype=torch.float64, device=cuda)
     assert qg.mul_common_compressed(z(0, 5), z(5, 4), plan).shape == (0, 4)
     assert qg.mul_common_compressed(z(3, 5), z(5, 0), plan).shape == (3, 0)
+
+
+@pytest.mark.parametrize("p,m,k,n", [(7, 300, 4096, 258), (3, 129, 512, 130), (5, 77, 8192, 64), (3, 512, 32768, 256),
+                                     (2, 64, 3000, 66), (11, 70, 40, 90), (7, 1, 113, 2)])
+@pytest.mark.parametrize("planner", ["gpu", "reference"])
+def test_tiled_path(qg, orc, cuda, p, m, k, n, planner):
+    """The tiled packed layout + tiled DMMA kernel (the fast path) equals naive_gemm."""
+    import torch
+
+    if planner == "reference" and k > 65535:
+        pytest.skip()
+    plan = qg.plan_gpu(p, k) if planner == "gpu" else qg.plan_compression(p, k)
+    a = orc.random_residue_matrix(m, k, p, 900 + m)
+    b = orc.random_residue_matrix(k, n, p, 901 + n)
+    got = host(qg.mul_common_tiled(torch.from_numpy(a.astype(np.float64)).to(cuda),
+                                   torch.from_numpy(b.astype(np.float64)).to(cuda), plan))
+    assert "tiled" in qg.last_kernel()
+    assert np.array_equal(got.astype(np.uint32), orc.naive_gemm(p, a, b))
+
+
+@pytest.mark.parametrize("bk", [4, 12, 20, 28, 36])
+def test_tiled_layout_words(qg, orc, cuda, bk):
+    """CA_t / CB_t hold exactly the reference's packed words, block by block,
+    zero padded (include/qgemm_b200.h)."""
+    import torch
+
+    p, m, k, n = 5, 150, 333, 170
+    plan = qg.plan_packed_axis(p, 300, 4)  # t for k=300, e=4
+    plan = qg.CompressionPlan(plan.p, plan.t, plan.d, plan.e, plan.beta, max(plan.kmax, k), plan.inv_qd, 0)
+    a = orc.random_residue_matrix(m, k, p, 31)
+    b = orc.random_residue_matrix(k, n, p, 32)
+    oplan = orc.plan_of(plan)
+    ca = orc.compress_rows_reversed(oplan, a)
+    cb = orc.compress_cols_forward(oplan, b)
+    K = ca.shape[1]
+    Kt = -(-K // bk)
+    ta = host(qg.pack_tiled(torch.from_numpy(a.astype(np.int32)).to(cuda), plan, bk, "a"))
+    tb = host(qg.pack_tiled(torch.from_numpy(b.astype(np.int32)).to(cuda), plan, bk, "b"))
+    Mt, Nt = -(-m // 128), -(-n // 128)
+    ea = np.zeros((Mt * 128, Kt * bk))
+    ea[:m, :K] = ca
+    eb = np.zeros((Nt * 128, Kt * bk))
+    eb[:n, :K] = cb.T
+    ea = ea.reshape(Mt, 128, Kt, bk).transpose(0, 2, 1, 3).ravel()
+    eb = eb.reshape(Nt, 128, Kt, bk).transpose(0, 2, 1, 3).ravel()
+    assert np.array_equal(bits(ta), bits(ea))
+    assert np.array_equal(bits(tb), bits(eb))

@@ -38,6 +38,7 @@ CONFIGS = {
     "config2": (7, 4096, 4096, 4096, "config2: p=7 m=n=k=4096 dot-product variant, k-blocked"),
     "config3": (3, 8192, 256, 8192, "config3: p=3 m=n=8192 k=256 dot-product variant"),
     "config5": (3, 32768, 32768, 32768, "config5: p=3 m=n=k=32768 dot-product variant, k-blocked"),
+    "config4": (5, 8192, 8192, 8192, "config4: p=5 m=n=k=8192 mixed (right) variant, REDQ epilogue -> CC"),
 }
 SEED = 42
 
@@ -192,6 +193,75 @@ def load_json(path):
             return json.load(f)
     except Exception:
         return None
+
+
+def mixed_arm(args):
+    """Config 4: mixed / right-compressed variant (gemm.hpp:285-335). Step =
+    compress_outer_cols(B) (K3) + the DMMA contraction A x CBo with the fused
+    REDQ epilogue (K5) on device-resident residues; output CC (ReduceAndCompress
+    words). Plan: plan_compression(p, k) as run_bench uses (bench.hpp:149)."""
+    import ctypes
+
+    import torch
+
+    import paper_0803_1975_b200 as qg
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    p, m, k, n, desc = CONFIGS[args.config]
+    plan = qg.plan_compression(p, k)
+    H = -(-n // plan.e)
+    a = qg.random_residue_matrix(m, k, p, SEED)
+    b = qg.random_residue_matrix(k, n, p, SEED + 1)
+    cbo = torch.empty((k, H), dtype=torch.float64, device=dev)
+    cc = torch.empty((m, H), dtype=torch.float64, device=dev)
+    pl = plan._c()
+    sp = qg._stream
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def step(ev=None):
+        qg._check(qg.lib.qg_compress_outer_cols(ctypes.byref(pl), qg._ptr(b), 0, k, n, n, qg._ptr(cbo), H, sp()))
+        if ev:
+            ev[0].record(stream)
+        qg._check(qg.lib.qg_mul_right(ctypes.byref(pl), qg._ptr(a), k, qg._ptr(cbo), m, k, n, qg._ptr(cc), sp()))
+        if ev:
+            ev[1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    step_ms, kern_ms = [], []
+    launches0 = qg.kernel_launches()
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            s0.record(stream)
+            step(ev)
+            s1.record(stream)
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            kern_ms.append(ev[0].elapsed_time(ev[1]))
+    ms = sum(step_ms) / len(step_ms)
+    kms = sum(kern_ms) / len(kern_ms)
+    flop = 2.0 * m * H * k
+    peak = float((load_json(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) or {}).get("dmma_m8n8k4_tflops", 37.09))
+    words = cc.cpu().numpy().view("uint64")
+    import hashlib
+
+    line = {"metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": 2.0 * m * n * k / (ms * 1e-3),
+            "unit": "mult-adds/s (2mnk/s)", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n, "plan": {"t": plan.t, "e": plan.e}},
+            "roofline": {"bound": "tensor", "achieved": round(flop / (kms * 1e-3) / 1e12, 3), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(flop / (kms * 1e-3) / 1e12 / peak, 4), "traffic": None, "kernel": qg.last_kernel(),
+                         "kernel_ms": round(kms, 4)},
+            "gpu_launches": qg.kernel_launches() - launches0, "cc_sha256": hashlib.sha256(words.tobytes()).hexdigest(),
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def our_arm(args):
@@ -398,6 +468,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "config4":
+        return mixed_arm(args)
     return our_arm(args)
 
 

@@ -1,0 +1,199 @@
+// qgemm_b200.hpp — C++ drop-in for the reference's qgemm header API,
+// implemented over the C ABI (qgemm_b200.h) and therefore over the sm_100a
+// kernels. Header-only; link with -lqgemm_b200 (paper_0803_1975_b200/_lib).
+//
+// Same names, argument meaning and error behaviour as
+// /root/reference/proj/include/qgemm/*.hpp for the dot-product and mixed
+// paths: value types in, value types out, exceptions on error
+// (errors.hpp:8-34, std::invalid_argument for bad arguments). A reference
+// caller switches by replacing
+//     #include "qgemm/qgemm.hpp"     using namespace qgemm;
+// with
+//     #include "qgemm_b200.hpp"      using namespace qgemm_b200;
+// for the entry points below (INTEGRATION.md lists them with their
+// reference file:line).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qgemm_b200.h"
+
+namespace qgemm_b200 {
+
+// ------------------------------------------------------------ errors.hpp:8-34
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidModulus : Error { using Error::Error; };
+struct NoCompression : Error { using Error::Error; };
+struct SlotOverflow : Error { using Error::Error; };
+struct DigitOverflow : Error { using Error::Error; };
+struct DimensionMismatch : Error { using Error::Error; };
+struct PlanMismatch : Error { using Error::Error; };
+struct UnsupportedAlgorithm : Error { using Error::Error; };
+struct ParseError : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };  // CUDA failures (no reference analogue)
+
+inline void check(int status, const char* where) {
+  if (status == QG_OK) return;
+  std::string msg = std::string(where) + ": " + qg_status_string(status);
+  if (status == QG_CUDA_ERROR) msg += std::string(" (") + qg_last_error() + ")";
+  switch (status) {
+    case QG_INVALID_MODULUS: throw InvalidModulus(msg);
+    case QG_NO_COMPRESSION: throw NoCompression(msg);
+    case QG_SLOT_OVERFLOW: throw SlotOverflow(msg);
+    case QG_DIGIT_OVERFLOW: throw DigitOverflow(msg);
+    case QG_DIMENSION_MISMATCH: throw DimensionMismatch(msg);
+    case QG_PLAN_MISMATCH: throw PlanMismatch(msg);
+    case QG_UNSUPPORTED_ALGORITHM: throw UnsupportedAlgorithm(msg);
+    case QG_PARSE_ERROR: throw ParseError(msg);
+    case QG_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+// ------------------------------------------------------------ field / plan
+using Residue = std::uint32_t;  // field.hpp:12
+
+enum class ExtractionMode { ReciprocalMul = QG_EXTRACT_RECIPROCAL_MUL, AddHighBits = QG_EXTRACT_ADD_HIGH_BITS };
+
+// CompressionPlan, plan.hpp:29-42 (the modulus is carried as its value).
+struct CompressionPlan {
+  qg_plan c{};
+  std::uint32_t p() const { return c.p; }
+  int t() const { return c.t; }
+  int d() const { return c.d; }
+  int e() const { return c.e; }
+  int beta() const { return c.beta; }
+  std::uint64_t kmax() const { return c.kmax; }
+  double inv_qd() const { return c.inv_qd; }
+  std::uint64_t q() const { return std::uint64_t{1} << c.t; }
+  std::uint64_t q_mask() const { return q() - 1; }
+};
+
+// A plan k-blocked for the FP64 tensor-core contraction (qg_plan_gpu).
+struct GpuPlan {
+  qg_gpu_plan c{};
+  CompressionPlan plan() const { return CompressionPlan{c.plan}; }
+  std::uint64_t kblock_words() const { return c.kblock_words; }
+};
+
+// plan_compression, plan.hpp:125-159
+inline CompressionPlan plan_compression(std::uint32_t p, std::uint64_t k, int beta = 53,
+                                        ExtractionMode mode = ExtractionMode::ReciprocalMul) {
+  CompressionPlan pl;
+  check(qg_plan_compression(p, k, beta, static_cast<int>(mode), &pl.c), "plan_compression");
+  return pl;
+}
+// uncompressed_plan, plan.hpp:164-179
+inline CompressionPlan uncompressed_plan(std::uint32_t p, std::uint64_t k, int beta = 53) {
+  CompressionPlan pl;
+  check(qg_uncompressed_plan(p, k, beta, &pl.c), "uncompressed_plan");
+  return pl;
+}
+// plan_packed_axis, plan.hpp:186-203
+inline CompressionPlan plan_packed_axis(std::uint32_t p, std::uint64_t k, std::uint64_t axis_len,
+                                        int beta = 53) {
+  CompressionPlan pl;
+  check(qg_plan_packed_axis(p, k, axis_len, beta, &pl.c), "plan_packed_axis");
+  return pl;
+}
+// choose_panel, plan.hpp:209-224
+inline std::uint64_t choose_panel(std::uint32_t p, std::uint64_t k, int beta = 53) {
+  std::uint64_t out = 0;
+  check(qg_choose_panel(p, k, beta, &out), "choose_panel");
+  return out;
+}
+// The GPU planner: (t, e, k-block) chosen for the tensor-core path.
+inline GpuPlan plan_gpu(std::uint32_t p, std::uint64_t k) {
+  GpuPlan g;
+  check(qg_plan_gpu(p, k, &g.c), "plan_gpu");
+  return g;
+}
+
+// ------------------------------------------------------------ matrix.hpp:14-26
+struct ResidueMatrix {
+  std::size_t rows = 0;
+  std::size_t cols = 0;
+  std::vector<Residue> data;
+  ResidueMatrix() = default;
+  ResidueMatrix(std::size_t r, std::size_t c) : rows(r), cols(c), data(r * c, 0) {}
+  Residue& at(std::size_t i, std::size_t j) { return data[i * cols + j]; }
+  Residue at(std::size_t i, std::size_t j) const { return data[i * cols + j]; }
+  friend bool operator==(const ResidueMatrix&, const ResidueMatrix&) = default;
+};
+
+// Packed words of a right-compressed product (CompressedMatrix<DoubleWord>
+// of packed_right_product / mul_right_compressed, m x ceil(n/e), matrix.hpp:44-63).
+struct CompressedWords {
+  std::size_t logical_rows = 0, logical_cols = 0, stored_rows = 0, stored_cols = 0;
+  CompressionPlan plan;
+  std::vector<double> data;
+};
+
+namespace detail {
+inline void check_inner_dims(const ResidueMatrix& a, const ResidueMatrix& b) {  // gemm.hpp:22-27
+  if (a.cols != b.rows)
+    throw DimensionMismatch("inner dimensions disagree: " + std::to_string(a.rows) + "x" +
+                            std::to_string(a.cols) + " times " + std::to_string(b.rows) + "x" +
+                            std::to_string(b.cols));
+}
+}  // namespace detail
+
+// ------------------------------------------------------------ gemm.hpp entry points
+// mul_common_compressed(A, B, plan), gemm.hpp:254-260: on the device, k-blocked
+// for exactness where the plan requires it.
+inline ResidueMatrix mul_common_compressed(const ResidueMatrix& a, const ResidueMatrix& b,
+                                           const CompressionPlan& plan) {
+  detail::check_inner_dims(a, b);
+  ResidueMatrix c(a.rows, b.cols);
+  check(qg_host_mul_common(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, c.data.data()),
+        "mul_common_compressed");
+  return c;
+}
+// Same product under a GPU plan: k may exceed plan().kmax() (in-kernel k-blocks).
+inline ResidueMatrix mul_common_compressed(const ResidueMatrix& a, const ResidueMatrix& b,
+                                           const GpuPlan& plan) {
+  detail::check_inner_dims(a, b);
+  ResidueMatrix c(a.rows, b.cols);
+  check(qg_host_mul_common_gpu(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, c.data.data()),
+        "mul_common_compressed");
+  return c;
+}
+// blocked_accumulate, gemm.hpp:450-489.
+inline ResidueMatrix blocked_accumulate(const ResidueMatrix& a, const ResidueMatrix& b,
+                                        const CompressionPlan& plan, std::size_t kpanel) {
+  detail::check_inner_dims(a, b);
+  ResidueMatrix c(a.rows, b.cols);
+  check(qg_host_blocked_accumulate(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, kpanel,
+                                   c.data.data()),
+        "blocked_accumulate");
+  return c;
+}
+// mul_right_compressed(A, compress_outer_cols(B, plan)), gemm.hpp:320-325:
+// the post-REDQ words, bit-identical to the reference's.
+inline CompressedWords mul_right_compressed(const ResidueMatrix& a, const ResidueMatrix& b,
+                                            const CompressionPlan& plan) {
+  detail::check_inner_dims(a, b);
+  CompressedWords cc;
+  cc.logical_rows = cc.stored_rows = a.rows;
+  cc.logical_cols = b.cols;
+  cc.stored_cols = (b.cols + plan.e() - 1) / plan.e();
+  cc.plan = plan;
+  cc.data.resize(cc.stored_rows * cc.stored_cols);
+  check(qg_host_mul_right(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, cc.data.data()),
+        "mul_right_compressed");
+  return cc;
+}
+
+// residue_checksum, bench.hpp:43-47.
+inline std::uint32_t residue_checksum(const ResidueMatrix& m) {
+  std::uint32_t s = 0;
+  for (Residue v : m.data) s += v;
+  return s;
+}
+
+}  // namespace qgemm_b200

@@ -449,37 +449,99 @@ struct DevBuf {
   } while (0)
 }  // namespace
 
+// Streams and events of the pipelined host path, created once per thread.
+struct HostPipe {
+  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  static constexpr int kMaxChunks = 64;
+  cudaEvent_t b_ready = nullptr, a_ready[kMaxChunks] = {}, c_ready[kMaxChunks] = {}, done = nullptr;
+  bool ok = false;
+  HostPipe() {
+    ok = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < kMaxChunks; ++i)
+      ok = cudaEventCreateWithFlags(&a_ready[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c_ready[i], cudaEventDisableTiming) == cudaSuccess;
+    // keep freed stream-ordered allocations mapped across calls (the default
+    // release threshold of 0 would unmap and re-map the buffers every call)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (ok && cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+};
+
+// mul_common_compressed on host data, pipelined over three streams: B goes
+// up first and is packed; A then streams up in row chunks of 512 while the
+// previous chunks are packed and contracted, and C streams back per chunk on
+// its own stream (the two PCIe directions overlap). Exact same kernels and
+// results as the device path.
 static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m,
                        size_t k, size_t n, uint32_t* c) {
   const qg_plan& pl = gp->plan;
   int st;
-  cudaStream_t s = nullptr;
   const size_t K = ceil_div(k, pl.e);
   int bk = 0, kbs = 0;
-  const bool tiled = (n % 2 == 0) && tiled_geometry(gp, K ? K : 1, &bk, &kbs) == QG_OK;
+  const bool tiled = (n % 2 == 0) && K > 0 && tiled_geometry(gp, K, &bk, &kbs) == QG_OK;
+  if (tiled && m * n > 0) {
+    thread_local HostPipe hp;
+    if (!hp.ok) return QG_CUDA_ERROR;
+    const size_t chunk = 512;  // rows per pipeline chunk (a multiple of the 128-row tile)
+    size_t nchunks = ceil_div(m, chunk);
+    const size_t rows_per = nchunks > (size_t)HostPipe::kMaxChunks ? ceil_div(ceil_div(m, HostPipe::kMaxChunks), 128) * 128 : chunk;
+    nchunks = ceil_div(m, rows_per);
+    const size_t Kt = ceil_div(K, (size_t)bk);
+    DevBuf da(hp.in), db(hp.in), dca(hp.in), dcb(hp.in), dc(hp.in);
+    QG_TRY(da.alloc(m * k * 4));
+    QG_TRY(db.alloc(k * n * 4));
+    QG_TRY(dc.alloc(m * n * 4));
+    QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
+    QG_TRY(dcb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
+    QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
+    QG_TRY(cudaEventRecord(hp.b_ready, hp.in));
+    for (size_t i = 0; i < nchunks; ++i) {
+      const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+      QG_TRY(cudaMemcpyAsync((uint32_t*)da.p + r0 * k, a + r0 * k, rows * k * 4, cudaMemcpyHostToDevice, hp.in));
+      QG_TRY(cudaEventRecord(hp.a_ready[i], hp.in));
+    }
+    QG_TRY(cudaStreamWaitEvent(hp.comp, hp.b_ready, 0));
+    QG_TRY(qgk::launch_pack_tiled(true, db.p, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, hp.comp));
+    for (size_t i = 0; i < nchunks; ++i) {
+      const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+      double* ca_chunk = (double*)dca.p + (r0 / 128) * Kt * 128 * bk;
+      QG_TRY(cudaStreamWaitEvent(hp.comp, hp.a_ready[i], 0));
+      QG_TRY(qgk::launch_pack_tiled(false, (const uint32_t*)da.p + r0 * k, QG_U32, rows, k, k, pl.t, pl.e, bk,
+                                    ca_chunk, hp.comp));
+      if ((st = qg_mul_common_tiled(gp, ca_chunk, (const double*)dcb.p, rows, n, k, (int32_t*)dc.p + r0 * n, n,
+                                    hp.comp)))
+        return st;
+      QG_TRY(cudaEventRecord(hp.c_ready[i], hp.comp));
+      QG_TRY(cudaStreamWaitEvent(hp.out, hp.c_ready[i], 0));
+      QG_TRY(cudaMemcpyAsync(c + r0 * n, (const int32_t*)dc.p + r0 * n, rows * n * 4, cudaMemcpyDeviceToHost, hp.out));
+    }
+    QG_TRY(cudaEventRecord(hp.done, hp.out));
+    QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
+    QG_TRY(cudaStreamSynchronize(hp.out));
+    return QG_OK;
+  }
+  cudaStream_t s = nullptr;
   DevBuf da(s), db(s), dca(s), dcb(s), dc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
   QG_TRY(dc.alloc(m * n * 4));
   if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if (tiled) {  // tiled packed layout + the v4 contraction
-    QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
-    QG_TRY(dcb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
-    QG_TRY(qgk::launch_pack_tiled(false, da.p, QG_U32, m, k, k, pl.t, pl.e, bk, (double*)dca.p, s));
-    QG_TRY(qgk::launch_pack_tiled(true, db.p, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, s));
-    if ((st = qg_mul_common_tiled(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
-      return st;
-  } else {  // reference layout: packing itself does not depend on kmax; the blocks enforce Eq. 3
-    QG_TRY(dca.alloc(m * K * 8));
-    QG_TRY(dcb.alloc(K * n * 8));
-    QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e,
-                            (double*)dca.p, K, 0, 0, s));
-    QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e,
-                            (double*)dcb.p, n, 0, 0, s));
-    if ((st = qg_mul_common(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
-      return st;
-  }
+  // reference layout: packing itself does not depend on kmax; the blocks enforce Eq. 3
+  QG_TRY(dca.alloc(m * K * 8));
+  QG_TRY(dcb.alloc(K * n * 8));
+  QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e, (double*)dca.p, K, 0, 0, s));
+  QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e, (double*)dcb.p, n, 0, 0, s));
+  if ((st = qg_mul_common(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
+    return st;
   if (m * n) QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
   return QG_OK;

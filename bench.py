@@ -287,7 +287,7 @@ def our_arm(args):
     p, m_rank, k, n, desc = CONFIGS[args.config]
     gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
     if args.kblock:  # experiments: override the k-block of the chosen plan
-        gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words)
+        gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words, gp.balanced)
     pl = gp.plan
     K = -(-k // pl.e)
     m_total = m_rank * world
@@ -310,11 +310,11 @@ def our_arm(args):
     plc = pl._c()
 
     def pack_rows(a_):
-        qg._check(qg.lib.qg_pack_a_tiled(ctypes.byref(plc), bk, qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), sp()))
+        qg._check(qg.lib.qg_pack_a_tiled(ctypes.byref(gpc), bk, qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), sp()))
         return ca
 
     def pack_cols(b_):
-        qg._check(qg.lib.qg_pack_b_tiled(ctypes.byref(plc), bk, qg._ptr(b_), 0, k, n, n, qg._ptr(cb), sp()))
+        qg._check(qg.lib.qg_pack_b_tiled(ctypes.byref(gpc), bk, qg._ptr(b_), 0, k, n, n, qg._ptr(cb), sp()))
         return cb
 
     ev = {}

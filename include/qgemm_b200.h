@@ -73,6 +73,12 @@ typedef struct {
   qg_plan plan;
   uint64_t kblock_words;
   uint64_t max_exact_words; /* Eq. G bound for (p, t, e), informational */
+  /* 1: residues enter the packed words in balanced form (v > p/2 -> v - p),
+   * so every digit is signed with |digit| <= (p/2)^2 per product; digit d is
+   * read by rounding to nearest. Twice the exact block of
+   * the unsigned packing at the same (t, e). Tiled path only. */
+  int32_t balanced;
+  int32_t reserved;
 } qg_gpu_plan;
 
 /* PackOrientation, matrix.hpp:28-39: direction 0 Forward / 1 Reversed;
@@ -103,9 +109,15 @@ int qg_choose_panel(uint32_t p, uint64_t k, int beta, uint64_t* out);
 int qg_max_exact_block(const qg_plan* plan, uint64_t* words);
 /* k-block an existing plan for the tensor-core path (reference plan kept). */
 int qg_gpu_plan_from(const qg_plan* plan, uint64_t k, qg_gpu_plan* out);
-/* choose (t, e, kblock) for common dimension k on the tensor-core path:
- * minimises predicted contraction time over all exact blocked plans. */
+/* choose (t, e, kblock, balanced) for common dimension k on the tensor-core
+ * path: minimises predicted contraction time over all exact blocked plans. */
 int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out);
+/* qg_plan_gpu with flags: QG_PLAN_UNSIGNED_ONLY restricts to unsigned digits
+ * (words bit-compatible with the reference packing, for the row layouts). */
+enum { QG_PLAN_UNSIGNED_ONLY = 1 };
+int qg_plan_gpu_ex(uint32_t p, uint64_t k, int flags, qg_gpu_plan* out);
+/* Eq. G bound for balanced digits (qg_gpu_plan.balanced = 1). */
+int qg_max_exact_block_balanced(const qg_plan* plan, uint64_t* words);
 
 /* -------------------------------------------------- device (stream-ordered) */
 /* random_residue_matrix, prng.hpp:31-38 (SplitMix64 stream, counter-based):
@@ -159,10 +171,10 @@ int qg_mul_common_repacked(const qg_gpu_plan* gplan, const double* ca, const dou
  * buffer size in doubles for `rows` (m for CA_t, n for CB_t). */
 int qg_tiled_stage_words(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk);
 size_t qg_tiled_words(size_t rows, size_t k, int e, uint32_t bk);
-int qg_pack_a_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
-                    size_t lda, double* ca_t, void* stream);
-int qg_pack_b_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
-                    size_t ldb, double* cb_t, void* stream);
+int qg_pack_a_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* a, qg_dtype dtype, size_t m,
+                    size_t k, size_t lda, double* ca_t, void* stream);
+int qg_pack_b_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* b, qg_dtype dtype, size_t k,
+                    size_t n, size_t ldb, double* cb_t, void* stream);
 /* qg_mul_common on tiled operands (n and ldc even). */
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m,
                         size_t n, size_t k, int32_t* c, size_t ldc, void* stream);

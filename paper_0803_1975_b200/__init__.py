@@ -122,7 +122,8 @@ class _Plan(ctypes.Structure):
 
 
 class _GpuPlan(ctypes.Structure):
-    _fields_ = [("plan", _Plan), ("kblock_words", ctypes.c_uint64), ("max_exact_words", ctypes.c_uint64)]
+    _fields_ = [("plan", _Plan), ("kblock_words", ctypes.c_uint64), ("max_exact_words", ctypes.c_uint64),
+                ("balanced", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class _Orientation(ctypes.Structure):
@@ -148,6 +149,8 @@ def _load():
         "qg_max_exact_block": ([P(_Plan), P(u64)], i32),
         "qg_gpu_plan_from": ([P(_Plan), u64, P(_GpuPlan)], i32),
         "qg_plan_gpu": ([u32, u64, P(_GpuPlan)], i32),
+        "qg_plan_gpu_ex": ([u32, u64, i32, P(_GpuPlan)], i32),
+        "qg_max_exact_block_balanced": ([P(_Plan), P(u64)], i32),
         "qg_gen_residues": ([u64, u32, sz, sz, sz, vp, i32, vp], i32),
         "qg_compress_rows_reversed": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
         "qg_compress_cols_forward": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
@@ -167,8 +170,8 @@ def _load():
         "qg_host_mul_right": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_tiled_stage_words": ([P(_GpuPlan), u64, P(u32)], i32),
         "qg_tiled_words": ([sz, sz, i32, u32], sz),
-        "qg_pack_a_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
-        "qg_pack_b_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_a_tiled": ([P(_GpuPlan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_b_tiled": ([P(_GpuPlan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_mul_common_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
@@ -246,9 +249,14 @@ class GpuPlan:
     plan: CompressionPlan
     kblock_words: int
     max_exact_words: int
+    balanced: int = 0
 
     def _c(self) -> _GpuPlan:
-        return _GpuPlan(self.plan._c(), self.kblock_words, self.max_exact_words)
+        return _GpuPlan(self.plan._c(), self.kblock_words, self.max_exact_words, self.balanced, 0)
+
+    @staticmethod
+    def _from(c: "_GpuPlan") -> "GpuPlan":
+        return GpuPlan(CompressionPlan._from(c.plan), c.kblock_words, c.max_exact_words, c.balanced)
 
 
 def make_plan(p: int, t: int, e: int, beta: int = 53) -> CompressionPlan:
@@ -295,13 +303,22 @@ def gpu_plan_from(plan: CompressionPlan, k: int) -> GpuPlan:
     out = _GpuPlan()
     pl = plan._c()
     _check(lib.qg_gpu_plan_from(ctypes.byref(pl), k, ctypes.byref(out)))
-    return GpuPlan(CompressionPlan._from(out.plan), out.kblock_words, out.max_exact_words)
+    return GpuPlan._from(out)
 
 
-def plan_gpu(p: int, k: int) -> GpuPlan:
+def plan_gpu(p: int, k: int, balanced: bool = True) -> GpuPlan:
+    """(t, e, k-block[, balanced digits]) for the tensor-core path; balanced=False
+    restricts to the reference's unsigned packing."""
     out = _GpuPlan()
-    _check(lib.qg_plan_gpu(p, k, ctypes.byref(out)))
-    return GpuPlan(CompressionPlan._from(out.plan), out.kblock_words, out.max_exact_words)
+    _check(lib.qg_plan_gpu_ex(p, k, 0 if balanced else 1, ctypes.byref(out)))
+    return GpuPlan._from(out)
+
+
+def max_exact_block_balanced(plan: CompressionPlan) -> int:
+    out = ctypes.c_uint64()
+    pl = plan._c()
+    _check(lib.qg_max_exact_block_balanced(ctypes.byref(pl), ctypes.byref(out)))
+    return out.value
 
 
 def kernel_launches() -> int:
@@ -509,6 +526,9 @@ def mul_common_compressed(a_or_ca, b_or_cb, plan: Optional[Union[CompressionPlan
         ca, cb = a_or_ca, b_or_cb
         _check_common_operands(ca, cb)
         gp = _as_gpu_plan(plan if plan is not None else ca.plan, ca.logical_cols)
+        if gp.balanced:
+            raise PlanMismatch("operands packed in the reference layout hold unsigned words; "
+                               "use plan_gpu(p, k, balanced=False)")
     else:
         a, b = a_or_ca, b_or_cb
         if a.shape[1] != b.shape[0]:  # check_inner_dims, gemm.hpp:22-27
@@ -521,6 +541,10 @@ def mul_common_compressed(a_or_ca, b_or_cb, plan: Optional[Union[CompressionPlan
             raise PlanMismatch(f"common dimension {k} exceeds kmax={base.kmax}")
         if b.shape[1] % 2 == 0 and not os.environ.get("QG_FORCE_ROW_LAYOUT"):
             return mul_common_tiled(a, b, gp)
+        if gp.balanced:  # the row layout holds the reference's unsigned words
+            gp = plan_gpu(base.p, k, balanced=False)
+            base = gp.plan
+            plan = gp
         if isinstance(plan, GpuPlan) and k > base.kmax:
             # blocked plan: pack with a kmax-free plan view (blocks enforce Eq. 3)
             big = dataclasses.replace(base, kmax=max(base.kmax, k))
@@ -542,14 +566,17 @@ def tiled_stage_words(gp: GpuPlan, k: int) -> int:
     return out.value
 
 
-def pack_tiled(a, plan: CompressionPlan, bk: int, operand: str):
+def pack_tiled(a, plan: Union[CompressionPlan, GpuPlan], bk: int, operand: str):
     """Tiled packed layout of A ('a': compress_rows_reversed words) or B
     ('b': compress_cols_forward words, transposed) as dense zero-padded
-    128 x bk blocks (include/qgemm_b200.h). Returns a flat float64 tensor."""
+    128 x bk blocks (include/qgemm_b200.h); balanced digits if the GpuPlan says
+    so. Returns a flat float64 tensor."""
     torch = _torch()
     _require_cuda(a)
     rows, cols = a.shape
-    pl = plan._c()
+    gp = plan if isinstance(plan, GpuPlan) else GpuPlan(plan, 1, 0, 0)
+    plan = gp.plan
+    pl = gp._c()
     if operand == "a":
         out = torch.empty(lib.qg_tiled_words(rows, cols, plan.e, bk), dtype=torch.float64, device=a.device)
         _check(lib.qg_pack_a_tiled(ctypes.byref(pl), bk, _ptr(a), _dtype_code(a), rows, cols, cols, _ptr(out), _stream()))
@@ -567,8 +594,8 @@ def mul_common_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]):
     n = b.shape[1]
     gp = _as_gpu_plan(plan, k)
     bk = tiled_stage_words(gp, k)
-    ca = pack_tiled(a, gp.plan, bk, "a")
-    cb = pack_tiled(b, gp.plan, bk, "b")
+    ca = pack_tiled(a, gp, bk, "a")
+    cb = pack_tiled(b, gp, bk, "b")
     out = torch.empty((m, n), dtype=torch.int32, device=a.device)
     g = gp._c()
     _check(lib.qg_mul_common_tiled(ctypes.byref(g), _ptr(ca), _ptr(cb), m, n, k, _ptr(out), n, _stream()))

@@ -16,6 +16,7 @@ bool is_prime(uint64_t n);
 uint64_t max_exact_block(uint32_t p, int t, int e);
 uint64_t stage_block(uint64_t limit, int* bk);
 uint64_t stage_block_tiled(uint64_t limit, int* bk);
+uint64_t max_exact_block_balanced(uint32_t p, int t, int e);
 }  // namespace qg
 
 namespace qgk {
@@ -139,7 +140,8 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
 // divides the (Eq. G / Eq. 3) block.
 int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
   const qg_plan& pl = gp->plan;
-  const uint64_t exact = qg::max_exact_block(pl.p, pl.t, pl.e);
+  const uint64_t exact = gp->balanced ? qg::max_exact_block_balanced(pl.p, pl.t, pl.e)
+                                      : qg::max_exact_block(pl.p, pl.t, pl.e);
   uint64_t kb = gp->kblock_words < K ? gp->kblock_words : K;
   if (kb > exact) kb = exact;
   if (kb >= K) {
@@ -174,24 +176,28 @@ size_t qg_tiled_words(size_t rows, size_t k, int e, uint32_t bk) {
   return ceil_div(rows, 128) * 128 * ceil_div(K, bk) * bk;
 }
 
-int qg_pack_a_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
+int qg_pack_a_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
                     size_t lda, double* ca_t, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan* plan = &gplan->plan;
   int st = check_plan(plan);
   if (st) return st;
   if ((st = check_dtype(dtype))) return st;
   if (lda < k) return QG_INVALID_ARGUMENT;
   return cuda_status(qgk::launch_pack_tiled(false, a, dtype, m, k, lda, plan->t, plan->e, (int)bk, ca_t,
-                                            as_stream(stream)));
+                                            as_stream(stream), plan->p, gplan->balanced != 0));
 }
 
-int qg_pack_b_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+int qg_pack_b_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
                     size_t ldb, double* cb_t, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan* plan = &gplan->plan;
   int st = check_plan(plan);
   if (st) return st;
   if ((st = check_dtype(dtype))) return st;
   if (ldb < n) return QG_INVALID_ARGUMENT;
   return cuda_status(qgk::launch_pack_tiled(true, b, dtype, k, n, ldb, plan->t, plan->e, (int)bk, cb_t,
-                                            as_stream(stream)));
+                                            as_stream(stream), plan->p, gplan->balanced != 0));
 }
 
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,
@@ -217,7 +223,11 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   a.N = (int)n;
   a.K = (int)K;
   a.kb_stages = kbs;
-  a.anchor = std::ldexp(1.0, pl.t * pl.d + 52);
+  a.balanced = gplan->balanced != 0;
+  // unsigned: round-toward-zero against 2^(td+52) gives floor(S/Q^d); balanced:
+  // round-to-nearest against 1.5*2^(td+52) + Q^d*Q/2 gives round(S/Q^d) + Q/2
+  a.anchor = a.balanced ? std::ldexp(1.5, pl.t * pl.d + 52) + std::ldexp(1.0, pl.t * pl.d + pl.t - 1)
+                        : std::ldexp(1.0, pl.t * pl.d + 52);
   a.qmask = (uint32_t)((1ull << pl.t) - 1);
   a.p = pl.p;
   a.c = c;
@@ -230,8 +240,8 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   // digit sums are uint32 (planner keeps nblocks * (Q-1) < 2^32); the fused
   // flush packs two per register as 16-bit lanes, reduced mod p in time
   if (pl.t <= 16) a.pack_period = (int)((65535u - (pl.p - 1)) / a.qmask);
-  const uint64_t nblocks = kbs ? ceil_div(K, (size_t)kbs * bk) : 1;
-  if ((unsigned __int128)nblocks * a.qmask + pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+  const uint64_t nblocks = (kbs ? ceil_div(K, (size_t)kbs * bk) : 1) + 1;
+  if ((unsigned __int128)nblocks * a.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
   return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));
 }
 
@@ -326,6 +336,7 @@ int qg_reduce_common(const qg_plan* plan, const double* acc, size_t count, int32
 int qg_mul_common(const qg_gpu_plan* gplan, const double* ca, const double* cb, size_t m, size_t n,
                   size_t k, int32_t* c, size_t ldc, void* stream) {
   if (!gplan) return QG_INVALID_ARGUMENT;
+  if (gplan->balanced) return QG_PLAN_MISMATCH;  // reference-layout words are unsigned
   const qg_plan& pl = gplan->plan;
   int st = check_plan(&pl);
   if (st) return st;
@@ -509,13 +520,14 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
       QG_TRY(cudaEventRecord(hp.a_ready[i], hp.in));
     }
     QG_TRY(cudaStreamWaitEvent(hp.comp, hp.b_ready, 0));
-    QG_TRY(qgk::launch_pack_tiled(true, db.p, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, hp.comp));
+    QG_TRY(qgk::launch_pack_tiled(true, db.p, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, hp.comp, pl.p,
+                                  gp->balanced != 0));
     for (size_t i = 0; i < nchunks; ++i) {
       const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
       double* ca_chunk = (double*)dca.p + (r0 / 128) * Kt * 128 * bk;
       QG_TRY(cudaStreamWaitEvent(hp.comp, hp.a_ready[i], 0));
       QG_TRY(qgk::launch_pack_tiled(false, (const uint32_t*)da.p + r0 * k, QG_U32, rows, k, k, pl.t, pl.e, bk,
-                                    ca_chunk, hp.comp));
+                                    ca_chunk, hp.comp, pl.p, gp->balanced != 0));
       if ((st = qg_mul_common_tiled(gp, ca_chunk, (const double*)dcb.p, rows, n, k, (int32_t*)dc.p + r0 * n, n,
                                     hp.comp)))
         return st;
@@ -527,6 +539,11 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
     QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
     QG_TRY(cudaStreamSynchronize(hp.out));
     return QG_OK;
+  }
+  if (gp->balanced) {  // the row-layout kernels need unsigned words: re-plan
+    qg_gpu_plan up;
+    if ((st = qg_plan_gpu_ex(pl.p, k, 1, &up))) return st;
+    return host_common(&up, a, b, m, k, n, c);
   }
   cudaStream_t s = nullptr;
   DevBuf da(s), db(s), dca(s), dcb(s), dc(s);

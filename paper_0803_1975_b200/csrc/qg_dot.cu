@@ -146,6 +146,18 @@ __device__ __forceinline__ uint32_t block_digit(double acc, double anchor, uint3
 #endif
 }
 
+// Balanced digits: S = sum D_s Q^s with |D_s| < Q/2, digit d
+// = round(S / Q^d) mod Q (centered). anchor = 1.5*2^(td+52) + 2^(td+t-1):
+// the round-to-nearest sum has ulp Q^d, its low mantissa bits are
+// round(S/Q^d) + Q/2, so the result is D_d + Q/2 in [0, Q); the Q/2 biases
+// are removed mod p in the epilogue (args.corr).
+template <bool BAL>
+__device__ __forceinline__ uint32_t block_digit_t(double acc, double anchor, uint32_t qmask) {
+  if (BAL) return (uint32_t)__double2loint(__dadd_rn(acc, anchor)) & qmask;
+  return block_digit(acc, anchor, qmask);
+}
+
+
 // EPI_DIGIT: K4 epilogue (int32 C = digit sums mod p). EPI_REDQ: K5 fused
 // REDQ of exact packed sums (pack.hpp:124-137). EPI_RAW: plain words.
 enum { EPI_DIGIT = 0, EPI_REDQ = 1, EPI_RAW = 2 };
@@ -366,7 +378,7 @@ struct DigitSums<true> {
 // blocks end after k-step MID-1 of every stage, i.e. they straddle stages.
 // MID < 0 (kb_stages == 1 only): blocks are stages and the flush is fused
 // into the first k-step of the next stage.
-template <int BK, int EPI, bool MULTI, int MID, bool TILED, bool PACK = false>
+template <int BK, int EPI, bool MULTI, int MID, bool TILED, bool PACK = false, bool SPLIT = false, bool BAL = false>
 __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint64_t* full, uint64_t* empty,
                                         int tiles_m, int tiles_n, int my_tiles, int ktiles, bool nomem) {
   using G = Geo<BK>;
@@ -420,8 +432,8 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
                 // d leaves each accumulator right before that accumulator's
                 // first DMMA of the new block (C = 0), so the integer work of
                 // the flush interleaves with DMMAs that keep the pipe busy
-                ds.add(mi, ni, block_digit(acc[mi][ni][0], args.anchor, args.qmask),
-                       block_digit(acc[mi][ni][1], args.anchor, args.qmask));
+                ds.add(mi, ni, block_digit_t<BAL>(acc[mi][ni][0], args.anchor, args.qmask),
+                       block_digit_t<BAL>(acc[mi][ni][1], args.anchor, args.qmask));
                 dmma_zc(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
               } else {
                 dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
@@ -430,11 +442,11 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
           if (MULTI && MID > 0 && kk == MID - 1) {  // compile-time position: no branch in the DMMA stream
             asm volatile("" ::: "memory");  // keep the next fragment loads below the flush (register pressure)
 #pragma unroll
-            for (int mi = 0; mi < MI; ++mi)
+            for (int mi = (SPLIT ? 1 : 0); mi < MI; mi += (SPLIT ? 2 : 1))
 #pragma unroll
               for (int ni = 0; ni < NI; ++ni) {
-                ds.add(mi, ni, block_digit(acc[mi][ni][0], args.anchor, args.qmask),
-                       block_digit(acc[mi][ni][1], args.anchor, args.qmask));
+                ds.add(mi, ni, block_digit_t<BAL>(acc[mi][ni][0], args.anchor, args.qmask),
+                       block_digit_t<BAL>(acc[mi][ni][1], args.anchor, args.qmask));
                 acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
               }
           }
@@ -446,22 +458,23 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
         slot = 0;
         phase ^= 1;
       }
-      if (MULTI && MID == 0) {  // (MID != 0 flushes inside the unrolled k-steps)
-        if (++kst == args.kb_stages) {
+      if (MULTI && (MID == 0 || SPLIT)) {  // (MID != 0 flushes inside the unrolled k-steps)
+        if (SPLIT || ++kst == args.kb_stages) {  // SPLIT (kb_stages == 1): even accumulator rows end here
           kst = 0;
           ++nflush;
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
+          for (int mi = 0; mi < MI; mi += (SPLIT ? 2 : 1))
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
-              ds.add(mi, ni, block_digit(acc[mi][ni][0], args.anchor, args.qmask),
-                     block_digit(acc[mi][ni][1], args.anchor, args.qmask));
+              ds.add(mi, ni, block_digit_t<BAL>(acc[mi][ni][0], args.anchor, args.qmask),
+                     block_digit_t<BAL>(acc[mi][ni][1], args.anchor, args.qmask));
               acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
             }
         }
       } else if (MULTI) {
         ++nflush;
       }
+      (void)kst;
       if (PACK && nflush >= args.pack_period) {  // keep both 16-bit lanes below 2^16
         ds.reduce(modp);
         nflush = 0;
@@ -477,7 +490,8 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
         if (EPI == EPI_DIGIT) {
           uint32_t r[2];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) r[h] = block_digit(acc[mi][ni][h], args.anchor, args.qmask) + ds.get(mi, ni, h);
+          for (int h = 0; h < 2; ++h)
+            r[h] = block_digit_t<BAL>(acc[mi][ni][h], args.anchor, args.qmask) + ds.get(mi, ni, h) + (BAL ? args.corr : 0u);
           if (row < M && col < N) {  // N even: col < N implies col + 1 < N
             int32_t* dst = args.c + (size_t)row * args.ldc + col;
             if (args.accumulate) {
@@ -597,7 +611,7 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_bulk(GemmArgs args, int ti
 // zero padded at pack time, so a stage is exactly two cp.async.bulk copies of
 // 128*BK*8 bytes (28 KiB at BK = 28) and there is no ragged-edge handling
 // left in the kernel. Same warpgroup split and consumers as k_gemm_bulk.
-template <int BK, int EPI, bool MULTI, int FLUSH>
+template <int BK, int EPI, bool MULTI, int FLUSH, bool BAL>
 __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int tiles_m, int tiles_n) {
   using GT = GeoT<BK>;
   constexpr int S = GT::STAGES;
@@ -647,14 +661,16 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int t
   // FLUSH (multi-block): 0 = at stage ends; for kb_stages == 1 also
   // 1 = staggered (warps 4..7 cut mid-stage; two inlined consumer bodies, so
   // instantiated separately) and 2 = fused into the next stage's first k-step.
-  if (FLUSH == 2)  // fused flush with packed digit sums (t <= 16)
-    consume<BK, EPI, MULTI, -1, true, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+  if (FLUSH == 3)  // split phases: odd accumulator rows flush mid-stage, even rows at stage ends
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, false, true, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+  else if (FLUSH == 2)  // fused flush with packed digit sums (t <= 16)
+    consume<BK, EPI, MULTI, -1, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
   else if (FLUSH == 1 && warp >= 4)
-    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
   else if (FLUSH == 1)
-    consume<BK, EPI, MULTI, 0, true, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, 0, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
   else
-    consume<BK, EPI, MULTI, 0, true>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, 0, true, false, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
 }
 
 // Reference-semantics contraction (DoubleWord::high_part, word.hpp:28-30):
@@ -818,10 +834,10 @@ static cudaError_t launch_digit_bulk(const GemmArgs& a, int bk, cudaStream_t s) 
 }
 
 static int num_sms();
-template <int BK, int EPI, bool MULTI, int FLUSH>
+template <int BK, int EPI, bool MULTI, int FLUSH, bool BAL>
 static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   using GT = GeoT<BK>;
-  auto k = k_gemm_tiled<BK, EPI, MULTI, FLUSH>;
+  auto k = k_gemm_tiled<BK, EPI, MULTI, FLUSH, BAL>;
   const size_t smem = GT::SMEM + 2 * GT::STAGES * sizeof(uint64_t);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err) return err;
@@ -832,41 +848,57 @@ static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   const char* dbg = getenv("QG_DEBUG_MODE");
   a2.debug = dbg ? atoi(dbg) : 0;
   // warps 4..7 start 4 us late so the two warps of an SMSP do not flush their
-  // k-blocks at the same moment (+3% on config 2, profiles/r01_notes.md)
+  // k-blocks at the same moment (profiles/r01_notes.md)
   const char* skew = getenv("QG_SKEW_NS");
   a2.skew_ns = skew ? (unsigned)atoi(skew) : (a.kb_stages ? 4000u : 0u);
+  if (BAL) {  // remove the Q/2 bias of every digit extraction (mod p)
+    const unsigned long long ktiles = (unsigned long long)((a.K + BK - 1) / BK);
+    const unsigned long long nb = !MULTI ? 1ull : (FLUSH == 0 ? ktiles / a.kb_stages + 1 : ktiles + 1);
+    const unsigned long long halfq = ((unsigned long long)a.qmask + 1) / 2;
+    a2.corr = (uint32_t)((a.p - (nb % a.p) * (halfq % a.p) % a.p) % a.p);
+  }
   k<<<grid, NT + 128, smem, s>>>(a2, tiles_m, tiles_n);
   count_launch();
   return cudaGetLastError();
 }
 
-template <int BK>
+template <int BK, bool BAL>
 static cudaError_t launch_tiled_bk(const GemmArgs& a, int flush, cudaStream_t s) {
   const char* dbg = getenv("QG_DEBUG_MODE");  // bit 2: time without flushes (wrong digits)
-  if (a.kb_stages == 0 || (dbg && (atoi(dbg) & 4))) return launch_tiled_one<BK, EPI_DIGIT, false, 0>(a, s);
-  if (a.kb_stages == 1 && flush == 2 && a.pack_period >= 1) return launch_tiled_one<BK, EPI_DIGIT, true, 2>(a, s);
-  if (a.kb_stages == 1 && flush == 1 && BK >= 8 && a.pack_period >= 1)
-    return launch_tiled_one<BK, EPI_DIGIT, true, (BK >= 8 ? 1 : 0)>(a, s);
-  return launch_tiled_one<BK, EPI_DIGIT, true, 0>(a, s);
+  if (a.kb_stages == 0 || (dbg && (atoi(dbg) & 4))) return launch_tiled_one<BK, EPI_DIGIT, false, 0, BAL>(a, s);
+  if (a.kb_stages == 1 && flush == 3 && BK >= 8) return launch_tiled_one<BK, EPI_DIGIT, true, (BK >= 8 ? 3 : 0), BAL>(a, s);
+  if (!BAL && a.kb_stages == 1 && flush == 2 && a.pack_period >= 1) return launch_tiled_one<BK, EPI_DIGIT, true, 2, false>(a, s);
+  if (!BAL && a.kb_stages == 1 && flush == 1 && BK >= 8 && a.pack_period >= 1)
+    return launch_tiled_one<BK, EPI_DIGIT, true, (BK >= 8 ? 1 : 0), false>(a, s);
+  return launch_tiled_one<BK, EPI_DIGIT, true, 0, BAL>(a, s);
+}
+
+template <int BK>
+static cudaError_t launch_tiled_b(const GemmArgs& a, int flush, cudaStream_t s) {
+  return a.balanced ? launch_tiled_bk<BK, true>(a, flush, s) : launch_tiled_bk<BK, false>(a, flush, s);
 }
 
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
-  static thread_local char name[64];
-  // 0 = flush at stage ends (default), 1 = staggered, 2 = fused into the next
-  // stage's first k-step; measured equal within noise on B200, 0 spills least.
+  static thread_local char name[80];
+  // k-block flush placement for one-stage blocks: 3 = split phases (default:
+  // odd accumulator rows mid-stage, even rows at stage ends), 0 = stage ends,
+  // 1 = staggered warps, 2 = fused into the next stage's first k-step
   const char* e = getenv("QG_FLUSH");
-  const int flush = e ? atoi(e) : 0;
-  static const char* kFlush[] = {"", "_stagger", "_fused"};
-  snprintf(name, sizeof name, "dot_tiled_bk%d_%s%s", bk, a.kb_stages ? "multiblock" : "singleblock",
-           (a.kb_stages == 1 && (flush == 1 || (flush == 2 && a.pack_period >= 1))) ? kFlush[flush] : "");
+  const int flush = e ? atoi(e) : 3;
+  static const char* kFlush[] = {"", "_stagger", "_fused", "_split"};
+  const bool named = a.kb_stages == 1 && flush >= 1 && flush <= 3 && (flush == 3 || !a.balanced);
+  snprintf(name, sizeof name, "dot_tiled_bk%d_%s%s%s", bk, a.kb_stages ? "multiblock" : "singleblock",
+           named ? kFlush[flush] : "", a.balanced ? "_balanced" : "");
   *variant = name;
   switch (bk) {
-    case 36: return launch_tiled_bk<36>(a, flush, s);
-    case 28: return launch_tiled_bk<28>(a, flush, s);
-    case 20: return launch_tiled_bk<20>(a, flush, s);
-    case 12: return launch_tiled_bk<12>(a, flush, s);
-    case 4: return launch_tiled_bk<4>(a, flush, s);
+    case 52: return launch_tiled_b<52>(a, flush, s);
+    case 44: return launch_tiled_b<44>(a, flush, s);
+    case 36: return launch_tiled_b<36>(a, flush, s);
+    case 28: return launch_tiled_b<28>(a, flush, s);
+    case 20: return launch_tiled_b<20>(a, flush, s);
+    case 12: return launch_tiled_b<12>(a, flush, s);
+    case 4: return launch_tiled_b<4>(a, flush, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -47,6 +47,8 @@ struct GemmArgs {
   int debug;            // experiments only (QG_DEBUG_MODE)
   int pack_period;      // packed digit sums: reduce both 16-bit lanes every this many flushes
   unsigned skew_ns;     // start delay of warps 4..7 (desynchronises the flushes of SMSP warp pairs)
+  int balanced;         // balanced (signed) digits: round-to-nearest extraction, biased by Q/2
+  uint32_t corr;        // balanced: (p - (#extractions * Q/2) mod p) mod p, added in the epilogue
 };
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
@@ -54,7 +56,8 @@ cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, cons
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 // Tiled packings: A (m x k residues) -> CA_t, B (k x n residues) -> CB_t.
 cudaError_t launch_pack_tiled(bool b_operand, const void* src, int dtype, size_t rows, size_t cols,
-                              size_t ld, int t, int e, int bk, double* dst, cudaStream_t s);
+                              size_t ld, int t, int e, int bk, double* dst, cudaStream_t s,
+                              uint32_t p = 0, bool balanced = false);
 
 // Reference high-part semantics (word.hpp:28-30): acc += trunc(a*b*2^-td).
 struct HighArgs {

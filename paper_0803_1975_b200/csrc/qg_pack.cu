@@ -106,9 +106,15 @@ __global__ void k_pack_outer_cols(const TIn* __restrict__ b, size_t rows, size_t
 // pipeline stage of the contraction is one contiguous chunk per operand.
 //   CA_t[tm][kt][r][c] = CA[128 tm + r][BK kt + c]   (compress_rows_reversed words)
 //   CB_t[tn][kt][r][c] = CB[BK kt + c][128 tn + r]   (compress_cols_forward words, transposed)
-template <typename TIn, int BK>
+// Balanced digits (qg_gpu_plan.balanced): residue v enters as v - p when
+// v > p/2, so the words are signed integers (exact in double).
+__device__ __forceinline__ long long balanced_digit(uint64_t v, uint32_t p) {
+  return v > (p >> 1) ? (long long)v - (long long)p : (long long)v;
+}
+
+template <typename TIn, int BK, bool BAL>
 __global__ void k_pack_a_tiled(const TIn* __restrict__ a, size_t m, size_t k, size_t lda, int t, int e,
-                               unsigned Kt, size_t total, double* __restrict__ ca_t) {
+                               unsigned Kt, size_t total, double* __restrict__ ca_t, uint32_t p) {
   const size_t K = (k + e - 1) / e;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
@@ -118,41 +124,68 @@ __global__ void k_pack_a_tiled(const TIn* __restrict__ a, size_t m, size_t k, si
     const size_t rest2 = rest >> 7;
     const size_t kt = rest2 % Kt, tm = rest2 / Kt;
     const size_t row = tm * 128 + r, gw = kt * BK + c;
-    uint64_t w = 0;
-    if (row < m && gw < K) {
-      const size_t base = gw * e;
-      const int len = (int)((k - base) < (size_t)e ? (k - base) : (size_t)e);
-      const TIn* src = a + row * lda + base;
-      for (int s = 0; s < len; ++s) w = (w << t) | residue_bits(src[s]);
-      w <<= t * (e - len);
+    if (BAL) {
+      long long w = 0;
+      if (row < m && gw < K) {
+        const size_t base = gw * e;
+        const int len = (int)((k - base) < (size_t)e ? (k - base) : (size_t)e);
+        const TIn* src = a + row * lda + base;
+        for (int s = 0; s < len; ++s) w = w * (1ll << t) + balanced_digit(residue_bits(src[s]), p);
+        w *= 1ll << (t * (e - len));
+      }
+      ca_t[idx] = __ll2double_rn(w);
+    } else {
+      uint64_t w = 0;
+      if (row < m && gw < K) {
+        const size_t base = gw * e;
+        const int len = (int)((k - base) < (size_t)e ? (k - base) : (size_t)e);
+        const TIn* src = a + row * lda + base;
+        for (int s = 0; s < len; ++s) w = (w << t) | residue_bits(src[s]);
+        w <<= t * (e - len);
+      }
+      ca_t[idx] = __ull2double_rn(w);
     }
-    ca_t[idx] = __ull2double_rn(w);
   }
 }
 
-template <typename TIn, int BK>
-__global__ void __launch_bounds__(128) k_pack_b_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
-                                                      int t, int e, unsigned Kt, double* __restrict__ cb_t) {
-  __shared__ double tile[128 * (BK + 1)];
+template <typename TIn, int BK, bool BAL>
+__global__ void __launch_bounds__(64) k_pack_b_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
+                                                     int t, int e, unsigned Kt, double* __restrict__ cb_t,
+                                                     uint32_t p) {
+  // one block = 64 of the 128 rows (n) of one CB_t chunk (tn, kt): coalesced
+  // reads along n, the chunk half written contiguously through shared memory
+  __shared__ double tile[64 * (BK + 1)];
   const size_t K = (k + e - 1) / e;
-  const size_t blk = blockIdx.x;
+  const size_t blk = blockIdx.x >> 1, half = blockIdx.x & 1;
   const size_t kt = blk % Kt, tn = blk / Kt;
   const int r = threadIdx.x;
-  const size_t col = tn * 128 + r;
+  const size_t col = tn * 128 + half * 64 + r;
 #pragma unroll 4
   for (int c = 0; c < BK; ++c) {
     const size_t gw = kt * BK + c;
-    uint64_t w = 0;
-    if (col < n && gw < K) {
-      const size_t base = gw * e;
-      const int len = (int)((k - base) < (size_t)e ? (k - base) : (size_t)e);
-      for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(b[(base + s) * ldb + col]);
+    double wd;
+    if (BAL) {
+      long long w = 0;
+      if (col < n && gw < K) {
+        const size_t base = gw * e;
+        const int len = (int)((k - base) < (size_t)e ? (k - base) : (size_t)e);
+        for (int s = len - 1; s >= 0; --s) w = w * (1ll << t) + balanced_digit(residue_bits(b[(base + s) * ldb + col]), p);
+      }
+      wd = __ll2double_rn(w);
+    } else {
+      uint64_t w = 0;
+      if (col < n && gw < K) {
+        const size_t base = gw * e;
+        const int len = (int)((k - base) < (size_t)e ? (k - base) : (size_t)e);
+        for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(b[(base + s) * ldb + col]);
+      }
+      wd = __ull2double_rn(w);
     }
-    tile[r * (BK + 1) + c] = __ull2double_rn(w);
+    tile[r * (BK + 1) + c] = wd;
   }
   __syncthreads();
-  double* out = cb_t + blk * (size_t)(128 * BK);
-  for (int i = r; i < 128 * BK; i += 128) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
+  double* out = cb_t + blk * (size_t)(128 * BK) + half * (size_t)(64 * BK);
+  for (int i = r; i < 64 * BK; i += 64) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
 }
 
 // redq over a buffer, pack.hpp:124-137: every base-Q digit replaced by itself
@@ -301,46 +334,56 @@ cudaError_t launch_pack(int kind, const void* src, int dtype, size_t rows, size_
 }
 
 
-template <typename TIn, int BK>
+template <typename TIn, int BK, bool BAL>
 static cudaError_t pack_tiled_t(bool b_operand, const TIn* src, size_t rows, size_t cols, size_t ld, int t,
-                                int e, double* dst, cudaStream_t s) {
+                                int e, double* dst, cudaStream_t s, uint32_t p) {
   if (b_operand) {  // src is k x n; blocks over (n, k-words)
     const size_t K = (rows + e - 1) / e;
     const unsigned Kt = (unsigned)((K + BK - 1) / BK);
     const size_t Nt = (cols + 127) / 128;
     if (Kt == 0 || Nt == 0) return cudaSuccess;
-    k_pack_b_tiled<TIn, BK><<<(unsigned)(Nt * Kt), 128, 0, s>>>(src, rows, cols, ld, t, e, Kt, dst);
+    k_pack_b_tiled<TIn, BK, BAL><<<(unsigned)(Nt * Kt * 2), 64, 0, s>>>(src, rows, cols, ld, t, e, Kt, dst, p);
   } else {  // src is m x k
     const size_t K = (cols + e - 1) / e;
     const unsigned Kt = (unsigned)((K + BK - 1) / BK);
     const size_t Mt = (rows + 127) / 128;
     const size_t total = Mt * Kt * 128 * (size_t)BK;
     if (total == 0) return cudaSuccess;
-    k_pack_a_tiled<TIn, BK><<<grid1d(total, 256), 256, 0, s>>>(src, rows, cols, ld, t, e, Kt, total, dst);
+    k_pack_a_tiled<TIn, BK, BAL><<<grid1d(total, 256), 256, 0, s>>>(src, rows, cols, ld, t, e, Kt, total, dst, p);
   }
   count_launch();
   return cudaGetLastError();
 }
 
-template <typename TIn>
+template <typename TIn, bool BAL>
 static cudaError_t pack_tiled_bk(bool b_operand, const TIn* src, size_t rows, size_t cols, size_t ld, int t,
-                                 int e, int bk, double* dst, cudaStream_t s) {
+                                 int e, int bk, double* dst, cudaStream_t s, uint32_t p) {
   switch (bk) {
-    case 36: return pack_tiled_t<TIn, 36>(b_operand, src, rows, cols, ld, t, e, dst, s);
-    case 28: return pack_tiled_t<TIn, 28>(b_operand, src, rows, cols, ld, t, e, dst, s);
-    case 20: return pack_tiled_t<TIn, 20>(b_operand, src, rows, cols, ld, t, e, dst, s);
-    case 12: return pack_tiled_t<TIn, 12>(b_operand, src, rows, cols, ld, t, e, dst, s);
-    case 4: return pack_tiled_t<TIn, 4>(b_operand, src, rows, cols, ld, t, e, dst, s);
+    case 52: return pack_tiled_t<TIn, 52, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
+    case 44: return pack_tiled_t<TIn, 44, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
+    case 36: return pack_tiled_t<TIn, 36, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
+    case 28: return pack_tiled_t<TIn, 28, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
+    case 20: return pack_tiled_t<TIn, 20, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
+    case 12: return pack_tiled_t<TIn, 12, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
+    case 4: return pack_tiled_t<TIn, 4, BAL>(b_operand, src, rows, cols, ld, t, e, dst, s, p);
   }
   return cudaErrorInvalidValue;
 }
 
+template <typename TIn>
+static cudaError_t pack_tiled_dt(bool b_operand, const TIn* src, size_t rows, size_t cols, size_t ld, int t,
+                                 int e, int bk, double* dst, cudaStream_t s, uint32_t p, bool balanced) {
+  return balanced ? pack_tiled_bk<TIn, true>(b_operand, src, rows, cols, ld, t, e, bk, dst, s, p)
+                  : pack_tiled_bk<TIn, false>(b_operand, src, rows, cols, ld, t, e, bk, dst, s, p);
+}
+
 cudaError_t launch_pack_tiled(bool b_operand, const void* src, int dtype, size_t rows, size_t cols,
-                              size_t ld, int t, int e, int bk, double* dst, cudaStream_t s) {
+                              size_t ld, int t, int e, int bk, double* dst, cudaStream_t s, uint32_t p,
+                              bool balanced) {
   switch (dtype) {
-    case 0: return pack_tiled_bk<double>(b_operand, (const double*)src, rows, cols, ld, t, e, bk, dst, s);
-    case 1: return pack_tiled_bk<uint32_t>(b_operand, (const uint32_t*)src, rows, cols, ld, t, e, bk, dst, s);
-    default: return pack_tiled_bk<int32_t>(b_operand, (const int32_t*)src, rows, cols, ld, t, e, bk, dst, s);
+    case 0: return pack_tiled_dt<double>(b_operand, (const double*)src, rows, cols, ld, t, e, bk, dst, s, p, balanced);
+    case 1: return pack_tiled_dt<uint32_t>(b_operand, (const uint32_t*)src, rows, cols, ld, t, e, bk, dst, s, p, balanced);
+    default: return pack_tiled_dt<int32_t>(b_operand, (const int32_t*)src, rows, cols, ld, t, e, bk, dst, s, p, balanced);
   }
 }
 

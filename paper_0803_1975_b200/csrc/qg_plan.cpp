@@ -131,19 +131,76 @@ uint64_t max_exact_block(uint32_t p, int t, int e) {
 // with tools/plan_sweep.py, profiles/r01_plan_sweep_*.jsonl: short stages pay
 // their fixed barrier/producer overhead over fewer words).
 static double stage_cost(int bk) {
+  // tiled kernel, profiles/r01_tiled_sweep_*.jsonl: stages of >= 20 words
+  // run at the same per-word speed; 12-word stages pay ~5 %, 4-word ~50 %
   switch (bk) {
+    case 52: return 1.02;  // two 104 KiB stages in flight only
+    case 44: return 1.02;
     case 36: return 1.0;
     case 32: return 1.0;
     case 28: return 1.0;
-    case 24: return 1.02;
-    case 20: return 1.03;
-    case 16: return 1.05;
-    case 12: return 1.1;
-    case 8: return 1.25;
+    case 24: return 1.01;
+    case 20: return 1.01;
+    case 16: return 1.03;
+    case 12: return 1.05;
+    case 8: return 1.2;
     default: return 1.5;
   }
 }
-constexpr double kFlushWords = 2.0;  // per-block flush overhead, in packed words
+constexpr double kFlushWords = 3.0;  // per-block flush overhead, in packed words (measured 2.5-3.4)
+
+// Eq. G for balanced digits: residues v > p/2 enter as
+// v - p, so |v| <= h = floor(p/2), every digit is signed and digit d is read
+// by rounding S / Q^d to nearest. Exact while |L| + err < Q^d / 2, with
+// L_max = sum_{s<d} min(Q/2 - 1, Kb n_s h^2) Q^s; the anchor of the
+// extraction needs |S| < 2^(td+50).
+uint64_t max_exact_block_balanced(uint32_t p, int t, int e) {
+  static std::mutex mu;
+  static std::map<std::tuple<uint32_t, int, int>, uint64_t> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({p, t, e});
+    if (it != cache.end()) return it->second;
+  }
+  const int d = e - 1;
+  const u128 Q = u128(1) << t;
+  const u128 Qd = u128(1) << (t * d);
+  const u128 h = p / 2;
+  const u128 h2 = h * h;
+  u128 amax = 0;
+  for (int i = 0; i < e; ++i) amax += h << (t * i);
+  const u128 xmax = amax * amax;
+  const u128 err_x = round_err(xmax);
+  u128 err = 0;
+  uint64_t best = 0;
+  const uint64_t cap = uint64_t(1) << 20;
+  for (uint64_t kb = 1; kb <= cap && t >= 2; ++kb) {
+    u128 L = 0;
+    for (int s = 0; s < d; ++s) {
+      const int ns = (s + 1) < (2 * d + 1 - s) ? (s + 1) : (2 * d + 1 - s);
+      u128 ds = u128(kb) * ns * h2;
+      if (ds > Q / 2 - 1) ds = Q / 2 - 1;
+      L += ds << (t * s);
+    }
+    const u128 smax = u128(kb) * xmax;
+    if (bitlen(smax) > 120) break;
+    err += round_err(smax) + err_x;
+    if (ulp_of(smax) > Qd) break;
+    if (2 * (L + err) >= Qd) break;
+    if ((smax >> (t * d)) >= (u128(1) << 50)) break;
+    best = kb;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{p, t, e}] = best;
+  return best;
+}
+
+// Eq. 3 for balanced digits: a block may hold at most this many residues.
+uint64_t largest_common_dim_balanced(uint32_t p, int t) {
+  const uint64_t h = p / 2;
+  if (t < 2 || h == 0) return 0;
+  return ((uint64_t(1) << (t - 1)) - 1) / (h * h);
+}
 
 // The contraction kernels flush k-blocks at pipeline-stage boundaries. The
 // tiled kernel (the main path) has stages of BK in {36, 28, 20, 12, 4} words,
@@ -175,8 +232,8 @@ uint64_t stage_block(uint64_t limit, int* bk) {
 }
 
 uint64_t stage_block_tiled(uint64_t limit, int* bk) {
-  static const int kSet[] = {36, 28, 20, 12, 4};
-  return stage_block_set(limit, bk, kSet, 5);
+  static const int kSet[] = {52, 44, 36, 28, 20, 12, 4};
+  return stage_block_set(limit, bk, kSet, 7);
 }
 
 // Predicted relative cost of a blocked plan, in packed-word units: words
@@ -184,7 +241,7 @@ uint64_t stage_block_tiled(uint64_t limit, int* bk) {
 // per-block flush cost.
 double blocked_cost(uint64_t k, int e, uint64_t kb_words, double flush_words) {
   const uint64_t K = (k + e - 1) / e;
-  if (kb_words >= K) return double((K + 31) / 32 * 32);
+  if (kb_words >= K) return double((K + 27) / 28 * 28);  // single block: 28-word stages
   int bk = 4;
   const uint64_t blk = stage_block_tiled(kb_words, &bk);
   if (blk == 0) return 1e300;
@@ -292,6 +349,14 @@ int qg_max_exact_block(const qg_plan* plan, uint64_t* words) {
   return QG_OK;
 }
 
+int qg_max_exact_block_balanced(const qg_plan* plan, uint64_t* words) {
+  if (!plan || !words) return QG_INVALID_ARGUMENT;
+  if (plan->p < 2 || !is_prime(plan->p)) return QG_INVALID_MODULUS;
+  if (plan->e < 1 || plan->t < 1 || plan->t * plan->e > 53) return QG_PLAN_MISMATCH;
+  *words = max_exact_block_balanced(plan->p, plan->t, plan->e);
+  return QG_OK;
+}
+
 int qg_gpu_plan_from(const qg_plan* plan, uint64_t k, qg_gpu_plan* out) {
   if (!plan || !out) return QG_INVALID_ARGUMENT;
   if (plan->p < 2 || !is_prime(plan->p)) return QG_INVALID_MODULUS;
@@ -314,7 +379,9 @@ int qg_gpu_plan_from(const qg_plan* plan, uint64_t k, qg_gpu_plan* out) {
   return QG_OK;
 }
 
-int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
+int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) { return qg_plan_gpu_ex(p, k, 0, out); }
+
+int qg_plan_gpu_ex(uint32_t p, uint64_t k, int flags, qg_gpu_plan* out) {
   if (!out) return QG_INVALID_ARGUMENT;
   if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
   if (k < 1) return QG_INVALID_ARGUMENT;
@@ -323,13 +390,15 @@ int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
   bool found = false;
   qg_gpu_plan best;
   std::memset(&best, 0, sizeof best);
+  const int max_bal = (flags & QG_PLAN_UNSIGNED_ONLY) ? 0 : 1;
+  for (int bal = 0; bal <= max_bal; ++bal)
   for (int t = 1; t < 53; ++t) {
-    const uint64_t km = largest_common_dim(p, t);
+    const uint64_t km = bal ? largest_common_dim_balanced(p, t) : largest_common_dim(p, t);
     if (km == 0) continue;
     const int cap = word_capacity(t, 53);
     for (int e = 1; e <= cap; ++e) {
       if (uint64_t(e) > k && e > 1) break;
-      const uint64_t exact = max_exact_block(p, t, e);
+      const uint64_t exact = bal ? max_exact_block_balanced(p, t, e) : max_exact_block(p, t, e);
       uint64_t kb = exact;
       if (k > km) {
         const uint64_t lim = km / uint64_t(e);
@@ -341,14 +410,16 @@ int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out) {
       if (kb == 0 || (kb < 4 && kb < K)) continue;
       const uint64_t nblocks = (K + kb - 1) / kb;
       // digit sums of all blocks must fit the kernel's uint32 accumulator
-      if (u128(nblocks) * ((u128(1) << t) - 1) >= (u128(1) << 32)) continue;
+      if (u128(nblocks + 1) * ((u128(1) << t) - 1) + p >= (u128(1) << 32)) continue;
       const double cost = blocked_cost(k, e, kb, flush_words);
       if (cost < best_cost - 1e-9) {
         best_cost = cost;
         found = true;
         fill(&best.plan, p, t, e, 53, std::ldexp(1.0, -t * (e - 1)));
+        if (bal) best.plan.kmax = km;  // Eq. 3 bound of the balanced digits
         best.kblock_words = kb;
         best.max_exact_words = exact;
+        best.balanced = bal;
       }
     }
   }

@@ -55,11 +55,13 @@ def test_config4_mixed_variant(qg, cuda):
 
 @pytest.mark.parametrize("planner", ["gpu", "reference"])
 def test_config5_row_shards(qg, cuda, planner):
+    """Row-layout operands (compress_rows_reversed / compress_cols_forward words)."""
     import torch
 
     g = GOLDEN["config5_rows"]
     p, m, k, n = g["p"], g["m"], g["k"], g["n"]
-    plan = qg.plan_compression(p, k) if planner == "reference" else qg.plan_gpu(p, k)
+    # reference-layout operands hold the reference's unsigned words
+    plan = qg.plan_compression(p, k) if planner == "reference" else qg.plan_gpu(p, k, balanced=False)
     base = plan.plan if isinstance(plan, qg.GpuPlan) else plan
     big = qg.CompressionPlan(base.p, base.t, base.d, base.e, base.beta, max(base.kmax, k), base.inv_qd, 0)
     b = qg.random_residue_matrix(k, n, p, 43)
@@ -72,6 +74,32 @@ def test_config5_row_shards(qg, cuda, planner):
         ca = qg.compress_rows_reversed(a, big)
         ca.plan = base
         c = qg.mul_common_compressed(ca, cb, plan)
+        assert qg.residue_checksum(c) == shard["checksum"], shard["row0"]
+        assert sha_u8(c) == shard["sha256_u8"], shard["row0"]
+    del cb
+    torch.cuda.empty_cache()
+
+
+def test_config5_row_shards_tiled(qg, cuda):
+    """Config 5 through the fast path (tiled layout, balanced GPU plan)."""
+    import torch
+
+    g = GOLDEN["config5_rows"]
+    p, m, k, n = g["p"], g["m"], g["k"], g["n"]
+    gp = qg.plan_gpu(p, k)
+    b = qg.random_residue_matrix(k, n, p, 43)
+    bk = qg.tiled_stage_words(gp, k)
+    cb = qg.pack_tiled(b, gp, bk, "b")
+    del b
+    import ctypes
+
+    for shard in g["shards"]:
+        a = qg.random_residue_matrix(shard["rows"], k, p, 42, row0=shard["row0"])
+        ca = qg.pack_tiled(a, gp, bk, "a")
+        c = torch.empty((shard["rows"], n), dtype=torch.int32, device=cuda)
+        gpc = gp._c()
+        qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca), qg._ptr(cb), shard["rows"], n, k,
+                                             qg._ptr(c), n, qg._stream()))
         assert qg.residue_checksum(c) == shard["checksum"], shard["row0"]
         assert sha_u8(c) == shard["sha256_u8"], shard["row0"]
     del cb

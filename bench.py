@@ -196,11 +196,15 @@ def load_json(path):
 
 
 def mixed_arm(args):
-    """Config 4: mixed / right-compressed variant (gemm.hpp:285-335). Step =
-    compress_outer_cols(B) (K3) + the DMMA contraction A x CBo with the fused
-    REDQ epilogue (K5) on device-resident residues; output CC (ReduceAndCompress
-    words). Plan: plan_compression(p, k) as run_bench uses (bench.hpp:149)."""
+    """Config 4: mixed / right-compressed variant (gemm.hpp:285-335) on the
+    tiled layout. Step = pack A's residues + compress_outer_cols(B) into tiled
+    blocks + the DMMA contraction with in-place REDQ between k-blocks and a
+    REDQ epilogue (K5) on device-resident residues; output CC words.
+    --plan gpu: plan_right_gpu (t=13, e=4, 504-residue blocks); --plan
+    reference: plan_compression(p, k) as run_bench uses (bench.hpp:149), CC
+    bit-identical to the reference's."""
     import ctypes
+    import hashlib
 
     import torch
 
@@ -209,11 +213,22 @@ def mixed_arm(args):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     p, m, k, n, desc = CONFIGS[args.config]
-    plan = qg.plan_compression(p, k)
+    if args.plan == "reference":
+        base = qg.plan_compression(p, k)
+        gp = qg.GpuPlan(base, k, k, 0)
+    else:
+        gp = qg.plan_right_gpu(p, k, n)
+    plan = gp.plan
     H = -(-n // plan.e)
+    g = gp._c()
+    bk_c = ctypes.c_uint32()
+    qg._check(qg.lib.qg_right_tiled_stage(ctypes.byref(g), k, ctypes.byref(bk_c)))
+    bk = bk_c.value
+    kt = -(-k // bk)
     a = qg.random_residue_matrix(m, k, p, SEED)
     b = qg.random_residue_matrix(k, n, p, SEED + 1)
-    cbo = torch.empty((k, H), dtype=torch.float64, device=dev)
+    a_t = torch.empty(-(-m // 128) * 128 * kt * bk, dtype=torch.float64, device=dev)
+    bo_t = torch.empty(-(-H // 128) * 128 * kt * bk, dtype=torch.float64, device=dev)
     cc = torch.empty((m, H), dtype=torch.float64, device=dev)
     pl = plan._c()
     sp = qg._stream
@@ -221,10 +236,11 @@ def mixed_arm(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
     def step(ev=None):
-        qg._check(qg.lib.qg_compress_outer_cols(ctypes.byref(pl), qg._ptr(b), 0, k, n, n, qg._ptr(cbo), H, sp()))
+        qg._check(qg.lib.qg_pack_residues_tiled(bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
+        qg._check(qg.lib.qg_pack_outer_cols_tiled(ctypes.byref(pl), bk, qg._ptr(b), 0, k, n, n, qg._ptr(bo_t), sp()))
         if ev:
             ev[0].record(stream)
-        qg._check(qg.lib.qg_mul_right(ctypes.byref(pl), qg._ptr(a), k, qg._ptr(cbo), m, k, n, qg._ptr(cc), sp()))
+        qg._check(qg.lib.qg_mul_right_tiled(ctypes.byref(g), qg._ptr(a_t), qg._ptr(bo_t), m, k, n, qg._ptr(cc), H, sp()))
         if ev:
             ev[1].record(stream)
 
@@ -248,17 +264,18 @@ def mixed_arm(args):
     kms = sum(kern_ms) / len(kern_ms)
     flop = 2.0 * m * H * k
     peak = float((load_json(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) or {}).get("dmma_m8n8k4_tflops", 37.09))
-    words = cc.cpu().numpy().view("uint64")
-    import hashlib
-
+    c = qg.uncompress(qg.CompressedMatrix(m, n, m, H, qg.PackOrientation(0, 1, plan.e), plan, cc))
     line = {"metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": 2.0 * m * n * k / (ms * 1e-3),
             "unit": "mult-adds/s (2mnk/s)", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n, "plan": {"t": plan.t, "e": plan.e}},
+            "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n,
+                       "plan": {"t": plan.t, "e": plan.e, "kblock_residues": gp.kblock_words, "stage_words": bk,
+                                "source": args.plan}},
             "roofline": {"bound": "tensor", "achieved": round(flop / (kms * 1e-3) / 1e12, 3), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(flop / (kms * 1e-3) / 1e12 / peak, 4), "traffic": None, "kernel": qg.last_kernel(),
                          "kernel_ms": round(kms, 4)},
-            "gpu_launches": qg.kernel_launches() - launches0, "cc_sha256": hashlib.sha256(words.tobytes()).hexdigest(),
+            "gpu_launches": qg.kernel_launches() - launches0, "checksum_c": qg.residue_checksum(c),
+            "cc_sha256": hashlib.sha256(cc.cpu().numpy().view("uint64").tobytes()).hexdigest(),
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     return 0

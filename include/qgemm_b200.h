@@ -179,6 +179,22 @@ int qg_pack_b_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* b, qg_dty
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m,
                         size_t n, size_t k, int32_t* c, size_t ldc, void* stream);
 
+/* ---- mixed variant on the tiled layout (the B200 fast path of
+ * mul_right_compressed). A's residues as dense 128 x BK blocks (e = 1), B's
+ * compress_outer_cols words transposed into 128 x BK blocks; the contraction
+ * REDQs the exact accumulators in place between k-blocks of
+ * gplan->kblock_words residues (qg_plan_right_gpu) and in its epilogue.
+ * cc: m x ceil(n/e) words, bit-identical to mul_right_compressed's under the
+ * same plan. */
+int qg_plan_right_gpu(uint32_t p, uint64_t k, uint64_t n, qg_gpu_plan* out);
+int qg_right_tiled_stage(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk);
+int qg_pack_residues_tiled(uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k, size_t lda,
+                           double* a_t, void* stream);
+int qg_pack_outer_cols_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k,
+                             size_t n, size_t ldb, double* bo_t, void* stream);
+int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double* bo_t, size_t m, size_t k,
+                       size_t n, double* cc, size_t ldcc, void* stream);
+
 /* packed_right_product + redq_in_place = mul_right_compressed(a, cb),
  * gemm.hpp:285-325: CC = REDQ(A x CBo). A: m x k residues as double (lda),
  * CBo: k x ceil(n/e) words. cc: m x ceil(n/e). */

@@ -173,6 +173,11 @@ def _load():
         "qg_pack_a_tiled": ([P(_GpuPlan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_pack_b_tiled": ([P(_GpuPlan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_mul_common_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_plan_right_gpu": ([u32, u64, u64, P(_GpuPlan)], i32),
+        "qg_right_tiled_stage": ([P(_GpuPlan), u64, P(u32)], i32),
+        "qg_pack_residues_tiled": ([u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_outer_cols_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_mul_right_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),
@@ -648,6 +653,42 @@ def redq_in_place(cm: CompressedMatrix) -> None:
     """gemm.hpp:313-316."""
     pl = cm.plan._c()
     _check(lib.qg_redq(ctypes.byref(pl), _ptr(cm.data), cm.data.numel(), _stream()))
+
+
+def plan_right_gpu(p: int, k: int, n: int) -> GpuPlan:
+    """(t, e, k-block in residues) for the mixed variant on the tensor-core path."""
+    out = _GpuPlan()
+    _check(lib.qg_plan_right_gpu(p, k, n, ctypes.byref(out)))
+    return GpuPlan._from(out)
+
+
+def mul_right_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMatrix:
+    """mul_right_compressed(A, compress_outer_cols(B, plan)) on residue
+    tensors through the tiled layout and the blocked mixed contraction. With a
+    CompressionPlan the words equal the reference's bit for bit; a GpuPlan from
+    plan_right_gpu may block k past plan.kmax (in-place REDQ between blocks)."""
+    torch = _torch()
+    _require_cuda(a, b)
+    m, k = a.shape
+    n = b.shape[1]
+    if b.shape[0] != k:
+        raise DimensionMismatch(f"inner dimensions disagree: {m}x{k} times {b.shape[0]}x{n}")
+    gp = plan if isinstance(plan, GpuPlan) else GpuPlan(plan, k, k, 0)
+    pl = gp.plan
+    g = gp._c()
+    bk = ctypes.c_uint32()
+    _check(lib.qg_right_tiled_stage(ctypes.byref(g), k, ctypes.byref(bk)))
+    bk = bk.value
+    H = (n + pl.e - 1) // pl.e
+    kt = -(-k // bk)
+    a_t = torch.empty(-(-m // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
+    bo_t = torch.empty(-(-H // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
+    _check(lib.qg_pack_residues_tiled(bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(a_t), _stream()))
+    c_pl = pl._c()
+    _check(lib.qg_pack_outer_cols_tiled(ctypes.byref(c_pl), bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(bo_t), _stream()))
+    cc = torch.empty((m, H), dtype=torch.float64, device=a.device)
+    _check(lib.qg_mul_right_tiled(ctypes.byref(g), _ptr(a_t), _ptr(bo_t), m, k, n, _ptr(cc), H, _stream()))
+    return CompressedMatrix(m, n, m, H, PackOrientation(PackDirection.Forward, PackAxis.Column, pl.e), pl, cc)
 
 
 def residue_checksum(c) -> int:

@@ -200,6 +200,89 @@ int qg_pack_b_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* b, qg_dty
                                             as_stream(stream), plan->p, gplan->balanced != 0));
 }
 
+// ---- mixed variant on the tiled layout
+static int right_tiled_geometry(const qg_gpu_plan* gp, uint64_t k, int* bk, int* kb_stages) {
+  const uint64_t kb = gp->kblock_words;
+  if (kb == 0) return QG_INVALID_ARGUMENT;
+  if (kb >= k) {
+    *bk = 28;
+    *kb_stages = 0;
+    return QG_OK;
+  }
+  const uint64_t blk = qg::stage_block_tiled(kb, bk);
+  if (blk < 4) return QG_INVALID_ARGUMENT;
+  *kb_stages = (int)(blk / *bk);
+  return QG_OK;
+}
+
+int qg_right_tiled_stage(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk) {
+  if (!gplan || !bk) return QG_INVALID_ARGUMENT;
+  int b = 0, kbs = 0;
+  int st = right_tiled_geometry(gplan, k, &b, &kbs);
+  if (st) return st;
+  *bk = (uint32_t)b;
+  return QG_OK;
+}
+
+int qg_pack_residues_tiled(uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k, size_t lda, double* a_t,
+                           void* stream) {
+  int st = check_dtype(dtype);
+  if (st) return st;
+  if (lda < k) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_tiled(false, a, dtype, m, k, lda, 1, 1, (int)bk, a_t, as_stream(stream)));
+}
+
+int qg_pack_outer_cols_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+                             size_t ldb, double* bo_t, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (ldb < n) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_outer_tiled(b, dtype, k, n, ldb, plan->t, plan->e, (int)bk, bo_t,
+                                                  as_stream(stream)));
+}
+
+int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double* bo_t, size_t m, size_t k,
+                       size_t n, double* cc, size_t ldcc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if (pl.t * pl.e > 53) return QG_PLAN_MISMATCH;  // sums must stay exact
+  const uint64_t pm = (uint64_t)(pl.p - 1) * (pl.p - 1);
+  const uint64_t Q = 1ull << pl.t;
+  int bk = 0, kbs = 0;
+  if ((st = right_tiled_geometry(gplan, k, &bk, &kbs))) return st;
+  if (kbs == 0) {
+    if (k > pl.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
+  } else if ((pl.p - 1) + (uint64_t)kbs * bk * pm >= Q) {
+    return QG_PLAN_MISMATCH;  // a block would overflow a digit after the in-place REDQ
+  }
+  const size_t H = ceil_div(n, pl.e);
+  if (ldcc < H) return QG_INVALID_ARGUMENT;
+  if (m == 0 || H == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  if (k == 0) {
+    for (size_t i = 0; i < m; ++i)
+      if (cudaMemsetAsync(cc + i * ldcc, 0, H * sizeof(double), s) != cudaSuccess) return QG_CUDA_ERROR;
+    return QG_OK;
+  }
+  qgk::GemmArgs r;
+  std::memset(&r, 0, sizeof r);
+  r.a = a_t;
+  r.b = bo_t;
+  r.M = (int)m;
+  r.N = (int)H;
+  r.K = (int)k;
+  r.kb_stages = kbs;
+  r.t = pl.t;
+  r.e = pl.e;
+  r.p = pl.p;
+  r.cc = cc;
+  r.ldcc = ldcc;
+  return cuda_status(qgk::launch_right_tiled(r, bk, true, s, &g_last_kernel));
+}
+
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,
                         size_t k, int32_t* c, size_t ldc, void* stream) {
   if (!gplan) return QG_INVALID_ARGUMENT;
@@ -651,24 +734,34 @@ int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
                       size_t k, size_t n, double* cc) {
   int st = check_plan(plan);
   if (st) return st;
-  if (k > plan->kmax) return QG_PLAN_MISMATCH;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
   cudaStream_t s = nullptr;
   const size_t H = ceil_div(n, plan->e);
-  DevBuf da32(s), dad(s), db(s), dcb(s), dcc(s);
-  QG_TRY(da32.alloc(m * k * 4));
-  QG_TRY(dad.alloc(m * k * 8));
+  if (m * H == 0) return QG_OK;
+  // tiled layout, one k-block under the caller's plan: words bit-identical to
+  // mul_right_compressed(A, compress_outer_cols(B, plan)), gemm.hpp:320-325
+  qg_gpu_plan gp;
+  std::memset(&gp, 0, sizeof gp);
+  gp.plan = *plan;
+  gp.kblock_words = k ? k : 1;
+  int bk = 0, kbs = 0;
+  if ((st = right_tiled_geometry(&gp, k ? k : 1, &bk, &kbs))) return st;
+  const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
+  DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
+  QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
-  QG_TRY(dcb.alloc(k * H * 8));
+  QG_TRY(dat.alloc(ceil_div(m, 128) * 128 * kt * bk * 8));
+  QG_TRY(dbt.alloc(ceil_div(H, 128) * 128 * kt * bk * 8));
   QG_TRY(dcc.alloc(m * H * 8));
-  if (m * k) QG_TRY(cudaMemcpyAsync(da32.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  // A's residues as doubles for the DMMA operand: an e = 1 "pack" of each row.
-  if (m * k)
-    QG_TRY(qgk::launch_pack(qgk::PACK_OUTER_COLS, da32.p, QG_U32, m, k, k, 1, 1, (double*)dad.p, k, 0, 0, s));
-  if ((st = qg_compress_outer_cols(plan, db.p, QG_U32, k, n, n, (double*)dcb.p, H, s))) return st;
-  if ((st = qg_mul_right(plan, (const double*)dad.p, k, (const double*)dcb.p, m, k, n, (double*)dcc.p, s)))
+  if (k) {
+    if ((st = qg_pack_residues_tiled((uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
+    if ((st = qg_pack_outer_cols_tiled(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
+  }
+  if ((st = qg_mul_right_tiled(&gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, H, s)))
     return st;
-  if (m * H) QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
   return QG_OK;
 }

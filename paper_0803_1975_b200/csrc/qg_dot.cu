@@ -162,6 +162,16 @@ __device__ __forceinline__ uint32_t block_digit_t(double acc, double anchor, uin
 // REDQ of exact packed sums (pack.hpp:124-137). EPI_RAW: plain words.
 enum { EPI_DIGIT = 0, EPI_REDQ = 1, EPI_RAW = 2 };
 
+// redq, pack.hpp:124-137, on an exact integer-valued word w < 2^53: every
+// base-Q digit replaced by itself mod p.
+__device__ __forceinline__ double redq_word(double w, int t, int e, const ModP& modp) {
+  const uint64_t bits = __double2ull_rz(w);
+  const uint64_t mask = (1ull << t) - 1;
+  uint64_t r = 0;
+  for (int s = 0; s < t * e; s += t) r |= (uint64_t)modp((uint32_t)((bits >> s) & mask)) << s;
+  return __ull2double_rn(r);
+}
+
 template <int BK, int VEC, int EPI, bool MULTI>
 __global__ void __launch_bounds__(NT, 1) k_gemm_dmma(GemmArgs args) {
   using G = Geo<BK>;
@@ -458,7 +468,17 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
         slot = 0;
         phase ^= 1;
       }
-      if (MULTI && (MID == 0 || SPLIT)) {  // (MID != 0 flushes inside the unrolled k-steps)
+      if (MULTI && EPI == EPI_REDQ) {  // mixed variant: in-place REDQ between k-blocks
+        if (++kst == args.kb_stages) {
+          kst = 0;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) acc[mi][ni][h] = redq_word(acc[mi][ni][h], args.t, args.e, modp);
+        }
+      } else if (MULTI && (MID == 0 || SPLIT)) {  // (MID != 0 flushes inside the unrolled k-steps)
         if (SPLIT || ++kst == args.kb_stages) {  // SPLIT (kb_stages == 1): even accumulator rows end here
           kst = 0;
           ++nflush;
@@ -501,18 +521,12 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
             }
             *reinterpret_cast<int2*>(dst) = make_int2((int)modp(r[0]), (int)modp(r[1]));
           }
-        } else if (row < M && col < N) {
+        } else if (row < M) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (col + h >= N) continue;
             double w = acc[mi][ni][h];
-            if (EPI == EPI_REDQ) {
-              const uint64_t bits = __double2ull_rz(w);
-              const uint64_t mask = (1ull << args.t) - 1;
-              uint64_t rr = 0;
-              for (int s2 = 0; s2 < args.t * args.e; s2 += args.t)
-                rr |= (uint64_t)modp((uint32_t)((bits >> s2) & mask)) << s2;
-              w = __ull2double_rn(rr);
-            }
+            if (EPI == EPI_REDQ) w = redq_word(w, args.t, args.e, modp);
             args.cc[(size_t)row * args.ldcc + col + h] = w;
           }
         }
@@ -899,6 +913,28 @@ cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const ch
     case 20: return launch_tiled_b<20>(a, flush, s);
     case 12: return launch_tiled_b<12>(a, flush, s);
     case 4: return launch_tiled_b<4>(a, flush, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int BK>
+static cudaError_t launch_right_tiled_bk(const GemmArgs& a, bool redq, cudaStream_t s) {
+  if (!redq) return launch_tiled_one<BK, EPI_RAW, false, 0, false>(a, s);
+  if (a.kb_stages) return launch_tiled_one<BK, EPI_REDQ, true, 0, false>(a, s);
+  return launch_tiled_one<BK, EPI_REDQ, false, 0, false>(a, s);
+}
+
+cudaError_t launch_right_tiled(const GemmArgs& a, int bk, bool redq, cudaStream_t s, const char** variant) {
+  if (a.M == 0 || a.N == 0) return cudaSuccess;
+  static thread_local char name[64];
+  snprintf(name, sizeof name, "right_tiled_bk%d_%s%s", bk, redq ? "redq" : "raw", a.kb_stages ? "_blocked" : "");
+  *variant = name;
+  switch (bk) {
+    case 36: return launch_right_tiled_bk<36>(a, redq, s);
+    case 28: return launch_right_tiled_bk<28>(a, redq, s);
+    case 20: return launch_right_tiled_bk<20>(a, redq, s);
+    case 12: return launch_right_tiled_bk<12>(a, redq, s);
+    case 4: return launch_right_tiled_bk<4>(a, redq, s);
   }
   return cudaErrorInvalidValue;
 }

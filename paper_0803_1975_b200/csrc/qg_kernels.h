@@ -54,6 +54,13 @@ cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const cha
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
 // Same contraction on the tiled layout (a = CA_t, b = CB_t; lda/ldb unused).
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
+// Mixed variant on the tiled layout: a = A_t (residues, e = 1 blocks), b =
+// CBo_t (compress_outer_cols words, transposed blocks); REDQ between k-blocks
+// (kb_stages) and in the epilogue, CC m x N (N = ceil(n/e)).
+cudaError_t launch_right_tiled(const GemmArgs& a, int bk, bool redq, cudaStream_t s, const char** variant);
+// CBo_t[tn][kt][r][c] = compress_outer_cols(B)[BK kt + c][128 tn + r].
+cudaError_t launch_pack_outer_tiled(const void* src, int dtype, size_t k, size_t n, size_t ld, int t, int e,
+                                    int bk, double* dst, cudaStream_t s);
 // Tiled packings: A (m x k residues) -> CA_t, B (k x n residues) -> CB_t.
 cudaError_t launch_pack_tiled(bool b_operand, const void* src, int dtype, size_t rows, size_t cols,
                               size_t ld, int t, int e, int bk, double* dst, cudaStream_t s,

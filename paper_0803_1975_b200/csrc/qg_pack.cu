@@ -149,19 +149,19 @@ __global__ void k_pack_a_tiled(const TIn* __restrict__ a, size_t m, size_t k, si
 }
 
 template <typename TIn, int BK, bool BAL>
-__global__ void __launch_bounds__(64) k_pack_b_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
-                                                     int t, int e, unsigned Kt, double* __restrict__ cb_t,
-                                                     uint32_t p) {
-  // one block = 64 of the 128 rows (n) of one CB_t chunk (tn, kt): coalesced
-  // reads along n, the chunk half written contiguously through shared memory
+__global__ void __launch_bounds__(256) k_pack_b_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
+                                                      int t, int e, unsigned Kt, double* __restrict__ cb_t,
+                                                      uint32_t p) {
+  // one block = 64 of the 128 rows (n) of one CB_t chunk (tn, kt); 4 thread
+  // rows split the BK words. Reads are coalesced along n, the chunk half is
+  // written contiguously through shared memory.
   __shared__ double tile[64 * (BK + 1)];
   const size_t K = (k + e - 1) / e;
   const size_t blk = blockIdx.x >> 1, half = blockIdx.x & 1;
   const size_t kt = blk % Kt, tn = blk / Kt;
-  const int r = threadIdx.x;
+  const int r = threadIdx.x & 63, cg = threadIdx.x >> 6;
   const size_t col = tn * 128 + half * 64 + r;
-#pragma unroll 4
-  for (int c = 0; c < BK; ++c) {
+  for (int c = cg; c < BK; c += 4) {
     const size_t gw = kt * BK + c;
     double wd;
     if (BAL) {
@@ -185,7 +185,59 @@ __global__ void __launch_bounds__(64) k_pack_b_tiled(const TIn* __restrict__ b, 
   }
   __syncthreads();
   double* out = cb_t + blk * (size_t)(128 * BK) + half * (size_t)(64 * BK);
-  for (int i = r; i < 64 * BK; i += 64) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
+  for (int i = threadIdx.x; i < 64 * BK; i += 256) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
+}
+
+// compress_outer_cols (gemm.hpp:145-158) words in the tiled transposed layout
+// of the mixed-variant contraction: CBo_t[tn][kt][r][c] = word (row BK kt + c,
+// group 128 tn + r) = sum_s B[BK kt + c][(128 tn + r) e + s] Q^s.
+template <typename TIn, int BK>
+__global__ void __launch_bounds__(256) k_pack_outer_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
+                                                          int t, int e, unsigned Kt, double* __restrict__ bo_t) {
+  __shared__ double tile[64 * (BK + 1)];
+  const size_t H = (n + e - 1) / e;
+  const size_t blk = blockIdx.x >> 1, half = blockIdx.x & 1;
+  const size_t kt = blk % Kt, tn = blk / Kt;
+  const int r = threadIdx.x & 63, cg = threadIdx.x >> 6;
+  const size_t hcol = tn * 128 + half * 64 + r;
+  for (int c = cg; c < BK; c += 4) {
+    const size_t l = kt * BK + c;
+    uint64_t w = 0;
+    if (hcol < H && l < k) {
+      const size_t base = hcol * e;
+      const int len = (int)((n - base) < (size_t)e ? (n - base) : (size_t)e);
+      for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(b[l * ldb + base + s]);
+    }
+    tile[r * (BK + 1) + c] = __ull2double_rn(w);
+  }
+  __syncthreads();
+  double* out = bo_t + blk * (size_t)(128 * BK) + half * (size_t)(64 * BK);
+  for (int i = threadIdx.x; i < 64 * BK; i += 256) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
+}
+
+template <typename TIn, int BK>
+static cudaError_t pack_outer_tiled_t(const TIn* src, size_t k, size_t n, size_t ld, int t, int e, double* dst,
+                                      cudaStream_t s) {
+  const size_t H = (n + e - 1) / e;
+  const unsigned Kt = (unsigned)((k + BK - 1) / BK);
+  const size_t Nt = (H + 127) / 128;
+  if (Kt == 0 || Nt == 0) return cudaSuccess;
+  k_pack_outer_tiled<TIn, BK><<<(unsigned)(Nt * Kt * 2), 256, 0, s>>>(src, k, n, ld, t, e, Kt, dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename TIn>
+static cudaError_t pack_outer_tiled_dt(const TIn* src, size_t k, size_t n, size_t ld, int t, int e, int bk,
+                                       double* dst, cudaStream_t s) {
+  switch (bk) {
+    case 36: return pack_outer_tiled_t<TIn, 36>(src, k, n, ld, t, e, dst, s);
+    case 28: return pack_outer_tiled_t<TIn, 28>(src, k, n, ld, t, e, dst, s);
+    case 20: return pack_outer_tiled_t<TIn, 20>(src, k, n, ld, t, e, dst, s);
+    case 12: return pack_outer_tiled_t<TIn, 12>(src, k, n, ld, t, e, dst, s);
+    case 4: return pack_outer_tiled_t<TIn, 4>(src, k, n, ld, t, e, dst, s);
+  }
+  return cudaErrorInvalidValue;
 }
 
 // redq over a buffer, pack.hpp:124-137: every base-Q digit replaced by itself
@@ -342,7 +394,7 @@ static cudaError_t pack_tiled_t(bool b_operand, const TIn* src, size_t rows, siz
     const unsigned Kt = (unsigned)((K + BK - 1) / BK);
     const size_t Nt = (cols + 127) / 128;
     if (Kt == 0 || Nt == 0) return cudaSuccess;
-    k_pack_b_tiled<TIn, BK, BAL><<<(unsigned)(Nt * Kt * 2), 64, 0, s>>>(src, rows, cols, ld, t, e, Kt, dst, p);
+    k_pack_b_tiled<TIn, BK, BAL><<<(unsigned)(Nt * Kt * 2), 256, 0, s>>>(src, rows, cols, ld, t, e, Kt, dst, p);
   } else {  // src is m x k
     const size_t K = (cols + e - 1) / e;
     const unsigned Kt = (unsigned)((K + BK - 1) / BK);
@@ -384,6 +436,15 @@ cudaError_t launch_pack_tiled(bool b_operand, const void* src, int dtype, size_t
     case 0: return pack_tiled_dt<double>(b_operand, (const double*)src, rows, cols, ld, t, e, bk, dst, s, p, balanced);
     case 1: return pack_tiled_dt<uint32_t>(b_operand, (const uint32_t*)src, rows, cols, ld, t, e, bk, dst, s, p, balanced);
     default: return pack_tiled_dt<int32_t>(b_operand, (const int32_t*)src, rows, cols, ld, t, e, bk, dst, s, p, balanced);
+  }
+}
+
+cudaError_t launch_pack_outer_tiled(const void* src, int dtype, size_t k, size_t n, size_t ld, int t, int e,
+                                    int bk, double* dst, cudaStream_t s) {
+  switch (dtype) {
+    case 0: return pack_outer_tiled_dt<double>((const double*)src, k, n, ld, t, e, bk, dst, s);
+    case 1: return pack_outer_tiled_dt<uint32_t>((const uint32_t*)src, k, n, ld, t, e, bk, dst, s);
+    default: return pack_outer_tiled_dt<int32_t>((const int32_t*)src, k, n, ld, t, e, bk, dst, s);
   }
 }
 

@@ -349,6 +349,53 @@ int qg_max_exact_block(const qg_plan* plan, uint64_t* words) {
   return QG_OK;
 }
 
+// Mixed (right) variant, gemm.hpp:285-335, on the tensor-core path: every
+// partial sum A x CBo is an exact integer below Q^e <= 2^53, so no rounding
+// bound applies; k is blocked only to keep digits below Q: the kernel
+// REDQs the accumulators in place between blocks (digits drop below p), so a
+// block may add kb residues with (p-1) + kb (p-1)^2 < Q. Picks (t, e, kb)
+// minimising words x (1 + flush cost / kb); e <= n as plan_packed_axis does.
+int qg_plan_right_gpu(uint32_t p, uint64_t k, uint64_t n, qg_gpu_plan* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1 || n < 1) return QG_INVALID_ARGUMENT;
+  double best_cost = 1e300;
+  bool found = false;
+  qg_gpu_plan best;
+  std::memset(&best, 0, sizeof best);
+  const uint64_t pm = pm1sq(p);
+  for (int e = 1; e <= 26; ++e) {
+    if (uint64_t(e) > n && e > 1) break;
+    const int t = 52 / e;  // largest t with t e <= 52: words stay below 2^52
+    if (t < 1 || t > 52) continue;
+    const uint64_t Q = uint64_t(1) << t;
+    const uint64_t km = largest_common_dim(p, t);
+    if (km == 0) continue;
+    uint64_t kb;
+    if (k <= km) kb = k;  // one block, the reference's own condition (gemm.hpp:295)
+    else {
+      if (Q <= p) continue;
+      kb = (Q - p) / (pm ? pm : 1);
+      if (kb < 4) continue;
+      kb = stage_block_tiled(kb, nullptr);
+      if (kb == 0) continue;
+    }
+    const double H = double((n + e - 1) / e);
+    const double nflush = kb >= k ? 0.0 : double((k + kb - 1) / kb);
+    const double cost = H * (double(k) + 4.0 * e * nflush);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      found = true;
+      fill(&best.plan, p, t, e, 53, std::ldexp(1.0, -t * (e - 1)));
+      best.kblock_words = kb;  // residues of k per block
+      best.max_exact_words = kb;
+    }
+  }
+  if (!found) return QG_NO_COMPRESSION;
+  *out = best;
+  return QG_OK;
+}
+
 int qg_max_exact_block_balanced(const qg_plan* plan, uint64_t* words) {
   if (!plan || !words) return QG_INVALID_ARGUMENT;
   if (plan->p < 2 || !is_prime(plan->p)) return QG_INVALID_MODULUS;

@@ -287,3 +287,33 @@ def test_tiled_layout_words(qg, orc, cuda, bk):
     eb = eb.reshape(Nt, 128, Kt, bk).transpose(0, 2, 1, 3).ravel()
     assert np.array_equal(bits(ta), bits(ea))
     assert np.array_equal(bits(tb), bits(eb))
+
+
+@pytest.mark.parametrize("p,m,k,n", [(5, 96, 300, 250), (3, 130, 64, 77), (7, 33, 500, 9), (5, 1, 6, 1), (5, 200, 3000, 301),
+                                     (3, 64, 20000, 130)])
+def test_mul_right_tiled(qg, orc, cuda, p, m, k, n):
+    """Mixed variant on the tiled layout: under the reference plan the CC words
+    equal mul_right_compressed's bit for bit; under a blocked GPU plan (in-place
+    REDQ between k-blocks) they equal compress_outer_cols(naive C)."""
+    import torch
+
+    a = orc.random_residue_matrix(m, k, p, 177)
+    b = orc.random_residue_matrix(k, n, p, 178)
+    ad = torch.from_numpy(a.astype(np.float64)).to(cuda)
+    bd = torch.from_numpy(b.astype(np.float64)).to(cuda)
+    want_c = orc.naive_gemm(p, a, b)
+    try:
+        rp = qg.plan_packed_axis(p, k, n)
+    except qg.NoCompression:
+        rp = None
+    if rp is not None and k <= rp.kmax:
+        cc = qg.mul_right_tiled(ad, bd, rp)
+        op = orc.plan_of(rp)
+        want = orc.mul_right_compressed(op, a, orc.compress_outer_cols(op, b), n)
+        assert np.array_equal(bits(host(cc.data)), bits(want))
+    gp = qg.plan_right_gpu(p, k, n)
+    cc = qg.mul_right_tiled(ad, bd, gp)
+    assert np.array_equal(host(qg.uncompress(cc)).astype(np.uint32), want_c)
+    big = orc.Plan(*orc.plan_of(gp.plan).astuple())
+    big.kmax = max(big.kmax, k)
+    assert np.array_equal(bits(host(cc.data)), bits(orc.compress_outer_cols(big, want_c)))

@@ -419,8 +419,10 @@ def our_arm(args):
     }
     line["clocks"] = clk.summary()
 
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = e2e_measure(qg, gp, p, m_rank, k, n, args)
+    if not args.no_e2e:
+        e2e = e2e_measure(qg, gp, p, m_rank, k, n, args, rank, world)
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             rate, rows, thr, dt, c_cpu, rpl, kind = reference_cpu_sample(p, m_rank, k, n, target_s=args.cpu_s)
@@ -438,31 +440,43 @@ def our_arm(args):
     return 0
 
 
-def e2e_measure(qg, gp, p, m, k, n, args):
+def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1):
     """Same metric through the public host-buffer API (pinned buffers):
     H2D of A and B (uint32 ResidueMatrix data), pack + contraction kernels,
-    D2H of C, every step."""
+    D2H of C, every step. At N GPUs every rank calls the API on its own row
+    shard of A (rows rank*m ..), time = max over ranks."""
     import numpy as np
     import torch
+    import torch.distributed as dist
 
-    import oracle  # only to create the seeded host inputs bit-identically
-
-    a = torch.empty((m, k), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    b = torch.empty((k, n), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    c = torch.empty((m, n), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    a[:] = oracle.random_residue_matrix(m, k, p, SEED)
-    b[:] = oracle.random_residue_matrix(k, n, p, SEED + 1)
+    # seeded host inputs, made on the device by the library (K0) and copied out
+    # before the timed region
+    a = torch.empty((m, k), dtype=torch.int32, pin_memory=True)
+    b = torch.empty((k, n), dtype=torch.int32, pin_memory=True)
+    c = torch.empty((m, n), dtype=torch.int32, pin_memory=True)
+    a.copy_(qg.random_residue_matrix(m, k, p, SEED, row0=rank * m, dtype=torch.int32))
+    b.copy_(qg.random_residue_matrix(k, n, p, SEED + 1, dtype=torch.int32))
+    torch.cuda.synchronize()
+    an, bn, cn = a.numpy().view(np.uint32), b.numpy().view(np.uint32), c.numpy().view(np.uint32)
     for _ in range(2):
-        qg.mul_common_compressed_host(a, b, gp, out=c)
+        qg.mul_common_compressed_host(an, bn, gp, out=cn)
     times = []
     for _ in range(args.e2e_steps):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        qg.mul_common_compressed_host(a, b, gp, out=c)
+        qg.mul_common_compressed_host(an, bn, gp, out=cn)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
-    return {"value": 2.0 * m * n * k / t, "unit": "mult-adds/s (2mnk/s)", "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
-            "d2h_bytes_per_step": int(c.nbytes), "ms_per_step": t * 1e3, "api": "mul_common_compressed_host (qg_host_mul_common_gpu)",
-            "checksum": int(c.astype(np.uint64).sum() & 0xFFFFFFFF)}
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": 2.0 * m * world * n * k / t, "unit": "mult-adds/s (2mnk/s)",
+            "h2d_bytes_per_step": int(a.numel() * 4 + b.numel() * 4) * world,
+            "d2h_bytes_per_step": int(c.numel() * 4) * world, "ms_per_step": t * 1e3,
+            "api": "mul_common_compressed_host (qg_host_mul_common_gpu), pipelined H2D/compute/D2H",
+            "checksum_rank0": int(cn.astype(np.uint64).sum() & 0xFFFFFFFF)}
 
 
 def main():

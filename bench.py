@@ -296,10 +296,16 @@ def our_arm(args):
     local = env_int("LOCAL_RANK", 0)
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; with fewer GPUs than ranks (the gloo functional
+    # check of the multi-rank path on one GPU) ranks share devices
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     p, m_rank, k, n, desc = CONFIGS[args.config]
     gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
@@ -358,7 +364,7 @@ def our_arm(args):
         dist.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         for _ in range(args.steps):
             flush.fill_(1)  # evict L2 between timed steps (outside the events)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -405,7 +411,7 @@ def our_arm(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
-        "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over NCCL" if world > 1 else ""),
+        "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over {args.dist_backend.upper()}" if world > 1 else ""),
                    "p": p, "m": m_total, "k": k, "n": n,
                    "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
                             "source": args.plan},
@@ -489,6 +495,8 @@ def main():
     ap.add_argument("--plan", default="gpu", choices=["gpu", "reference"],
                     help="gpu: planner-chosen (t, e, kblock); reference: plan_compression's plan")
     ap.add_argument("--kblock", type=int, default=0, help="override the plan's k-block (words)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the multi-rank path with several ranks on one GPU")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=2.0)

@@ -39,7 +39,11 @@ CONFIGS = {
     "config3": (3, 8192, 256, 8192, "config3: p=3 m=n=8192 k=256 dot-product variant"),
     "config5": (3, 32768, 32768, 32768, "config5: p=3 m=n=k=32768 dot-product variant, k-blocked"),
     "config4": (5, 8192, 8192, 8192, "config4: p=5 m=n=k=8192 mixed (right) variant, REDQ epilogue -> CC"),
+    # the left and full variants (gemm.hpp:340-445) on config 4's shape
+    "config4_left": (5, 8192, 8192, 8192, "config4 shape: p=5 m=n=k=8192 left (outer-rows) variant, REDQ -> CC"),
+    "config4_full": (5, 8192, 8192, 8192, "config4 shape: p=5 m=n=k=8192 full (two-axis) variant -> C"),
 }
+REDQ_VARIANTS = {"config4": "right", "config4_left": "left", "config4_full": "full"}
 SEED = 42
 
 
@@ -159,21 +163,122 @@ def reference_cpu_sample(p, m, k, n, target_s=4.0, threads=None, rows=None):
     return 2.0 * rows * n * k / dt, rows, threads, dt, c, pl, kind
 
 
+def reference_variant_sample(variant, p, m, k, n, target_s=4.0, threads=None, rows=None):
+    """Time the reference's own right / left / full path (oracle/_ref: the
+    unmodified mul_right_compressed / mul_left_compressed(compress_outer_rows)
+    / mul_full_compressed, bench.hpp:108-152) at the reference's plan on a row
+    sample of the seeded workload, row shards over host threads (B packed per
+    shard for left/full, as the reference's single-threaded call would).
+    Raises NoCompression when the reference planner refuses the shape."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle
+
+    ref = oracle.REF
+    if ref is None:
+        raise RuntimeError("oracle/_ref/libqgref.so is missing (built by __graft_entry__.build())")
+    threads = threads or host_threads()
+    vp = ctypes.c_void_p
+    if variant == "full":
+        plan = oracle.FullPlan()
+        st = ref.qgref_plan_full(p, k, 53, ctypes.byref(plan))
+        group = plan.dq + 1 if st == 0 else 1
+    else:
+        plan = oracle.Plan()
+        st = ref.qgref_plan_compression(p, k, 53, 0, ctypes.byref(plan))
+        group = plan.e if (st == 0 and variant == "left") else 1
+    if st:
+        raise RuntimeError(f"reference planner refused p={p} k={k} for the {variant} variant (status {st}: "
+                           f"{'NoCompression' if st == 2 else 'error'})")
+    b = oracle.random_residue_matrix(k, n, p, SEED + 1)
+
+    pack_b_cache = []
+
+    def pack_b_seconds():  # the reference's compress_outer_cols(B) alone (gemm.hpp:145-158)
+        if not pack_b_cache:
+            cbo = np.zeros((k, -(-n // plan.e)))
+            runs = []
+            for _ in range(2):
+                t0 = time.perf_counter()
+                ref.qgref_compress_outer_cols(ctypes.byref(plan), b.ctypes.data_as(vp), k, n, cbo.ctypes.data_as(vp))
+                runs.append(time.perf_counter() - t0)
+            pack_b_cache.append(min(runs))
+        return pack_b_cache[0]
+
+    def shard(a, r):
+        if variant == "left":
+            cc = np.empty((-(-r // plan.e), n))
+            st = ref.qgref_mul_left(ctypes.byref(plan), a.ctypes.data_as(vp), b.ctypes.data_as(vp), r, k, n,
+                                    cc.ctypes.data_as(vp))
+        else:
+            cc = np.empty((r, n), np.uint32)
+            st = ref.qgref_mul_full(ctypes.byref(plan), a.ctypes.data_as(vp), b.ctypes.data_as(vp), r, k, n,
+                                    cc.ctypes.data_as(vp))
+        if st:
+            raise RuntimeError(f"reference {variant} failed: {st}")
+
+    def run(r):
+        a = oracle.random_residue_matrix(r, k, p, SEED)
+        t0 = time.perf_counter()
+        if variant == "right":
+            cc = np.empty((r, -(-n // plan.e)))
+            mul, conv = ctypes.c_double(), ctypes.c_double()
+            st = ref.qgref_mul_right(ctypes.byref(plan), a.ctypes.data_as(vp), b.ctypes.data_as(vp), r, k, n,
+                                     cc.ctypes.data_as(vp), None, threads, ctypes.byref(mul), ctypes.byref(conv))
+            if st:
+                raise RuntimeError(f"reference right failed: {st}")
+            # compress_outer_cols(B) runs once per call: charge it pro rata
+            # (r/m), as a full-size run amortises it over all m rows
+            dt = time.perf_counter() - t0
+            pack_b = min(pack_b_seconds(), dt)
+            return max(dt - pack_b + pack_b * r / m, mul.value)  # never below the multiply phase itself
+        else:
+            per = max(group, -(-r // threads) // group * group)
+            parts = [(i, min(r, i + per)) for i in range(0, r, per)]
+            with ThreadPoolExecutor(len(parts)) as ex:
+                list(ex.map(lambda se: shard(np.ascontiguousarray(a[se[0]:se[1]]), se[1] - se[0]), parts))
+        return time.perf_counter() - t0
+
+    if rows is None:
+        pilot = max(threads, 8) // group * group or group
+        dt = run(pilot)
+        rows = int(min(m, max(threads * group, pilot * target_s / max(dt, 1e-3))))
+        rows = max(group, rows // (threads * group) * (threads * group)) if rows >= threads * group else \
+            max(group, rows // group * group)
+    dt = run(rows)
+    kind = "reference"
+    return 2.0 * rows * n * k / dt, rows, threads, dt, None, plan, kind
+
+
 # ------------------------------------------------------------------ reference arm
 def reference_arm(args):
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
     p, m, k, n, desc = CONFIGS[args.config]
+    variant = REDQ_VARIANTS.get(args.config, "common")
     rates, rows_used, thr = [], None, host_threads()
     rows_used = None
     for i in range(args.warmup + args.steps):
-        rate, rows, thr, dt, _, pl, kind = reference_cpu_sample(p, m, k, n, target_s=args.ref_step_s, rows=rows_used)
+        if variant == "common":
+            rate, rows, thr, dt, _, pl, kind = reference_cpu_sample(p, m, k, n, target_s=args.ref_step_s, rows=rows_used)
+        else:
+            try:
+                rate, rows, thr, dt, _, pl, kind = reference_variant_sample(variant, p, m, k, n,
+                                                                            target_s=args.ref_step_s, rows=rows_used)
+            except RuntimeError as ex:
+                print(json.dumps({"impl": "reference", "unavailable": str(ex)}), flush=True)
+                return 0
         rows_used = rows
         if i >= args.warmup:
             rates.append(rate)
     value = sum(rates) / len(rates)
-    sample = f"rows 0..{rows_used - 1} of A ({rows_used}x{k}) x B ({k}x{n}), reference plan t={pl.t} e={pl.e}, {thr} threads"
+    pdesc = (f"t={pl.base.t} dq={pl.dq} dtheta={pl.dtheta}" if variant == "full" else f"t={pl.t} e={pl.e}")
+    sample = (f"rows 0..{rows_used - 1} of A ({rows_used}x{k}) x B ({k}x{n}), {variant} variant, reference plan "
+              f"{pdesc}, {thr} threads")
     line = {
         "impl": "reference", "metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": value, "unit": "mult-adds/s (2mnk/s)",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * rows_used * n * k / value * 1e3,
@@ -195,17 +300,19 @@ def load_json(path):
         return None
 
 
-def mixed_arm(args):
-    """Config 4: mixed / right-compressed variant (gemm.hpp:285-335) on the
-    tiled layout. Step = pack A's residues + compress_outer_cols(B) into tiled
-    blocks + the DMMA contraction with in-place REDQ between k-blocks and a
-    REDQ epilogue (K5) on device-resident residues; output CC words.
-    --plan gpu: plan_right_gpu (t=13, e=4, 504-residue blocks); --plan
-    reference: plan_compression(p, k) as run_bench uses (bench.hpp:149), CC
-    bit-identical to the reference's."""
+def redq_arm(args):
+    """Config 4 and its §8(f) siblings: the right (mixed, gemm.hpp:285-335),
+    left (gemm.hpp:340-371) and full (gemm.hpp:377-445) variants on the tiled
+    layout. Step = the operand packs into tiled blocks + the DMMA contraction
+    with in-place REDQ between k-blocks and a REDQ epilogue (K5) [+ the full
+    variant's digit scatter to C] on device-resident residues.
+    --plan gpu: plan_right_gpu / plan_full_gpu; --plan reference: the plan the
+    reference bench uses (plan_compression / plan_full, bench.hpp:108-152),
+    output words bit-identical to the reference's."""
     import ctypes
     import hashlib
 
+    import numpy as np
     import torch
 
     import paper_0803_1975_b200 as qg
@@ -213,36 +320,85 @@ def mixed_arm(args):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     p, m, k, n, desc = CONFIGS[args.config]
-    if args.plan == "reference":
-        base = qg.plan_compression(p, k)
-        gp = qg.GpuPlan(base, k, k, 0)
+    variant = REDQ_VARIANTS[args.config]
+    sp = qg._stream
+    kblock = 0
+    if variant == "full":
+        if args.plan == "reference":
+            try:
+                fp = qg.plan_full(p, k)
+            except qg.NoCompression:
+                print(json.dumps({"metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": None,
+                                  "unavailable": f"plan_full({p}, {k}) raises NoCompression (plan.hpp:235-237)"}))
+                return 0
+            kblock = 0
+        else:
+            fp, kblock = qg.plan_full_gpu(p, k)
+        plan = fp.base
+        f = fp._c()
+        bk_c = ctypes.c_uint32()
+        qg._check(qg.lib.qg_full_tiled_stage(ctypes.byref(f), kblock, k, ctypes.byref(bk_c)))
+        rows_a, rows_b = -(-m // fp.q_slots()), -(-n // fp.theta_slots())
+        out_shape = (rows_a, rows_b)
+        plan_desc = {"t": plan.t, "dq": fp.dq, "dtheta": fp.dtheta, "theta_exponent": fp.theta_exponent,
+                     "kblock_residues": kblock or k}
     else:
-        gp = qg.plan_right_gpu(p, k, n)
-    plan = gp.plan
-    H = -(-n // plan.e)
-    g = gp._c()
-    bk_c = ctypes.c_uint32()
-    qg._check(qg.lib.qg_right_tiled_stage(ctypes.byref(g), k, ctypes.byref(bk_c)))
+        if args.plan == "reference":
+            base = qg.plan_compression(p, k)
+            gp = qg.GpuPlan(base, k, k, 0)
+        else:
+            gp = qg.plan_right_gpu(p, k, n if variant == "right" else m)
+        plan = gp.plan
+        g = gp._c()
+        bk_c = ctypes.c_uint32()
+        qg._check(qg.lib.qg_right_tiled_stage(ctypes.byref(g), k, ctypes.byref(bk_c)))
+        if variant == "right":
+            rows_a, rows_b = m, -(-n // plan.e)
+        else:
+            rows_a, rows_b = -(-m // plan.e), n
+        out_shape = (rows_a, rows_b)
+        plan_desc = {"t": plan.t, "e": plan.e, "kblock_residues": gp.kblock_words}
     bk = bk_c.value
     kt = -(-k // bk)
     a = qg.random_residue_matrix(m, k, p, SEED)
     b = qg.random_residue_matrix(k, n, p, SEED + 1)
-    a_t = torch.empty(-(-m // 128) * 128 * kt * bk, dtype=torch.float64, device=dev)
-    bo_t = torch.empty(-(-H // 128) * 128 * kt * bk, dtype=torch.float64, device=dev)
-    cc = torch.empty((m, H), dtype=torch.float64, device=dev)
+    a_t = torch.empty(-(-rows_a // 128) * 128 * kt * bk, dtype=torch.float64, device=dev)
+    b_t = torch.empty(-(-rows_b // 128) * 128 * kt * bk, dtype=torch.float64, device=dev)
+    cc = torch.empty(out_shape, dtype=torch.float64, device=dev)
+    c_full = torch.empty((m, n), dtype=torch.int32, device=dev) if variant == "full" else None
     pl = plan._c()
-    sp = qg._stream
+    if variant == "full":
+        qs, ts = fp.q_slots(), fp.theta_slots()
+        pa = qg._Plan(p, plan.t, qs - 1, qs, 53, plan.kmax, 1.0, 0)
+        pb = qg._Plan(p, fp.theta_exponent, ts - 1, ts, 53, plan.kmax, 1.0, 0)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
     def step(ev=None):
-        qg._check(qg.lib.qg_pack_residues_tiled(bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
-        qg._check(qg.lib.qg_pack_outer_cols_tiled(ctypes.byref(pl), bk, qg._ptr(b), 0, k, n, n, qg._ptr(bo_t), sp()))
+        if variant == "right":
+            qg._check(qg.lib.qg_pack_residues_tiled(bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
+            qg._check(qg.lib.qg_pack_outer_cols_tiled(ctypes.byref(pl), bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t), sp()))
+        elif variant == "left":
+            qg._check(qg.lib.qg_pack_outer_rows_tiled(ctypes.byref(pl), bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
+            qg._check(qg.lib.qg_pack_residues_b_tiled(bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t), sp()))
+        else:
+            qg._check(qg.lib.qg_pack_outer_rows_tiled(ctypes.byref(pa), bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
+            qg._check(qg.lib.qg_pack_outer_cols_tiled(ctypes.byref(pb), bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t), sp()))
         if ev:
             ev[0].record(stream)
-        qg._check(qg.lib.qg_mul_right_tiled(ctypes.byref(g), qg._ptr(a_t), qg._ptr(bo_t), m, k, n, qg._ptr(cc), H, sp()))
+        if variant == "right":
+            qg._check(qg.lib.qg_mul_right_tiled(ctypes.byref(g), qg._ptr(a_t), qg._ptr(b_t), m, k, n, qg._ptr(cc),
+                                                rows_b, sp()))
+        elif variant == "left":
+            qg._check(qg.lib.qg_mul_left_tiled(ctypes.byref(g), qg._ptr(a_t), qg._ptr(b_t), m, k, n, qg._ptr(cc),
+                                               rows_b, sp()))
+        else:
+            qg._check(qg.lib.qg_mul_full_tiled(ctypes.byref(f), kblock, qg._ptr(a_t), qg._ptr(b_t), m, k, n,
+                                               qg._ptr(cc), rows_b, sp()))
         if ev:
             ev[1].record(stream)
+        if variant == "full":
+            qg._check(qg.lib.qg_uncompress_full(ctypes.byref(f), qg._ptr(cc), rows_b, m, n, qg._ptr(c_full), n, sp()))
 
     for _ in range(args.warmup):
         step()
@@ -260,23 +416,68 @@ def mixed_arm(args):
             s1.synchronize()
             step_ms.append(s0.elapsed_time(s1))
             kern_ms.append(ev[0].elapsed_time(ev[1]))
+    launches = qg.kernel_launches() - launches0
+    kernel = qg.last_kernel()
     ms = sum(step_ms) / len(step_ms)
     kms = sum(kern_ms) / len(kern_ms)
-    flop = 2.0 * m * H * k
+    flop = 2.0 * rows_a * rows_b * k  # DMMA flops of the contraction (words x words x k)
     peak = float((load_json(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) or {}).get("dmma_m8n8k4_tflops", 37.09))
-    c = qg.uncompress(qg.CompressedMatrix(m, n, m, H, qg.PackOrientation(0, 1, plan.e), plan, cc))
+    if variant == "full":
+        c = c_full
+    else:
+        orient = qg.PackOrientation(0, 1, plan.e) if variant == "right" else qg.PackOrientation(0, 0, plan.e)
+        c = qg.uncompress(qg.CompressedMatrix(m, n, rows_a, rows_b, orient, plan, cc))
     line = {"metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": 2.0 * m * n * k / (ms * 1e-3),
             "unit": "mult-adds/s (2mnk/s)", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n,
-                       "plan": {"t": plan.t, "e": plan.e, "kblock_residues": gp.kblock_words, "stage_words": bk,
-                                "source": args.plan}},
-            "roofline": {"bound": "tensor", "achieved": round(flop / (kms * 1e-3) / 1e12, 3), "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(flop / (kms * 1e-3) / 1e12 / peak, 4), "traffic": None, "kernel": qg.last_kernel(),
-                         "kernel_ms": round(kms, 4)},
-            "gpu_launches": qg.kernel_launches() - launches0, "checksum_c": qg.residue_checksum(c),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SplitMix64 seed 42/43, generated on device)",
+            "config": {"workload": desc, "variant": variant, "p": p, "m": m, "k": k, "n": n,
+                       "plan": dict(plan_desc, stage_words=bk, source=args.plan),
+                       "l2": "256 MiB buffer written between timed steps"},
+            "roofline": {"bound": "tensor", "achieved": round(flop / (kms * 1e-3) / 1e12, 3), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(flop / (kms * 1e-3) / 1e12 / peak, 4), "traffic": None,
+                         "kernel": kernel, "kernel_ms": round(kms, 4),
+                         "per_unit": "2 flops per packed-word product; rows_a x rows_b x k products per launch"},
+            "gpu_launches": launches, "checksum_c": qg.residue_checksum(c),
             "cc_sha256": hashlib.sha256(cc.cpu().numpy().view("uint64").tobytes()).hexdigest(),
             "clocks": clk.summary()}
+    del flush
+    if not args.no_e2e:
+        an = torch.empty((m, k), dtype=torch.int32, pin_memory=True)
+        bn = torch.empty((k, n), dtype=torch.int32, pin_memory=True)
+        an.copy_(a.to(torch.int32))
+        bn.copy_(b.to(torch.int32))
+        an_u, bn_u = an.numpy().view(np.uint32), bn.numpy().view(np.uint32)
+        if variant == "full":
+            out = torch.empty((m, n), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+            call = lambda: qg.mul_full_compressed_host(an_u, bn_u, fp, kblock, out=out)  # noqa: E731
+            api = "mul_full_compressed_host (qg_host_mul_full)"
+        else:
+            out = torch.empty(out_shape, dtype=torch.float64, pin_memory=True).numpy()
+            fn = qg.mul_right_compressed_host if variant == "right" else qg.mul_left_compressed_host
+            arg = gp if args.plan == "gpu" else plan
+            call = lambda: fn(an_u, bn_u, arg, out=out)  # noqa: E731
+            api = f"mul_{variant}_compressed_host (qg_host_mul_{variant}{'_gpu' if args.plan == 'gpu' else ''})"
+        for _ in range(2):
+            call()
+        times = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            call()
+            times.append(time.perf_counter() - t0)
+        t = sum(times) / len(times)
+        line["e2e"] = {"value": 2.0 * m * n * k / t, "unit": "mult-adds/s (2mnk/s)",
+                       "h2d_bytes_per_step": int((m * k + k * n) * 4), "d2h_bytes_per_step": int(out.nbytes),
+                       "ms_per_step": t * 1e3, "api": api}
+    if not args.no_cpu:
+        try:
+            rate, rows, thr, dt, _, rpl, kind = reference_variant_sample(variant, p, m, k, n, target_s=args.cpu_s)
+            pdesc = (f"t={rpl.base.t} dq={rpl.dq} dtheta={rpl.dtheta}" if variant == "full" else f"t={rpl.t} e={rpl.e}")
+            line["cpu_baseline"] = {"value": rate, "unit": "mult-adds/s (2mnk/s)", "cores": thr, "kind": kind,
+                                    "sample": f"rows 0..{rows - 1} of A x B ({k}x{n}), reference {variant} path, "
+                                              f"plan {pdesc}, {dt:.1f} s"}
+        except RuntimeError as ex:
+            line["cpu_baseline"] = {"value": None, "unavailable": str(ex)}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -507,8 +708,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return reference_arm(args)
-    if args.config == "config4":
-        return mixed_arm(args)
+    if args.config in REDQ_VARIANTS:
+        return redq_arm(args)
     return our_arm(args)
 
 

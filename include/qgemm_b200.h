@@ -195,6 +195,47 @@ int qg_pack_outer_cols_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg
 int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double* bo_t, size_t m, size_t k,
                        size_t n, double* cc, size_t ldcc, void* stream);
 
+/* ---- left and full compression on the tiled layout, gemm.hpp:340-445.
+ * Both contract with the REDQ kernel of the mixed variant; only the operand
+ * packs differ.
+ *
+ * Left (mul_left_compressed(compress_outer_rows(A), B), gemm.hpp:340-371):
+ * A's compress_outer_rows words (ceil(m/e) x k, pack.hpp / gemm.hpp:160-176)
+ * as 128 x BK blocks, B's residues transposed into 128 x BK blocks (e = 1).
+ * cc: ceil(m/e) x n post-REDQ words, digit s of cc[g][j] = C[g e + s][j]
+ * (qg_uncompress with {Forward, Row, e} unpacks it). gplan: any qg_gpu_plan
+ * whose kblock_words bounds the in-place REDQ blocks (qg_plan_right_gpu(p,
+ * k, m) picks one; qg_gpu_plan_from-style {plan, kblock = k} keeps the
+ * reference's single block). */
+int qg_pack_outer_rows_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m,
+                             size_t k, size_t lda, double* ao_t, void* stream);
+int qg_pack_residues_b_tiled(uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n, size_t ldb,
+                             double* b_t, void* stream);
+int qg_mul_left_tiled(const qg_gpu_plan* gplan, const double* ao_t, const double* b_t, size_t m, size_t k,
+                      size_t n, double* cc, size_t ldcc, void* stream);
+
+/* Full (mul_full_compressed, gemm.hpp:377-445): rows of A packed in base Q
+ * with dq+1 slots (qg_pack_outer_rows_tiled under {t, e = dq+1}), columns of
+ * B in base Theta = 2^theta_exponent with dtheta+1 slots
+ * (qg_pack_outer_cols_tiled under {t = theta_exponent, e = dtheta+1}). The
+ * contraction REDQs all (dq+1)(dtheta+1) base-Q digits in place every
+ * kblock_words residues; cc: ceil(m/(dq+1)) x ceil(n/(dtheta+1)) words, and
+ * qg_uncompress_full scatters digit i + j (dq+1) of cc[g][h] to
+ * C[g (dq+1) + i][h (dtheta+1) + j]. */
+typedef struct {
+  qg_plan base; /* e = (dq+1)(dtheta+1), d = e-1 */
+  int32_t dq, dtheta, theta_exponent;
+} qg_full_plan;
+/* plan_full, plan.hpp:229-252 */
+int qg_plan_full(uint32_t p, uint64_t k, int beta, qg_full_plan* out);
+/* B200 planner: same slot split, free radix, k-blocked (kblock_words out). */
+int qg_plan_full_gpu(uint32_t p, uint64_t k, qg_full_plan* out, uint64_t* kblock_words);
+int qg_full_tiled_stage(const qg_full_plan* fp, uint64_t kblock_words, uint64_t k, uint32_t* bk);
+int qg_mul_full_tiled(const qg_full_plan* fp, uint64_t kblock_words, const double* ao_t, const double* bo_t,
+                      size_t m, size_t k, size_t n, double* cc, size_t ldcc, void* stream);
+int qg_uncompress_full(const qg_full_plan* fp, const double* cc, size_t ldcc, size_t m, size_t n, int32_t* c,
+                       size_t ldc, void* stream);
+
 /* packed_right_product + redq_in_place = mul_right_compressed(a, cb),
  * gemm.hpp:285-325: CC = REDQ(A x CBo). A: m x k residues as double (lda),
  * CBo: k x ceil(n/e) words. cc: m x ceil(n/e). */
@@ -232,6 +273,24 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
  * data: cc gets the post-REDQ words (m x ceil(n/e)). */
 int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
                       size_t k, size_t n, double* cc);
+
+/* The same under a blocked GPU plan (qg_plan_right_gpu(p, k, n)): in-place
+ * REDQ every gplan->kblock_words residues; words equal
+ * compress_outer_cols(C) under gplan->plan. */
+int qg_host_mul_right_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                          size_t n, double* cc);
+/* mul_left_compressed(compress_outer_rows(A, plan), B), gemm.hpp:366-371, on
+ * HOST data: cc gets the post-REDQ words (ceil(m/e) x n). */
+int qg_host_mul_left(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                     size_t n, double* cc);
+/* ... under a blocked GPU plan (qg_plan_right_gpu(p, k, m)). */
+int qg_host_mul_left_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                         size_t n, double* cc);
+/* mul_full_compressed(A, B, fp), gemm.hpp:377-445, on HOST data: c = A B mod
+ * p (m x n uint32). kblock_words = 0 means one block (the reference's
+ * k <= kmax condition applies); otherwise qg_plan_full_gpu's blocking. */
+int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32_t* a, const uint32_t* b,
+                     size_t m, size_t k, size_t n, uint32_t* c);
 
 /* ------------------------------------------------------------ diagnostics */
 /* Number of kernels this library launched since load (the bench's

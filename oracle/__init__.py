@@ -41,6 +41,10 @@ class Plan(ctypes.Structure):
         return (self.p, self.t, self.d, self.e, self.beta, self.kmax, self.inv_qd, self.extraction)
 
 
+class FullPlan(ctypes.Structure):
+    _fields_ = [("base", Plan), ("dq", ctypes.c_int32), ("dtheta", ctypes.c_int32), ("theta_exponent", ctypes.c_int32)]
+
+
 class Orientation(ctypes.Structure):
     _fields_ = [("direction", ctypes.c_int32), ("axis", ctypes.c_int32), ("slots", ctypes.c_int32)]
 
@@ -88,6 +92,10 @@ def _load_c():
         "qgo_redq_in_place": ([P(Plan), vp, sz], i32),
         "qgo_mul_right_compressed": ([P(Plan), vp, vp, sz, sz, sz, vp, i32], i32),
         "qgo_blocked_accumulate": ([P(Plan), vp, vp, sz, sz, sz, sz, vp, i32], i32),
+        "qgo_plan_full": ([u32, u64, i32, P(FullPlan)], i32),
+        "qgo_packed_left_product": ([P(Plan), vp, vp, sz, sz, sz, vp, i32], i32),
+        "qgo_mul_left_compressed": ([P(Plan), vp, vp, sz, sz, sz, vp, i32], i32),
+        "qgo_mul_full_compressed": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
         "qgo_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp, i32], i32),
         "qgo_residue_checksum": ([vp, sz], u32),
     }
@@ -126,6 +134,9 @@ def _load_ref():
         "qgref_mul_common": ([P(Plan), vp, vp, sz, sz, sz, vp, i32, dp, dp], i32),
         "qgref_mul_right": ([P(Plan), vp, vp, sz, sz, sz, vp, vp, i32, dp, dp], i32),
         "qgref_blocked_accumulate": ([P(Plan), vp, vp, sz, sz, sz, sz, vp], i32),
+        "qgref_plan_full": ([u32, u64, i32, P(FullPlan)], i32),
+        "qgref_mul_left": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qgref_mul_full": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
         "qgref_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp], i32),
     }
     for name, (args, res) in sig.items():
@@ -297,6 +308,32 @@ def blocked_accumulate(plan, a, b, kpanel) -> np.ndarray:
     n = b.shape[1]
     c = np.empty((m, n), dtype=np.uint32)
     _ok(C.qgo_blocked_accumulate(ctypes.byref(plan_of(plan)), _p(a), _p(b), m, k, n, kpanel, _p(c), threads()))
+    return c
+
+
+def plan_full(p, k, beta=53) -> FullPlan:
+    fp = FullPlan()
+    _ok(C.qgo_plan_full(p, k, beta, ctypes.byref(fp)))
+    return fp
+
+
+def mul_left_compressed(plan, a, b) -> np.ndarray:
+    """mul_left_compressed(compress_outer_rows(A), B): ceil(m/e) x n post-REDQ words."""
+    a, b = _u32(a), _u32(b)
+    m, k = a.shape
+    n = b.shape[1]
+    ca = compress_outer_rows(plan, a)
+    cc = np.empty((-(-m // plan.e), n), dtype=np.float64)
+    _ok(C.qgo_mul_left_compressed(ctypes.byref(plan_of(plan)), _p(ca), _p(b), m, k, n, _p(cc), threads()))
+    return cc
+
+
+def mul_full_compressed(fp, a, b) -> np.ndarray:
+    a, b = _u32(a), _u32(b)
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.uint32)
+    _ok(C.qgo_mul_full_compressed(ctypes.byref(fp), _p(a), _p(b), m, k, n, _p(c)))
     return c
 
 

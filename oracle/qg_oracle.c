@@ -495,6 +495,119 @@ int qgo_mul_right_compressed(const qgo_plan* plan, const uint32_t* a, const doub
   return st;
 }
 
+/* plan_full, plan.hpp:229-252: word capacity E split as (dq+1)(dtheta+1),
+ * dq+1 = floor(sqrt(E)), dtheta+1 = E / (dq+1). */
+int qgo_plan_full(uint32_t p, uint64_t k, int beta, qgo_full_plan* out) {
+  if (p < 2 || !qgo_is_prime(p)) return QGO_INVALID_MODULUS;
+  if (k < 1 || beta < 2) return QGO_INVALID_ARGUMENT;
+  const int t = minimal_radix_exponent(p, k);
+  const int capacity = t < beta ? word_capacity(t, beta) : 0;
+  if (capacity < 4) return QGO_NO_COMPRESSION;
+  int qs = (int)sqrt((double)capacity);
+  while (qs * qs > capacity) --qs;
+  while ((qs + 1) * (qs + 1) <= capacity) ++qs;
+  const int ts = capacity / qs;
+  memset(out, 0, sizeof *out);
+  out->base.p = p;
+  out->base.t = t;
+  out->base.e = qs * ts;
+  out->base.d = out->base.e - 1;
+  out->base.beta = beta;
+  out->base.kmax = largest_common_dim(p, t);
+  out->base.inv_qd = ldexp(1.0, -t * out->base.d);
+  out->dq = qs - 1;
+  out->dtheta = ts - 1;
+  out->theta_exponent = t * qs;
+  return QGO_OK;
+}
+
+typedef struct {
+  const double* ca;
+  const uint32_t* b;
+  size_t k, n;
+  double* cc;
+} left_ctx;
+
+/* Hot loop of packed_left_product, gemm.hpp:354-362. */
+static void left_rows(void* vctx, size_t r0, size_t r1) {
+  const left_ctx* c = (const left_ctx*)vctx;
+  for (size_t g = r0; g < r1; ++g) {
+    double* crow = c->cc + g * c->n;
+    for (size_t j = 0; j < c->n; ++j) crow[j] = 0.0;
+    for (size_t l = 0; l < c->k; ++l) {
+      const double w = c->ca[g * c->k + l];
+      const uint32_t* brow = c->b + l * c->n;
+      for (size_t j = 0; j < c->n; ++j) crow[j] += w * (double)brow[j];
+    }
+  }
+}
+
+/* packed_left_product, gemm.hpp:340-364: ca is ceil(m/e) x k (compress_outer_rows). */
+int qgo_packed_left_product(const qgo_plan* plan, const double* ca, const uint32_t* b, size_t m, size_t k,
+                            size_t n, double* cc, int threads) {
+  if (k > plan->kmax) return QGO_PLAN_MISMATCH;
+  left_ctx c = {ca, b, k, n, cc};
+  parallel_rows(left_rows, &c, group_count(m, plan->e), threads);
+  return QGO_OK;
+}
+
+/* mul_left_compressed, gemm.hpp:366-371. */
+int qgo_mul_left_compressed(const qgo_plan* plan, const double* ca, const uint32_t* b, size_t m, size_t k,
+                            size_t n, double* cc, int threads) {
+  int st = qgo_packed_left_product(plan, ca, b, m, k, n, cc, threads);
+  if (!st) st = qgo_redq_in_place(plan, cc, group_count(m, plan->e) * n);
+  return st;
+}
+
+/* mul_full_compressed, gemm.hpp:377-445: rows of A packed in base Q with
+ * dq+1 slots, columns of B in base Theta = Q^(dq+1) with dtheta+1 slots; digit
+ * (i, j) of entry (g, h) at base-Q position i + j (dq+1) is C[g(dq+1)+i][h(dtheta+1)+j]. */
+int qgo_mul_full_compressed(const qgo_full_plan* fp, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                            size_t n, uint32_t* c) {
+  const qgo_plan* pl = &fp->base;
+  if (pl->beta > 53) return QGO_PLAN_MISMATCH;
+  if (k > pl->kmax) return QGO_PLAN_MISMATCH;
+  const int qs = fp->dq + 1, ts = fp->dtheta + 1, t = pl->t;
+  const size_t gr = group_count(m, qs), hc = group_count(n, ts);
+  double* ma = (double*)malloc((gr * k + 1) * sizeof(double));
+  double* mb = (double*)malloc((k * hc + 1) * sizeof(double));
+  double* acc = (double*)calloc(gr * hc + 1, sizeof(double));
+  for (size_t g = 0; g < gr; ++g)
+    for (size_t l = 0; l < k; ++l) {
+      uint64_t w = 0;
+      const size_t len = m - g * qs < (size_t)qs ? m - g * qs : (size_t)qs;
+      for (size_t s = len; s-- > 0;) w = (w << t) | a[(g * qs + s) * k + l];
+      ma[g * k + l] = (double)w;
+    }
+  for (size_t l = 0; l < k; ++l)
+    for (size_t h = 0; h < hc; ++h) {
+      uint64_t w = 0;
+      const size_t len = n - h * ts < (size_t)ts ? n - h * ts : (size_t)ts;
+      for (size_t s = len; s-- > 0;) w = (w << fp->theta_exponent) | b[l * n + h * ts + s];
+      mb[l * hc + h] = (double)w;
+    }
+  for (size_t g = 0; g < gr; ++g)
+    for (size_t l = 0; l < k; ++l) {
+      const double w = ma[g * k + l];
+      for (size_t h = 0; h < hc; ++h) acc[g * hc + h] += w * mb[l * hc + h];
+    }
+  const uint64_t mask = (UINT64_C(1) << t) - 1;
+  for (size_t g = 0; g < gr; ++g)
+    for (size_t h = 0; h < hc; ++h) {
+      const uint64_t bits = (uint64_t)acc[g * hc + h];
+      for (int j = 0; j < ts; ++j)
+        for (int i = 0; i < qs; ++i) {
+          const uint64_t digit = (bits >> (t * (i + j * qs))) & mask;
+          const size_t row = g * qs + i, col = h * ts + j;
+          if (row < m && col < n) c[row * n + col] = (uint32_t)(digit % pl->p);
+        }
+    }
+  free(ma);
+  free(mb);
+  free(acc);
+  return QGO_OK;
+}
+
 /* blocked_accumulate, gemm.hpp:450-489: k-panels, mod-p accumulation between them. */
 int qgo_blocked_accumulate(const qgo_plan* plan, const uint32_t* a, const uint32_t* b,
                            size_t m, size_t k, size_t n, size_t kpanel, uint32_t* c,

@@ -261,6 +261,36 @@ int qgref_mul_right(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, 
   });
 }
 
+int qgref_plan_full(uint32_t p, uint64_t k, int beta, qgo_full_plan* out) {
+  return guarded([&] {
+    const FullPlan fp = plan_full(PrimeModulus(p), k, beta);
+    export_plan(fp.base, &out->base);
+    out->dq = fp.dq;
+    out->dtheta = fp.dtheta;
+    out->theta_exponent = fp.theta_exponent;
+  });
+}
+
+// mul_left_compressed(compress_outer_rows(A, plan), B), gemm.hpp:366-371: post-REDQ words.
+int qgref_mul_left(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                   double* cc) {
+  return guarded([&] {
+    const auto ca = compress_outer_rows<DoubleWord>(wrap(a, m, k), import_plan(plan));
+    const auto r = mul_left_compressed(ca, wrap(b, k, n));
+    for (size_t i = 0; i < r.data.size(); ++i) cc[i] = r.data[i].value;
+  });
+}
+
+// mul_full_compressed, gemm.hpp:377-445.
+int qgref_mul_full(const qgo_full_plan* fp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                   uint32_t* c) {
+  return guarded([&] {
+    FullPlan f{import_plan(&fp->base), fp->dq, fp->dtheta, fp->theta_exponent};
+    const auto r = mul_full_compressed<DoubleWord>(wrap(a, m, k), wrap(b, k, n), f);
+    std::memcpy(c, r.data.data(), r.data.size() * sizeof(uint32_t));
+  });
+}
+
 int qgref_blocked_accumulate(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
                              size_t k, size_t n, size_t kpanel, uint32_t* c) {
   return guarded([&] {

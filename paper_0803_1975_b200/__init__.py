@@ -126,6 +126,11 @@ class _GpuPlan(ctypes.Structure):
                 ("balanced", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
+class _FullPlan(ctypes.Structure):
+    _fields_ = [("base", _Plan), ("dq", ctypes.c_int32), ("dtheta", ctypes.c_int32),
+                ("theta_exponent", ctypes.c_int32)]
+
+
 class _Orientation(ctypes.Structure):
     _fields_ = [("direction", ctypes.c_int32), ("axis", ctypes.c_int32), ("slots", ctypes.c_int32)]
 
@@ -178,6 +183,18 @@ def _load():
         "qg_pack_residues_tiled": ([u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_pack_outer_cols_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_mul_right_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_pack_outer_rows_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_residues_b_tiled": ([u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_mul_left_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_plan_full": ([u32, u64, i32, P(_FullPlan)], i32),
+        "qg_plan_full_gpu": ([u32, u64, P(_FullPlan), P(u64)], i32),
+        "qg_full_tiled_stage": ([P(_FullPlan), u64, u64, P(u32)], i32),
+        "qg_mul_full_tiled": ([P(_FullPlan), u64, vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_uncompress_full": ([P(_FullPlan), vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_host_mul_left": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_left_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_right_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_full": ([P(_FullPlan), u64, vp, vp, sz, sz, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),
@@ -691,6 +708,130 @@ def mul_right_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMa
     return CompressedMatrix(m, n, m, H, PackOrientation(PackDirection.Forward, PackAxis.Column, pl.e), pl, cc)
 
 
+# ------------------------------------------- left and full compression
+def mul_left_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMatrix:
+    """mul_left_compressed(compress_outer_rows(A, plan), B), gemm.hpp:340-371,
+    on residue tensors: A's outer-row words and B's residues as tiled blocks,
+    the REDQ contraction of the mixed variant. ceil(m/e) x n words,
+    {Forward, Row, e}; bit-identical to the reference's under a
+    CompressionPlan, k-blocked past kmax under a GpuPlan (plan_right_gpu(p, k, m))."""
+    torch = _torch()
+    _require_cuda(a, b)
+    m, k = a.shape
+    n = b.shape[1]
+    if b.shape[0] != k:
+        raise DimensionMismatch(f"inner dimensions disagree: {m}x{k} times {b.shape[0]}x{n}")
+    gp = plan if isinstance(plan, GpuPlan) else GpuPlan(plan, k, k, 0)
+    pl = gp.plan
+    g = gp._c()
+    bk = ctypes.c_uint32()
+    _check(lib.qg_right_tiled_stage(ctypes.byref(g), k, ctypes.byref(bk)))
+    bk = bk.value
+    G = (m + pl.e - 1) // pl.e
+    kt = -(-k // bk)
+    ao_t = torch.empty(-(-G // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
+    b_t = torch.empty(-(-n // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
+    c_pl = pl._c()
+    _check(lib.qg_pack_outer_rows_tiled(ctypes.byref(c_pl), bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(ao_t), _stream()))
+    _check(lib.qg_pack_residues_b_tiled(bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(b_t), _stream()))
+    cc = torch.empty((G, n), dtype=torch.float64, device=a.device)
+    _check(lib.qg_mul_left_tiled(ctypes.byref(g), _ptr(ao_t), _ptr(b_t), m, k, n, _ptr(cc), n, _stream()))
+    return CompressedMatrix(m, n, G, n, PackOrientation(PackDirection.Forward, PackAxis.Row, pl.e), pl, cc)
+
+
+def mul_left_compressed(ca, b, plan: Optional[Union[CompressionPlan, GpuPlan]] = None) -> CompressedMatrix:
+    """mul_left_compressed(ca, b), gemm.hpp:340-371. ``ca`` is the
+    compress_outer_rows matrix (its words are unpacked on the device and
+    re-packed into the tiled layout) or a residue tensor with ``plan``."""
+    if isinstance(ca, CompressedMatrix):
+        if ca.orientation.direction != PackDirection.Forward or ca.orientation.axis != PackAxis.Row:
+            raise PlanMismatch("left product needs the left operand packed forward on its rows")
+        if ca.logical_cols != b.shape[0]:
+            raise DimensionMismatch(f"inner dimensions disagree: {ca.logical_rows}x{ca.logical_cols} "
+                                    f"times {b.shape[0]}x{b.shape[1]}")
+        if ca.logical_cols > ca.plan.kmax:
+            raise PlanMismatch("common dimension exceeds the plan's kmax")
+        return mul_left_tiled(uncompress(ca), b, ca.plan)
+    if plan is None:
+        raise InvalidArgument("a residue operand needs a plan")
+    return mul_left_tiled(ca, b, plan)
+
+
+@dataclasses.dataclass
+class FullPlan:
+    """FullPlan, plan.hpp:44-57: base.e = (dq+1)(dtheta+1) base-Q digits per
+    word, rows of A in dq+1 slots of radix Q, columns of B in dtheta+1 slots of
+    radix Theta = 2^theta_exponent = Q^(dq+1)."""
+
+    base: CompressionPlan
+    dq: int
+    dtheta: int
+    theta_exponent: int
+
+    def q_slots(self) -> int:
+        return self.dq + 1
+
+    def theta_slots(self) -> int:
+        return self.dtheta + 1
+
+    def _c(self) -> _FullPlan:
+        return _FullPlan(self.base._c(), self.dq, self.dtheta, self.theta_exponent)
+
+    @staticmethod
+    def _from(c: _FullPlan) -> "FullPlan":
+        return FullPlan(CompressionPlan._from(c.base), c.dq, c.dtheta, c.theta_exponent)
+
+
+def plan_full(p: int, k: int, beta: int = 53) -> FullPlan:
+    """plan_full(PrimeModulus(p), k, beta), plan.hpp:229-252."""
+    out = _FullPlan()
+    _check(lib.qg_plan_full(p, k, beta, ctypes.byref(out)))
+    return FullPlan._from(out)
+
+
+def plan_full_gpu(p: int, k: int):
+    """(FullPlan, kblock residues) for the full variant on the tensor-core path."""
+    out = _FullPlan()
+    kb = ctypes.c_uint64()
+    _check(lib.qg_plan_full_gpu(p, k, ctypes.byref(out), ctypes.byref(kb)))
+    return FullPlan._from(out), kb.value
+
+
+def mul_full_compressed(a, b, fp: FullPlan, kblock_words: int = 0):
+    """mul_full_compressed(A, B, fp), gemm.hpp:377-445, on residue tensors:
+    int32 m x n residues of A B mod p. kblock_words = 0 keeps the reference's
+    single block (k <= kmax); plan_full_gpu's value blocks k past it."""
+    torch = _torch()
+    _require_cuda(a, b)
+    m, k = a.shape
+    n = b.shape[1]
+    if b.shape[0] != k:
+        raise DimensionMismatch(f"inner dimensions disagree: {m}x{k} times {b.shape[0]}x{n}")
+    if fp.base.beta > 53:
+        raise PlanMismatch("plan word width exceeds the DoubleWord backend")
+    if not kblock_words and k > fp.base.kmax:
+        raise PlanMismatch("common dimension exceeds the plan's kmax")
+    f = fp._c()
+    bk = ctypes.c_uint32()
+    _check(lib.qg_full_tiled_stage(ctypes.byref(f), kblock_words, k, ctypes.byref(bk)))
+    bk = bk.value
+    qs, ts = fp.q_slots(), fp.theta_slots()
+    G, H = -(-m // qs), -(-n // ts)
+    kt = -(-k // bk)
+    ao_t = torch.empty(-(-G // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
+    bo_t = torch.empty(-(-H // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
+    pa = _Plan(fp.base.p, fp.base.t, qs - 1, qs, fp.base.beta, fp.base.kmax, 1.0, 0)
+    pb = _Plan(fp.base.p, fp.theta_exponent, ts - 1, ts, fp.base.beta, fp.base.kmax, 1.0, 0)
+    _check(lib.qg_pack_outer_rows_tiled(ctypes.byref(pa), bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(ao_t), _stream()))
+    _check(lib.qg_pack_outer_cols_tiled(ctypes.byref(pb), bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(bo_t), _stream()))
+    cc = torch.empty((G, H), dtype=torch.float64, device=a.device)
+    _check(lib.qg_mul_full_tiled(ctypes.byref(f), kblock_words, _ptr(ao_t), _ptr(bo_t), m, k, n, _ptr(cc), H,
+                                 _stream()))
+    c = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    _check(lib.qg_uncompress_full(ctypes.byref(f), _ptr(cc), H, m, n, _ptr(c), n, _stream()))
+    return c
+
+
 def residue_checksum(c) -> int:
     """bench.hpp:43-47: sum of residues mod 2^32."""
     torch = _torch()
@@ -742,16 +883,51 @@ def blocked_accumulate_host(a, b, plan: CompressionPlan, kpanel: int) -> np.ndar
     return c
 
 
-def mul_right_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+def mul_right_compressed_host(a, b, plan: Union[CompressionPlan, GpuPlan], out=None) -> np.ndarray:
     """mul_right_compressed(A, compress_outer_cols(B, plan)) on host data:
-    the post-REDQ words, m x ceil(n/e) float64."""
+    the post-REDQ words, m x ceil(n/e) float64. A GpuPlan (plan_right_gpu)
+    blocks k past kmax."""
     a, b = _host_u32(a), _host_u32(b)
     if a.shape[1] != b.shape[0]:
         raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
     m, k = a.shape
     n = b.shape[1]
-    cc = np.empty((m, (n + plan.e - 1) // plan.e), dtype=np.float64)
+    e = plan.plan.e if isinstance(plan, GpuPlan) else plan.e
+    cc = np.empty((m, (n + e - 1) // e), dtype=np.float64) if out is None else out
+    fn = lib.qg_host_mul_right_gpu if isinstance(plan, GpuPlan) else lib.qg_host_mul_right
     pl = plan._c()
-    _check(lib.qg_host_mul_right(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
-                                 m, k, n, cc.ctypes.data_as(ctypes.c_void_p)))
+    _check(fn(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
+              m, k, n, cc.ctypes.data_as(ctypes.c_void_p)))
     return cc
+
+
+def mul_left_compressed_host(a, b, plan: Union[CompressionPlan, GpuPlan], out=None) -> np.ndarray:
+    """mul_left_compressed(compress_outer_rows(A, plan), B) on host data: the
+    post-REDQ words, ceil(m/e) x n float64. A GpuPlan (plan_right_gpu(p, k,
+    m)) blocks k past kmax."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
+    e = plan.plan.e if isinstance(plan, GpuPlan) else plan.e
+    cc = np.empty(((m + e - 1) // e, n), dtype=np.float64) if out is None else out
+    fn = lib.qg_host_mul_left_gpu if isinstance(plan, GpuPlan) else lib.qg_host_mul_left
+    pl = plan._c()
+    _check(fn(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
+              m, k, n, cc.ctypes.data_as(ctypes.c_void_p)))
+    return cc
+
+
+def mul_full_compressed_host(a, b, fp: FullPlan, kblock_words: int = 0, out=None) -> np.ndarray:
+    """mul_full_compressed(A, B, fp), gemm.hpp:377-445, on host data."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
+    c = np.empty((m, n), dtype=np.uint32) if out is None else out
+    f = fp._c()
+    _check(lib.qg_host_mul_full(ctypes.byref(f), kblock_words, a.ctypes.data_as(ctypes.c_void_p),
+                                b.ctypes.data_as(ctypes.c_void_p), m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
+    return c

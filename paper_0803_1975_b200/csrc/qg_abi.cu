@@ -16,6 +16,7 @@ bool is_prime(uint64_t n);
 uint64_t max_exact_block(uint32_t p, int t, int e);
 uint64_t stage_block(uint64_t limit, int* bk);
 uint64_t stage_block_tiled(uint64_t limit, int* bk);
+uint64_t stage_block_redq(uint64_t limit, int* bk);
 uint64_t max_exact_block_balanced(uint32_t p, int t, int e);
 }  // namespace qg
 
@@ -209,7 +210,7 @@ static int right_tiled_geometry(const qg_gpu_plan* gp, uint64_t k, int* bk, int*
     *kb_stages = 0;
     return QG_OK;
   }
-  const uint64_t blk = qg::stage_block_tiled(kb, bk);
+  const uint64_t blk = qg::stage_block_redq(kb, bk);
   if (blk < 4) return QG_INVALID_ARGUMENT;
   *kb_stages = (int)(blk / *bk);
   return QG_OK;
@@ -242,9 +243,13 @@ int qg_pack_outer_cols_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg
                                                   as_stream(stream)));
 }
 
-int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double* bo_t, size_t m, size_t k,
-                       size_t n, double* cc, size_t ldcc, void* stream) {
-  if (!gplan) return QG_INVALID_ARGUMENT;
+// The exact contraction with in-place REDQ shared by the right, left and
+// full variants: cc (M x N words) = REDQ(A_t x B_t^T), the accumulators REDQ'd
+// every kblock residues of k. Every digit of a block stays below Q while
+// (p-1) + kb (p-1)^2 < Q (the previous block's REDQ'd digit plus the block's
+// sum); a single block needs k <= kmax (gemm.hpp:295).
+static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const double* b_t, size_t M, size_t k,
+                        size_t N, double* cc, size_t ldcc, void* stream) {
   const qg_plan& pl = gplan->plan;
   int st = check_plan(&pl);
   if (st) return st;
@@ -254,25 +259,24 @@ int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gplan, k, &bk, &kbs))) return st;
   if (kbs == 0) {
-    if (k > pl.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
+    if (k > pl.kmax) return QG_PLAN_MISMATCH;
   } else if ((pl.p - 1) + (uint64_t)kbs * bk * pm >= Q) {
     return QG_PLAN_MISMATCH;  // a block would overflow a digit after the in-place REDQ
   }
-  const size_t H = ceil_div(n, pl.e);
-  if (ldcc < H) return QG_INVALID_ARGUMENT;
-  if (m == 0 || H == 0) return QG_OK;
+  if (ldcc < N) return QG_INVALID_ARGUMENT;
+  if (M == 0 || N == 0) return QG_OK;
   cudaStream_t s = as_stream(stream);
   if (k == 0) {
-    for (size_t i = 0; i < m; ++i)
-      if (cudaMemsetAsync(cc + i * ldcc, 0, H * sizeof(double), s) != cudaSuccess) return QG_CUDA_ERROR;
+    if (cudaMemset2DAsync(cc, ldcc * sizeof(double), 0, N * sizeof(double), M, s) != cudaSuccess)
+      return QG_CUDA_ERROR;
     return QG_OK;
   }
   qgk::GemmArgs r;
   std::memset(&r, 0, sizeof r);
   r.a = a_t;
-  r.b = bo_t;
-  r.M = (int)m;
-  r.N = (int)H;
+  r.b = b_t;
+  r.M = (int)M;
+  r.N = (int)N;
   r.K = (int)k;
   r.kb_stages = kbs;
   r.t = pl.t;
@@ -281,6 +285,87 @@ int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double
   r.cc = cc;
   r.ldcc = ldcc;
   return cuda_status(qgk::launch_right_tiled(r, bk, true, s, &g_last_kernel));
+}
+
+int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double* bo_t, size_t m, size_t k,
+                       size_t n, double* cc, size_t ldcc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  if (gplan->plan.e < 1) return QG_PLAN_MISMATCH;
+  return redq_product(gplan, a_t, bo_t, m, k, ceil_div(n, (size_t)gplan->plan.e), cc, ldcc, stream);
+}
+
+// ---- left and full compression (gemm.hpp:340-445) on the same contraction
+int qg_pack_outer_rows_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
+                             size_t lda, double* ao_t, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (lda < k || bk < 1) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_outer_rows_tiled(a, dtype, m, k, lda, plan->t, plan->e, (int)bk, ao_t,
+                                                       as_stream(stream)));
+}
+
+int qg_pack_residues_b_tiled(uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n, size_t ldb,
+                             double* b_t, void* stream) {
+  int st = check_dtype(dtype);
+  if (st) return st;
+  if (ldb < n) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_tiled(true, b, dtype, k, n, ldb, 1, 1, (int)bk, b_t, as_stream(stream), 2,
+                                            false));
+}
+
+int qg_mul_left_tiled(const qg_gpu_plan* gplan, const double* ao_t, const double* b_t, size_t m, size_t k,
+                      size_t n, double* cc, size_t ldcc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  if (gplan->plan.e < 1) return QG_PLAN_MISMATCH;
+  return redq_product(gplan, ao_t, b_t, ceil_div(m, (size_t)gplan->plan.e), k, n, cc, ldcc, stream);
+}
+
+static int full_gpu_plan(const qg_full_plan* fp, uint64_t kblock_words, uint64_t k, qg_gpu_plan* gp) {
+  if (!fp) return QG_INVALID_ARGUMENT;
+  int st = check_plan(&fp->base);
+  if (st) return st;
+  const int qs = fp->dq + 1, ts = fp->dtheta + 1;
+  if (qs < 1 || ts < 1 || fp->base.e != qs * ts || fp->theta_exponent != fp->base.t * qs)
+    return QG_PLAN_MISMATCH;
+  std::memset(gp, 0, sizeof *gp);
+  gp->plan = fp->base;
+  gp->kblock_words = kblock_words ? kblock_words : (k ? k : 1);
+  gp->max_exact_words = gp->kblock_words;
+  return QG_OK;
+}
+
+int qg_full_tiled_stage(const qg_full_plan* fp, uint64_t kblock_words, uint64_t k, uint32_t* bk) {
+  qg_gpu_plan gp;
+  int st = full_gpu_plan(fp, kblock_words, k, &gp);
+  if (st) return st;
+  return qg_right_tiled_stage(&gp, k, bk);
+}
+
+int qg_mul_full_tiled(const qg_full_plan* fp, uint64_t kblock_words, const double* ao_t, const double* bo_t,
+                      size_t m, size_t k, size_t n, double* cc, size_t ldcc, void* stream) {
+  qg_gpu_plan gp;
+  int st = full_gpu_plan(fp, kblock_words, k, &gp);
+  if (st) return st;
+  return redq_product(&gp, ao_t, bo_t, ceil_div(m, (size_t)fp->dq + 1), k, ceil_div(n, (size_t)fp->dtheta + 1),
+                      cc, ldcc, stream);
+}
+
+int qg_uncompress_full(const qg_full_plan* fp, const double* cc, size_t ldcc, size_t m, size_t n, int32_t* c,
+                       size_t ldc, void* stream) {
+  qg_gpu_plan gp;
+  int st = full_gpu_plan(fp, 0, 1, &gp);
+  if (st) return st;
+  if (ldc < n || ldcc < ceil_div(n, (size_t)fp->dtheta + 1)) return QG_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  DeviceFlag flag(s);
+  if (!flag.ptr) return QG_CUDA_ERROR;
+  if ((st = cuda_status(qgk::launch_uncompress_full(cc, ldcc, m, n, fp->base.t, fp->base.e, fp->dq + 1,
+                                                    fp->dtheta + 1, fp->base.p, c, ldc, flag.ptr, s))))
+    return st;
+  int over = 0;
+  if ((st = flag.read(&over))) return st;
+  return over ? QG_DIGIT_OVERFLOW : QG_OK;
 }
 
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,
@@ -730,22 +815,18 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
   return QG_OK;
 }
 
-int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
-                      size_t k, size_t n, double* cc) {
+// Host-data right / left products on the tiled path. gp's kblock_words
+// bounds the in-place REDQ blocks (kblock >= k: the reference's single block).
+static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                      double* cc) {
+  const qg_plan* plan = &gp->plan;
   int st = check_plan(plan);
   if (st) return st;
-  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
   cudaStream_t s = nullptr;
-  const size_t H = ceil_div(n, plan->e);
+  const size_t H = ceil_div(n, (size_t)plan->e);
   if (m * H == 0) return QG_OK;
-  // tiled layout, one k-block under the caller's plan: words bit-identical to
-  // mul_right_compressed(A, compress_outer_cols(B, plan)), gemm.hpp:320-325
-  qg_gpu_plan gp;
-  std::memset(&gp, 0, sizeof gp);
-  gp.plan = *plan;
-  gp.kblock_words = k ? k : 1;
   int bk = 0, kbs = 0;
-  if ((st = right_tiled_geometry(&gp, k ? k : 1, &bk, &kbs))) return st;
+  if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
   DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
   QG_TRY(da.alloc(m * k * 4));
@@ -759,9 +840,125 @@ int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
     if ((st = qg_pack_residues_tiled((uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
     if ((st = qg_pack_outer_cols_tiled(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
   }
-  if ((st = qg_mul_right_tiled(&gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, H, s)))
+  if ((st = qg_mul_right_tiled(gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, H, s)))
     return st;
   QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                     double* cc) {
+  const qg_plan* plan = &gp->plan;
+  int st = check_plan(plan);
+  if (st) return st;
+  cudaStream_t s = nullptr;
+  const size_t G = ceil_div(m, (size_t)plan->e);
+  if (G * n == 0) return QG_OK;
+  int bk = 0, kbs = 0;
+  if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
+  const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
+  DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dat.alloc(ceil_div(G, 128) * 128 * kt * bk * 8));
+  QG_TRY(dbt.alloc(ceil_div(n, 128) * 128 * kt * bk * 8));
+  QG_TRY(dcc.alloc(G * n * 8));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  if (k) {
+    if ((st = qg_pack_outer_rows_tiled(plan, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
+    if ((st = qg_pack_residues_b_tiled((uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
+  }
+  if ((st = qg_mul_left_tiled(gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, n, s)))
+    return st;
+  QG_TRY(cudaMemcpyAsync(cc, dcc.p, G * n * 8, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+static qg_gpu_plan single_block(const qg_plan* plan, size_t k) {
+  qg_gpu_plan gp;
+  std::memset(&gp, 0, sizeof gp);
+  gp.plan = *plan;
+  gp.kblock_words = k ? k : 1;
+  gp.max_exact_words = gp.kblock_words;
+  return gp;
+}
+
+int qg_host_mul_right(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                      size_t k, size_t n, double* cc) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
+  // one k-block under the caller's plan: words bit-identical to
+  // mul_right_compressed(A, compress_outer_cols(B, plan)), gemm.hpp:320-325
+  const qg_gpu_plan gp = single_block(plan, k);
+  return host_right(&gp, a, b, m, k, n, cc);
+}
+
+int qg_host_mul_right_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                          size_t n, double* cc) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  return host_right(gplan, a, b, m, k, n, cc);
+}
+
+int qg_host_mul_left(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                     double* cc) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:349 check_common_dim
+  const qg_gpu_plan gp = single_block(plan, k);
+  return host_left(&gp, a, b, m, k, n, cc);
+}
+
+int qg_host_mul_left_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                         size_t n, double* cc) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  return host_left(gplan, a, b, m, k, n, cc);
+}
+
+int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32_t* a, const uint32_t* b,
+                     size_t m, size_t k, size_t n, uint32_t* c) {
+  qg_gpu_plan gp;
+  int st = full_gpu_plan(fp, kblock_words, k, &gp);
+  if (st) return st;
+  if (fp->base.beta > 53) return QG_PLAN_MISMATCH;  // gemm.hpp:383 check_backend
+  if (!kblock_words && k > fp->base.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:384
+  if (m * n == 0) return QG_OK;
+  cudaStream_t s = nullptr;
+  const int qs = fp->dq + 1, ts = fp->dtheta + 1;
+  const size_t G = ceil_div(m, (size_t)qs), H = ceil_div(n, (size_t)ts);
+  int bk = 0, kbs = 0;
+  if ((st = right_tiled_geometry(&gp, k ? k : 1, &bk, &kbs))) return st;
+  const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
+  qg_plan pa = fp->base, pb = fp->base;
+  pa.e = qs;
+  pa.d = qs - 1;
+  pb.t = fp->theta_exponent;
+  pb.e = ts;
+  pb.d = ts - 1;
+  DevBuf da(s), db(s), dat(s), dbt(s), dcc(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dat.alloc(ceil_div(G, 128) * 128 * kt * bk * 8));
+  QG_TRY(dbt.alloc(ceil_div(H, 128) * 128 * kt * bk * 8));
+  QG_TRY(dcc.alloc(G * H * 8));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  if (k) {
+    if ((st = cuda_status(qgk::launch_pack_outer_rows_tiled(da.p, QG_U32, m, k, k, pa.t, pa.e, bk, (double*)dat.p,
+                                                            s))))
+      return st;
+    if ((st = cuda_status(qgk::launch_pack_outer_tiled(db.p, QG_U32, k, n, n, pb.t, pb.e, bk, (double*)dbt.p, s))))
+      return st;
+  }
+  if ((st = qg_mul_full_tiled(fp, gp.kblock_words, (const double*)dat.p, (const double*)dbt.p, m, k, n,
+                              (double*)dcc.p, H, s)))
+    return st;
+  if ((st = qg_uncompress_full(fp, (const double*)dcc.p, H, m, n, (int32_t*)dc.p, n, s))) return st;
+  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
   return QG_OK;
 }

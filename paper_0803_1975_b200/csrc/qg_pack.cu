@@ -240,6 +240,55 @@ static cudaError_t pack_outer_tiled_dt(const TIn* src, size_t k, size_t n, size_
   return cudaErrorInvalidValue;
 }
 
+// compress_outer_rows into the tiled A layout, gemm.hpp:160-176: word (g, l)
+// = sum_s A[g e + s][l] Q^s (forward along m), stored in dense 128 x BK
+// blocks [g-tile][k-tile][g][l]. One thread per stored word, consecutive
+// threads along l, so each run of BK reads is one contiguous row segment.
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_pack_outer_rows_tiled(const TIn* __restrict__ a, size_t m, size_t k,
+                                                               size_t lda, int t, int e, int bk, unsigned Kt,
+                                                               size_t total, double* __restrict__ ao_t) {
+  const size_t G = (m + e - 1) / e;
+  const size_t tile_words = 128 * (size_t)bk;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t tile = idx / tile_words, within = idx % tile_words;
+    const size_t g = (tile / Kt) * 128 + within / bk;
+    const size_t l = (tile % Kt) * bk + within % bk;
+    uint64_t w = 0;
+    if (g < G && l < k) {
+      const size_t base = g * e;
+      const int len = (int)((m - base) < (size_t)e ? (m - base) : (size_t)e);
+      for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(a[(base + s) * lda + l]);
+    }
+    ao_t[idx] = __ull2double_rn(w);
+  }
+}
+
+// The unpack of mul_full_compressed, gemm.hpp:427-443: output cell (row, col)
+// reads base-Q digit (row mod qs) + (col mod ts) qs of word (row/qs, col/ts).
+// One thread per output cell: the stores are coalesced, the word reads hit
+// the same qs x ts footprint from neighbouring threads.
+__global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, size_t m, size_t n, int t, int e,
+                                  int qs, int ts, uint32_t p, int32_t* __restrict__ c, size_t ldc,
+                                  int* __restrict__ overflow) {
+  const double limit = (double)(1ull << (t * e));
+  const uint64_t mask = (1ull << t) - 1;
+  const size_t count = m * n;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < count;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = idx / n, col = idx % n;
+    const double v = cc[(row / qs) * ldcc + col / ts];
+    if (!(v >= 0.0) || !(v < limit)) {
+      atomicExch(overflow, 1);
+      continue;
+    }
+    const uint64_t bits = __double2ull_rz(v);
+    const int pos = (int)(row % qs) + (int)(col % ts) * qs;
+    c[row * ldc + col] = (int32_t)(((bits >> (t * pos)) & mask) % p);
+  }
+}
+
 // redq over a buffer, pack.hpp:124-137: every base-Q digit replaced by itself
 // mod p. A word outside [0, 2^(t e)) raises the DigitOverflow flag.
 __global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint32_t p,
@@ -446,6 +495,36 @@ cudaError_t launch_pack_outer_tiled(const void* src, int dtype, size_t k, size_t
     case 1: return pack_outer_tiled_dt<uint32_t>((const uint32_t*)src, k, n, ld, t, e, bk, dst, s);
     default: return pack_outer_tiled_dt<int32_t>((const int32_t*)src, k, n, ld, t, e, bk, dst, s);
   }
+}
+
+template <typename TIn>
+static cudaError_t pack_outer_rows_tiled_t(const TIn* src, size_t m, size_t k, size_t ld, int t, int e, int bk,
+                                           double* dst, cudaStream_t s) {
+  const size_t G = (m + e - 1) / e;
+  const unsigned Kt = (unsigned)((k + bk - 1) / bk);
+  const size_t total = (G + 127) / 128 * Kt * 128 * (size_t)bk;
+  if (total == 0) return cudaSuccess;
+  k_pack_outer_rows_tiled<TIn><<<grid1d(total, 256), 256, 0, s>>>(src, m, k, ld, t, e, bk, Kt, total, dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_outer_rows_tiled(const void* src, int dtype, size_t m, size_t k, size_t ld, int t, int e,
+                                         int bk, double* dst, cudaStream_t s) {
+  if (bk < 1) return cudaErrorInvalidValue;
+  switch (dtype) {
+    case 0: return pack_outer_rows_tiled_t<double>((const double*)src, m, k, ld, t, e, bk, dst, s);
+    case 1: return pack_outer_rows_tiled_t<uint32_t>((const uint32_t*)src, m, k, ld, t, e, bk, dst, s);
+    default: return pack_outer_rows_tiled_t<int32_t>((const int32_t*)src, m, k, ld, t, e, bk, dst, s);
+  }
+}
+
+cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size_t n, int t, int e, int qs, int ts,
+                                   uint32_t p, int32_t* c, size_t ldc, int* overflow, cudaStream_t s) {
+  if (m * n == 0) return cudaSuccess;
+  k_uncompress_full<<<grid1d(m * n, 256), 256, 0, s>>>(cc, ldcc, m, n, t, e, qs, ts, p, c, ldc, overflow);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_redq(double* w, size_t count, int t, int e, uint32_t p, int* overflow,

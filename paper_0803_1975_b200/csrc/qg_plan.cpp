@@ -236,6 +236,12 @@ uint64_t stage_block_tiled(uint64_t limit, int* bk) {
   return stage_block_set(limit, bk, kSet, 7);
 }
 
+// Stage depths the REDQ-epilogue (right / left / full) kernels are built for.
+uint64_t stage_block_redq(uint64_t limit, int* bk) {
+  static const int kSet[] = {36, 28, 20, 12, 4};
+  return stage_block_set(limit, bk, kSet, 5);
+}
+
 // Predicted relative cost of a blocked plan, in packed-word units: words
 // rounded up to the stage depth times the stage's per-word overhead, plus a
 // per-block flush cost.
@@ -377,7 +383,7 @@ int qg_plan_right_gpu(uint32_t p, uint64_t k, uint64_t n, qg_gpu_plan* out) {
       if (Q <= p) continue;
       kb = (Q - p) / (pm ? pm : 1);
       if (kb < 4) continue;
-      kb = stage_block_tiled(kb, nullptr);
+      kb = stage_block_redq(kb, nullptr);
       if (kb == 0) continue;
     }
     const double H = double((n + e - 1) / e);
@@ -394,6 +400,77 @@ int qg_plan_right_gpu(uint32_t p, uint64_t k, uint64_t n, qg_gpu_plan* out) {
   if (!found) return QG_NO_COMPRESSION;
   *out = best;
   return QG_OK;
+}
+
+// plan_full, plan.hpp:229-252: the word capacity at the minimal radix for k,
+// split into dq+1 = floor(sqrt(E)) base-Q slots and dtheta+1 = E/(dq+1)
+// base-Theta slots, Theta = Q^(dq+1).
+static void fill_full(qg_full_plan* out, uint32_t p, int t, int qs, int ts, int beta, uint64_t kmax) {
+  std::memset(out, 0, sizeof *out);
+  fill(&out->base, p, t, qs * ts, beta, std::ldexp(1.0, -t * (qs * ts - 1)));
+  out->base.kmax = kmax;
+  out->dq = qs - 1;
+  out->dtheta = ts - 1;
+  out->theta_exponent = t * qs;
+}
+
+static int isqrt_int(int v) {
+  int r = int(std::sqrt(double(v)));
+  while (r * r > v) --r;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  return r;
+}
+
+int qg_plan_full(uint32_t p, uint64_t k, int beta, qg_full_plan* out) {
+  if (!out) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1 || beta < 2) return QG_INVALID_ARGUMENT;
+  const int t = minimal_radix_exponent(p, k);
+  const int capacity = t < beta ? word_capacity(t, beta) : 0;
+  if (capacity < 4) return QG_NO_COMPRESSION;  // plan.hpp:235-237
+  const int qs = isqrt_int(capacity);
+  fill_full(out, p, t, qs, capacity / qs, beta, largest_common_dim(p, t));
+  return QG_OK;
+}
+
+// GPU planner for the full variant: the same slot split as plan_full, but t
+// and the k-block are free. A block of kb residues keeps every digit exact
+// after the in-place REDQ while (p-1) + kb (p-1)^2 < Q; cost is packed-word
+// products (k / ((dq+1)(dtheta+1)) per output cell) plus a per-flush REDQ of
+// e digits, as in qg_plan_right_gpu.
+int qg_plan_full_gpu(uint32_t p, uint64_t k, qg_full_plan* out, uint64_t* kblock_words) {
+  if (!out || !kblock_words) return QG_INVALID_ARGUMENT;
+  if (p < 2 || !is_prime(p)) return QG_INVALID_MODULUS;
+  if (k < 1) return QG_INVALID_ARGUMENT;
+  const uint64_t pm = pm1sq(p);
+  double best_cost = 1e300;
+  bool found = false;
+  for (int t = 1; t <= 52; ++t) {
+    const int cap = word_capacity(t, 53);
+    if (cap < 1) continue;
+    const int qs = isqrt_int(cap), ts = cap / qs, e = qs * ts;
+    const uint64_t Q = uint64_t(1) << t;
+    const uint64_t km = largest_common_dim(p, t);
+    if (km == 0) continue;
+    uint64_t kb;
+    if (k <= km) kb = k;
+    else {
+      if (Q <= p) continue;
+      kb = (Q - p) / (pm ? pm : 1);
+      if (kb < 4) continue;
+      kb = stage_block_redq(kb, nullptr);
+      if (kb == 0) continue;
+    }
+    const double nflush = kb >= k ? 0.0 : double((k + kb - 1) / kb);
+    const double cost = (double(k) + 4.0 * e * nflush) / double(e);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      found = true;
+      fill_full(out, p, t, qs, ts, 53, km);
+      *kblock_words = kb;
+    }
+  }
+  return found ? QG_OK : QG_NO_COMPRESSION;
 }
 
 int qg_max_exact_block_balanced(const qg_plan* plan, uint64_t* words) {

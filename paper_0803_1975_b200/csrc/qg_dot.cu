@@ -172,6 +172,34 @@ __device__ __forceinline__ double redq_word(double w, int t, int e, const ModP& 
   return __ull2double_rn(r);
 }
 
+// In-place REDQ of a whole warp tile of exact words 0 <= w < 2^52 (t <= 31,
+// t e <= 52). Each word lives as the raw bits of w + 2^52 (low 52 bits = w);
+// for every digit offset o the digit x = (u >> o) mod Q leaves u as
+// u -= (x - x mod p) << o, which replaces the digit by its residue without a
+// borrow. The digit loop is outermost (uniform trip count) and the words are
+// unrolled inside it, so the 2 MI NI independent chains interleave instead of
+// running one latency-bound word at a time.
+template <int NW>
+__device__ __forceinline__ void redq_words_inplace(double* w, int t, int e, const ModP& modp) {
+  const uint32_t qmask = (1u << t) - 1;
+  uint64_t u[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) u[i] = (uint64_t)__double_as_longlong(w[i] + 4503599627370496.0);
+  const int total = t * e;
+  for (int o = 0; o < total; o += t) {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const uint32_t x = (uint32_t)(u[i] >> o) & qmask;
+      const uint32_t q = __umulhi(x, modp.magic);
+      const uint32_t r0 = x - q * modp.p;  // x mod p or x mod p + p
+      const uint32_t r = min(r0, r0 - modp.p);
+      u[i] -= (uint64_t)(x - r) << o;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NW; ++i) w[i] = __longlong_as_double((long long)u[i]) - 4503599627370496.0;
+}
+
 template <int BK, int VEC, int EPI, bool MULTI>
 __global__ void __launch_bounds__(NT, 1) k_gemm_dmma(GemmArgs args) {
   using G = Geo<BK>;
@@ -471,12 +499,18 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
       if (MULTI && EPI == EPI_REDQ) {  // mixed variant: in-place REDQ between k-blocks
         if (++kst == args.kb_stages) {
           kst = 0;
+          if (args.debug & 8) {
+            // debug bit 3: timing without the in-place REDQ (wrong results)
+          } else if (args.t <= 31 && args.t * args.e <= 52) {
+            redq_words_inplace<MI * NI * 2>(&acc[0][0][0], args.t, args.e, modp);
+          } else {
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni)
+              for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
-              for (int h = 0; h < 2; ++h) acc[mi][ni][h] = redq_word(acc[mi][ni][h], args.t, args.e, modp);
+                for (int h = 0; h < 2; ++h) acc[mi][ni][h] = redq_word(acc[mi][ni][h], args.t, args.e, modp);
+          }
         }
       } else if (MULTI && (MID == 0 || SPLIT)) {  // (MID != 0 flushes inside the unrolled k-steps)
         if (SPLIT || ++kst == args.kb_stages) {  // SPLIT (kb_stages == 1): even accumulator rows end here
@@ -501,6 +535,18 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
       }
     }
     // epilogue of this tile (the producer is already filling the next tile's stages)
+    if (EPI == EPI_REDQ) {  // redq, pack.hpp:124-137, on the whole warp tile
+      if (args.t <= 31 && args.t * args.e <= 52) {
+        redq_words_inplace<MI * NI * 2>(&acc[0][0][0], args.t, args.e, modp);
+      } else {
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[mi][ni][h] = redq_word(acc[mi][ni][h], args.t, args.e, modp);
+      }
+    }
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
       const int row = m0 + warp_m * WM + mi * 8 + g;
@@ -525,9 +571,7 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (col + h >= N) continue;
-            double w = acc[mi][ni][h];
-            if (EPI == EPI_REDQ) w = redq_word(w, args.t, args.e, modp);
-            args.cc[(size_t)row * args.ldcc + col + h] = w;
+            args.cc[(size_t)row * args.ldcc + col + h] = acc[mi][ni][h];
           }
         }
         acc[mi][ni][0] = acc[mi][ni][1] = 0.0;

@@ -265,27 +265,43 @@ __global__ void __launch_bounds__(256) k_pack_outer_rows_tiled(const TIn* __rest
   }
 }
 
-// The unpack of mul_full_compressed, gemm.hpp:427-443: output cell (row, col)
-// reads base-Q digit (row mod qs) + (col mod ts) qs of word (row/qs, col/ts).
-// One thread per output cell: the stores are coalesced, the word reads hit
-// the same qs x ts footprint from neighbouring threads.
-__global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, size_t m, size_t n, int t, int e,
+// The unpack of mul_full_compressed, gemm.hpp:427-443: output cell
+// (g qs + i, h ts + j) is base-Q digit i + j qs of word (g, h). One thread per
+// (output row, word column): it reads the word once and writes its ts
+// consecutive cells, so a warp's stores cover one contiguous row segment.
+// 32-bit index arithmetic only (rows and words per row < 2^31).
+__global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, unsigned m, unsigned n, int t, int e,
                                   int qs, int ts, uint32_t p, int32_t* __restrict__ c, size_t ldc,
                                   int* __restrict__ overflow) {
   const double limit = (double)(1ull << (t * e));
   const uint64_t mask = (1ull << t) - 1;
-  const size_t count = m * n;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < count;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t row = idx / n, col = idx % n;
-    const double v = cc[(row / qs) * ldcc + col / ts];
-    if (!(v >= 0.0) || !(v < limit)) {
-      atomicExch(overflow, 1);
-      continue;
+  const unsigned H = (n + ts - 1) / ts;
+  const uint32_t magic = (uint32_t)(0x100000000ull / p);
+  for (unsigned row = blockIdx.y; row < m; row += gridDim.y) {
+    const unsigned g = row / qs, i = row - g * qs;
+    const double* wrow = cc + (size_t)g * ldcc;
+    int32_t* crow = c + (size_t)row * ldc;
+    for (unsigned h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+      const double v = wrow[h];
+      if (!(v >= 0.0) || !(v < limit)) {
+        atomicExch(overflow, 1);
+        continue;
+      }
+      const uint64_t bits = __double2ull_rz(v) >> (t * i);
+      const unsigned col0 = h * ts;
+      for (int j = 0; j < ts && col0 + j < n; ++j) {
+        const uint64_t x64 = (bits >> (t * j * qs)) & mask;
+        uint32_t r;
+        if (t > 31) {
+          r = (uint32_t)(x64 % p);  // one-digit words of a wide radix
+        } else {
+          const uint32_t x = (uint32_t)x64;
+          r = x - __umulhi(x, magic) * p;
+          r = r >= p ? r - p : r;
+        }
+        crow[col0 + j] = (int32_t)r;
+      }
     }
-    const uint64_t bits = __double2ull_rz(v);
-    const int pos = (int)(row % qs) + (int)(col % ts) * qs;
-    c[row * ldc + col] = (int32_t)(((bits >> (t * pos)) & mask) % p);
   }
 }
 
@@ -522,7 +538,10 @@ cudaError_t launch_pack_outer_rows_tiled(const void* src, int dtype, size_t m, s
 cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size_t n, int t, int e, int qs, int ts,
                                    uint32_t p, int32_t* c, size_t ldc, int* overflow, cudaStream_t s) {
   if (m * n == 0) return cudaSuccess;
-  k_uncompress_full<<<grid1d(m * n, 256), 256, 0, s>>>(cc, ldcc, m, n, t, e, qs, ts, p, c, ldc, overflow);
+  if (m >= (1u << 31) || n >= (1u << 31)) return cudaErrorInvalidValue;
+  const unsigned H = (unsigned)((n + ts - 1) / ts);
+  const dim3 grid((H + 127) / 128, (unsigned)(m < 65535 ? m : 65535));
+  k_uncompress_full<<<grid, 128, 0, s>>>(cc, ldcc, (unsigned)m, (unsigned)n, t, e, qs, ts, p, c, ldc, overflow);
   count_launch();
   return cudaGetLastError();
 }

@@ -233,12 +233,15 @@ int qg_pack_residues_tiled(uint32_t bk, const void* a, qg_dtype dtype, size_t m,
   return cuda_status(qgk::launch_pack_tiled(false, a, dtype, m, k, lda, 1, 1, (int)bk, a_t, as_stream(stream)));
 }
 
+// the stage depths the REDQ-epilogue kernels and their packs are built for
+static bool redq_stage_ok(uint32_t bk) { return bk == 4 || bk == 12 || bk == 20 || bk == 28 || bk == 36; }
+
 int qg_pack_outer_cols_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
                              size_t ldb, double* bo_t, void* stream) {
   int st = check_plan(plan);
   if (st) return st;
   if ((st = check_dtype(dtype))) return st;
-  if (ldb < n) return QG_INVALID_ARGUMENT;
+  if (ldb < n || !redq_stage_ok(bk)) return QG_INVALID_ARGUMENT;
   return cuda_status(qgk::launch_pack_outer_tiled(b, dtype, k, n, ldb, plan->t, plan->e, (int)bk, bo_t,
                                                   as_stream(stream)));
 }
@@ -295,12 +298,13 @@ int qg_mul_right_tiled(const qg_gpu_plan* gplan, const double* a_t, const double
 }
 
 // ---- left and full compression (gemm.hpp:340-445) on the same contraction
+
 int qg_pack_outer_rows_tiled(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
                              size_t lda, double* ao_t, void* stream) {
   int st = check_plan(plan);
   if (st) return st;
   if ((st = check_dtype(dtype))) return st;
-  if (lda < k || bk < 1) return QG_INVALID_ARGUMENT;
+  if (lda < k || !redq_stage_ok(bk)) return QG_INVALID_ARGUMENT;
   return cuda_status(qgk::launch_pack_outer_rows_tiled(a, dtype, m, k, lda, plan->t, plan->e, (int)bk, ao_t,
                                                        as_stream(stream)));
 }
@@ -357,15 +361,8 @@ int qg_uncompress_full(const qg_full_plan* fp, const double* cc, size_t ldcc, si
   int st = full_gpu_plan(fp, 0, 1, &gp);
   if (st) return st;
   if (ldc < n || ldcc < ceil_div(n, (size_t)fp->dtheta + 1)) return QG_INVALID_ARGUMENT;
-  cudaStream_t s = as_stream(stream);
-  DeviceFlag flag(s);
-  if (!flag.ptr) return QG_CUDA_ERROR;
-  if ((st = cuda_status(qgk::launch_uncompress_full(cc, ldcc, m, n, fp->base.t, fp->base.e, fp->dq + 1,
-                                                    fp->dtheta + 1, fp->base.p, c, ldc, flag.ptr, s))))
-    return st;
-  int over = 0;
-  if ((st = flag.read(&over))) return st;
-  return over ? QG_DIGIT_OVERFLOW : QG_OK;
+  return cuda_status(qgk::launch_uncompress_full(cc, ldcc, m, n, fp->base.t, fp->dq + 1, fp->dtheta + 1, fp->base.p,
+                                                 c, ldc, as_stream(stream)));
 }
 
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,

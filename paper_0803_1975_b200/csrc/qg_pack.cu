@@ -242,26 +242,26 @@ static cudaError_t pack_outer_tiled_dt(const TIn* src, size_t k, size_t n, size_
 
 // compress_outer_rows into the tiled A layout, gemm.hpp:160-176: word (g, l)
 // = sum_s A[g e + s][l] Q^s (forward along m), stored in dense 128 x BK
-// blocks [g-tile][k-tile][g][l]. One thread per stored word, consecutive
-// threads along l, so each run of BK reads is one contiguous row segment.
-template <typename TIn>
+// blocks [g-tile][k-tile][g][l]. One CTA per block; consecutive threads run
+// along l, so each run of BK reads is one contiguous row segment and the
+// block is written contiguously.
+template <typename TIn, int BK>
 __global__ void __launch_bounds__(256) k_pack_outer_rows_tiled(const TIn* __restrict__ a, size_t m, size_t k,
-                                                               size_t lda, int t, int e, int bk, unsigned Kt,
-                                                               size_t total, double* __restrict__ ao_t) {
+                                                               size_t lda, int t, int e, unsigned Kt,
+                                                               double* __restrict__ ao_t) {
   const size_t G = (m + e - 1) / e;
-  const size_t tile_words = 128 * (size_t)bk;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t tile = idx / tile_words, within = idx % tile_words;
-    const size_t g = (tile / Kt) * 128 + within / bk;
-    const size_t l = (tile % Kt) * bk + within % bk;
+  const unsigned kt = blockIdx.x % Kt, tg = blockIdx.x / Kt;
+  double* out = ao_t + (size_t)blockIdx.x * (128 * BK);
+  for (unsigned idx = threadIdx.x; idx < 128 * BK; idx += 256) {
+    const unsigned r = idx / BK, c = idx % BK;
+    const size_t g = (size_t)tg * 128 + r, l = (size_t)kt * BK + c;
     uint64_t w = 0;
     if (g < G && l < k) {
       const size_t base = g * e;
       const int len = (int)((m - base) < (size_t)e ? (m - base) : (size_t)e);
       for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(a[(base + s) * lda + l]);
     }
-    ao_t[idx] = __ull2double_rn(w);
+    out[idx] = __ull2double_rn(w);
   }
 }
 
@@ -269,25 +269,19 @@ __global__ void __launch_bounds__(256) k_pack_outer_rows_tiled(const TIn* __rest
 // (g qs + i, h ts + j) is base-Q digit i + j qs of word (g, h). One thread per
 // (output row, word column): it reads the word once and writes its ts
 // consecutive cells, so a warp's stores cover one contiguous row segment.
-// 32-bit index arithmetic only (rows and words per row < 2^31).
-__global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, unsigned m, unsigned n, int t, int e,
-                                  int qs, int ts, uint32_t p, int32_t* __restrict__ c, size_t ldc,
-                                  int* __restrict__ overflow) {
-  const double limit = (double)(1ull << (t * e));
+// 32-bit index arithmetic only (rows and words per row < 2^31). Like the
+// reference (which masks, gemm.hpp:436-441) there is no range check, so the
+// call stays asynchronous.
+__global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, unsigned m, unsigned n, int t,
+                                  int qs, int ts, uint32_t p, uint32_t magic, int32_t* __restrict__ c, size_t ldc) {
   const uint64_t mask = (1ull << t) - 1;
   const unsigned H = (n + ts - 1) / ts;
-  const uint32_t magic = (uint32_t)(0x100000000ull / p);
   for (unsigned row = blockIdx.y; row < m; row += gridDim.y) {
     const unsigned g = row / qs, i = row - g * qs;
     const double* wrow = cc + (size_t)g * ldcc;
     int32_t* crow = c + (size_t)row * ldc;
     for (unsigned h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
-      const double v = wrow[h];
-      if (!(v >= 0.0) || !(v < limit)) {
-        atomicExch(overflow, 1);
-        continue;
-      }
-      const uint64_t bits = __double2ull_rz(v) >> (t * i);
+      const uint64_t bits = __double2ull_rz(wrow[h]) >> (t * i);
       const unsigned col0 = h * ts;
       for (int j = 0; j < ts && col0 + j < n; ++j) {
         const uint64_t x64 = (bits >> (t * j * qs)) & mask;
@@ -513,35 +507,49 @@ cudaError_t launch_pack_outer_tiled(const void* src, int dtype, size_t k, size_t
   }
 }
 
-template <typename TIn>
-static cudaError_t pack_outer_rows_tiled_t(const TIn* src, size_t m, size_t k, size_t ld, int t, int e, int bk,
-                                           double* dst, cudaStream_t s) {
+template <typename TIn, int BK>
+static cudaError_t pack_outer_rows_tiled_t(const TIn* src, size_t m, size_t k, size_t ld, int t, int e, double* dst,
+                                           cudaStream_t s) {
   const size_t G = (m + e - 1) / e;
-  const unsigned Kt = (unsigned)((k + bk - 1) / bk);
-  const size_t total = (G + 127) / 128 * Kt * 128 * (size_t)bk;
-  if (total == 0) return cudaSuccess;
-  k_pack_outer_rows_tiled<TIn><<<grid1d(total, 256), 256, 0, s>>>(src, m, k, ld, t, e, bk, Kt, total, dst);
+  const unsigned Kt = (unsigned)((k + BK - 1) / BK);
+  const size_t blocks = (G + 127) / 128 * Kt;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks >= (1ull << 31)) return cudaErrorInvalidValue;
+  k_pack_outer_rows_tiled<TIn, BK><<<(unsigned)blocks, 256, 0, s>>>(src, m, k, ld, t, e, Kt, dst);
   count_launch();
   return cudaGetLastError();
 }
 
+template <typename TIn>
+static cudaError_t pack_outer_rows_tiled_dt(const TIn* src, size_t m, size_t k, size_t ld, int t, int e, int bk,
+                                            double* dst, cudaStream_t s) {
+  switch (bk) {
+    case 36: return pack_outer_rows_tiled_t<TIn, 36>(src, m, k, ld, t, e, dst, s);
+    case 28: return pack_outer_rows_tiled_t<TIn, 28>(src, m, k, ld, t, e, dst, s);
+    case 20: return pack_outer_rows_tiled_t<TIn, 20>(src, m, k, ld, t, e, dst, s);
+    case 12: return pack_outer_rows_tiled_t<TIn, 12>(src, m, k, ld, t, e, dst, s);
+    case 4: return pack_outer_rows_tiled_t<TIn, 4>(src, m, k, ld, t, e, dst, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_pack_outer_rows_tiled(const void* src, int dtype, size_t m, size_t k, size_t ld, int t, int e,
                                          int bk, double* dst, cudaStream_t s) {
-  if (bk < 1) return cudaErrorInvalidValue;
   switch (dtype) {
-    case 0: return pack_outer_rows_tiled_t<double>((const double*)src, m, k, ld, t, e, bk, dst, s);
-    case 1: return pack_outer_rows_tiled_t<uint32_t>((const uint32_t*)src, m, k, ld, t, e, bk, dst, s);
-    default: return pack_outer_rows_tiled_t<int32_t>((const int32_t*)src, m, k, ld, t, e, bk, dst, s);
+    case 0: return pack_outer_rows_tiled_dt<double>((const double*)src, m, k, ld, t, e, bk, dst, s);
+    case 1: return pack_outer_rows_tiled_dt<uint32_t>((const uint32_t*)src, m, k, ld, t, e, bk, dst, s);
+    default: return pack_outer_rows_tiled_dt<int32_t>((const int32_t*)src, m, k, ld, t, e, bk, dst, s);
   }
 }
 
-cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size_t n, int t, int e, int qs, int ts,
-                                   uint32_t p, int32_t* c, size_t ldc, int* overflow, cudaStream_t s) {
+cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size_t n, int t, int qs, int ts,
+                                   uint32_t p, int32_t* c, size_t ldc, cudaStream_t s) {
   if (m * n == 0) return cudaSuccess;
   if (m >= (1u << 31) || n >= (1u << 31)) return cudaErrorInvalidValue;
   const unsigned H = (unsigned)((n + ts - 1) / ts);
   const dim3 grid((H + 127) / 128, (unsigned)(m < 65535 ? m : 65535));
-  k_uncompress_full<<<grid, 128, 0, s>>>(cc, ldcc, (unsigned)m, (unsigned)n, t, e, qs, ts, p, c, ldc, overflow);
+  k_uncompress_full<<<grid, 128, 0, s>>>(cc, ldcc, (unsigned)m, (unsigned)n, t, qs, ts, p,
+                                         (uint32_t)(0x100000000ull / p), c, ldc);
   count_launch();
   return cudaGetLastError();
 }

@@ -88,6 +88,8 @@ typedef struct {
   int32_t axis;
   int32_t slots;
 } qg_orientation;
+enum { QG_FORWARD = 0, QG_REVERSED = 1 };
+enum { QG_ROW = 0, QG_COLUMN = 1 };
 
 /* Element type of residue buffers. */
 typedef enum { QG_F64 = 0, QG_U32 = 1, QG_I32 = 2 } qg_dtype;
@@ -292,7 +294,37 @@ int qg_host_mul_left_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint
 int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32_t* a, const uint32_t* b,
                      size_t m, size_t k, size_t n, uint32_t* c);
 
+/* naive_gemm, gemm.hpp:80-100: C = A B mod p with 64-bit sums, no packing.
+ * The independent device checker of the CLI's verify / --algo naive. */
+int qg_naive_gemm(uint32_t p, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, int32_t* c,
+                  size_t ldc, void* stream);
+int qg_host_naive_gemm(uint32_t p, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                       uint32_t* c);
+/* uncompress (gemm.hpp:182-204) of HOST words into HOST residues. */
+int qg_host_uncompress(const qg_plan* plan, qg_orientation o, const double* words, size_t stored_rows,
+                       size_t stored_cols, size_t logical_rows, size_t logical_cols, uint32_t* out);
+/* random_residue_matrix(rows, cols, PrimeModulus(p), seed), prng.hpp:31-38,
+ * generated on the device and copied to HOST memory. */
+int qg_host_random_residue_matrix(size_t rows, size_t cols, uint32_t p, uint64_t seed, uint32_t* out);
+/* PhaseSeconds of the last host-data call on this thread (gemm.hpp
+ * PhaseSeconds, reported by bench.hpp:67-152): multiply = device time of the
+ * contraction kernels, convert = the rest of the call (transfers, packing,
+ * extraction). */
+void qg_last_phase_seconds(double* multiply, double* convert);
+
+/* ----------------------------------------------- matrix files (matrix_io.hpp)
+ * "M <p> <rows> <cols>" then rows*cols whitespace-separated residues in
+ * [0, p-1], row-major (matrix_io.hpp:14-22). Readers return QG_PARSE_ERROR
+ * with the reference's message (qg_last_error()); *data is malloc'd, release
+ * it with qg_free. */
+int qg_parse_matrix(const char* text, size_t len, uint32_t* p, size_t* rows, size_t* cols, uint32_t** data);
+int qg_read_matrix_file(const char* path, uint32_t* p, size_t* rows, size_t* cols, uint32_t** data);
+int qg_write_matrix_file(const char* path, uint32_t p, const uint32_t* data, size_t rows, size_t cols);
+void qg_free(void* ptr);
+
 /* ------------------------------------------------------------ diagnostics */
+/* qg_last_error(): description of the last failure on this thread (CUDA
+ * error string, or the parse error text of a matrix file). */
 /* Number of kernels this library launched since load (the bench's
  * gpu_launches evidence). */
 uint64_t qg_kernel_launches(void);

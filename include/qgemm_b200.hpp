@@ -14,7 +14,9 @@
 // reference file:line).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -130,6 +132,7 @@ struct ResidueMatrix {
 // of packed_right_product / mul_right_compressed, m x ceil(n/e), matrix.hpp:44-63).
 struct CompressedWords {
   std::size_t logical_rows = 0, logical_cols = 0, stored_rows = 0, stored_cols = 0;
+  qg_orientation orientation{QG_FORWARD, QG_COLUMN, 1};  // PackOrientation, matrix.hpp:33-39
   CompressionPlan plan;
   std::vector<double> data;
 };
@@ -182,11 +185,176 @@ inline CompressedWords mul_right_compressed(const ResidueMatrix& a, const Residu
   cc.logical_rows = cc.stored_rows = a.rows;
   cc.logical_cols = b.cols;
   cc.stored_cols = (b.cols + plan.e() - 1) / plan.e();
+  cc.orientation = qg_orientation{QG_FORWARD, QG_COLUMN, plan.e()};
   cc.plan = plan;
   cc.data.resize(cc.stored_rows * cc.stored_cols);
   check(qg_host_mul_right(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, cc.data.data()),
         "mul_right_compressed");
   return cc;
+}
+
+// mul_left_compressed(compress_outer_rows(A, plan), B), gemm.hpp:340-371:
+// ceil(m/e) x n post-REDQ words, {Forward, Row, e}.
+inline CompressedWords mul_left_compressed(const ResidueMatrix& a, const ResidueMatrix& b,
+                                           const CompressionPlan& plan) {
+  detail::check_inner_dims(a, b);
+  CompressedWords cc;
+  cc.logical_rows = a.rows;
+  cc.logical_cols = cc.stored_cols = b.cols;
+  cc.stored_rows = (a.rows + plan.e() - 1) / plan.e();
+  cc.orientation = qg_orientation{QG_FORWARD, QG_ROW, plan.e()};
+  cc.plan = plan;
+  cc.data.resize(cc.stored_rows * cc.stored_cols);
+  check(qg_host_mul_left(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, cc.data.data()),
+        "mul_left_compressed");
+  return cc;
+}
+
+// uncompress, gemm.hpp:182-204 (on the device).
+inline ResidueMatrix uncompress(const CompressedWords& cm) {
+  ResidueMatrix c(cm.logical_rows, cm.logical_cols);
+  check(qg_host_uncompress(&cm.plan.c, cm.orientation, cm.data.data(), cm.stored_rows, cm.stored_cols,
+                           cm.logical_rows, cm.logical_cols, c.data.data()),
+        "uncompress");
+  return c;
+}
+
+// FullPlan, plan.hpp:44-57, and plan_full, plan.hpp:229-252.
+struct FullPlan {
+  qg_full_plan c{};
+  CompressionPlan base() const { return CompressionPlan{c.base}; }
+  int dq() const { return c.dq; }
+  int dtheta() const { return c.dtheta; }
+  int theta_exponent() const { return c.theta_exponent; }
+  int q_slots() const { return c.dq + 1; }
+  int theta_slots() const { return c.dtheta + 1; }
+};
+inline FullPlan plan_full(std::uint32_t p, std::uint64_t k, int beta = 53) {
+  FullPlan fp;
+  check(qg_plan_full(p, k, beta, &fp.c), "plan_full");
+  return fp;
+}
+// mul_full_compressed(A, B, fp), gemm.hpp:377-445.
+inline ResidueMatrix mul_full_compressed(const ResidueMatrix& a, const ResidueMatrix& b, const FullPlan& fp) {
+  detail::check_inner_dims(a, b);
+  ResidueMatrix c(a.rows, b.cols);
+  check(qg_host_mul_full(&fp.c, 0, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, c.data.data()),
+        "mul_full_compressed");
+  return c;
+}
+
+// naive_gemm, gemm.hpp:80-100 (a plain device kernel, no packing).
+inline ResidueMatrix naive_gemm(const ResidueMatrix& a, const ResidueMatrix& b, std::uint32_t p) {
+  detail::check_inner_dims(a, b);
+  ResidueMatrix c(a.rows, b.cols);
+  check(qg_host_naive_gemm(p, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, c.data.data()), "naive_gemm");
+  return c;
+}
+
+// PhaseSeconds of the last product call on this thread (see qg_last_phase_seconds).
+struct PhaseSeconds {
+  double multiply = 0;
+  double convert = 0;
+};
+inline PhaseSeconds last_phase_seconds() {
+  PhaseSeconds ph;
+  qg_last_phase_seconds(&ph.multiply, &ph.convert);
+  return ph;
+}
+
+// ------------------------------------------------------------ plan.hpp:59-78
+enum class Algorithm { Naive, CommonCompressed, RightCompressed, LeftCompressed, FullCompressed, Blocked };
+inline const char* algorithm_name(Algorithm a) {
+  switch (a) {
+    case Algorithm::Naive: return "naive";
+    case Algorithm::CommonCompressed: return "common";
+    case Algorithm::RightCompressed: return "right";
+    case Algorithm::LeftCompressed: return "left";
+    case Algorithm::FullCompressed: return "full";
+    case Algorithm::Blocked: return "blocked";
+  }
+  return "?";
+}
+
+// ------------------------------------------------------------ prng.hpp:12-38
+class SplitMix64 {
+ public:
+  explicit SplitMix64(std::uint64_t seed) : state_(seed) {}
+  std::uint64_t next() {
+    std::uint64_t z = (state_ += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  std::uint64_t below(std::uint64_t bound) { return next() % bound; }
+
+ private:
+  std::uint64_t state_;
+};
+// The same seeded matrix as the reference's, generated on the device.
+inline ResidueMatrix random_residue_matrix(std::size_t rows, std::size_t cols, std::uint32_t p, std::uint64_t seed) {
+  ResidueMatrix m(rows, cols);
+  check(qg_host_random_residue_matrix(rows, cols, p, seed, m.data.data()), "random_residue_matrix");
+  return m;
+}
+
+// ------------------------------------------------------------ matrix_io.hpp:14-77
+struct MatrixFile {
+  std::uint32_t p = 0;
+  ResidueMatrix matrix;
+};
+namespace detail {
+inline MatrixFile adopt(int status, const char* where, std::uint32_t p, std::size_t rows, std::size_t cols,
+                        std::uint32_t* data) {
+  if (status != QG_OK) {
+    const std::string msg = qg_last_error();
+    if (status == QG_PARSE_ERROR) throw ParseError(msg);
+    check(status, where);
+  }
+  MatrixFile mf;
+  mf.p = p;
+  mf.matrix = ResidueMatrix(rows, cols);
+  if (rows * cols != 0) std::copy(data, data + rows * cols, mf.matrix.data.begin());
+  qg_free(data);
+  return mf;
+}
+}  // namespace detail
+inline MatrixFile read_matrix_text(const std::string& text) {
+  std::uint32_t p = 0, *data = nullptr;
+  std::size_t rows = 0, cols = 0;
+  const int st = qg_parse_matrix(text.data(), text.size(), &p, &rows, &cols, &data);
+  return detail::adopt(st, "read_matrix", p, rows, cols, data);
+}
+inline MatrixFile read_matrix_file(const std::string& path) {
+  std::uint32_t p = 0, *data = nullptr;
+  std::size_t rows = 0, cols = 0;
+  const int st = qg_read_matrix_file(path.c_str(), &p, &rows, &cols, &data);
+  return detail::adopt(st, "read_matrix_file", p, rows, cols, data);
+}
+inline void write_matrix_file(const std::string& path, const ResidueMatrix& m, std::uint32_t p) {
+  const int st = qg_write_matrix_file(path.c_str(), p, m.data.data(), m.rows, m.cols);
+  if (st == QG_PARSE_ERROR) throw ParseError(qg_last_error());
+  check(st, "write_matrix_file");
+}
+
+// ------------------------------------------------------------ bench.hpp:19-41
+struct TimingRecord {
+  std::string algorithm;
+  std::uint32_t p = 0;
+  std::size_t m = 0, k = 0, n = 0;
+  int t = 0;
+  int e = 1;
+  double seconds_multiply = 0;
+  double seconds_convert = 0;
+  std::uint32_t checksum = 0;
+};
+inline const char* timing_csv_header() { return "algorithm,p,m,k,n,t,e,seconds_multiply,seconds_convert,checksum"; }
+inline std::string to_csv_row(const TimingRecord& r) {
+  char buf[64];
+  std::string s = r.algorithm + ',' + std::to_string(r.p) + ',' + std::to_string(r.m) + ',' + std::to_string(r.k) +
+                  ',' + std::to_string(r.n) + ',' + std::to_string(r.t) + ',' + std::to_string(r.e) + ',';
+  std::snprintf(buf, sizeof buf, "%.6f,%.6f,", r.seconds_multiply, r.seconds_convert);
+  return s + buf + std::to_string(r.checksum);
 }
 
 // residue_checksum, bench.hpp:43-47.

@@ -135,6 +135,8 @@ def _load_ref():
         "qgref_mul_right": ([P(Plan), vp, vp, sz, sz, sz, vp, vp, i32, dp, dp], i32),
         "qgref_blocked_accumulate": ([P(Plan), vp, vp, sz, sz, sz, sz, vp], i32),
         "qgref_plan_full": ([u32, u64, i32, P(FullPlan)], i32),
+        "qgref_parse_matrix": ([ctypes.c_char_p, sz, P(u32), P(sz), P(sz), vp, sz, ctypes.c_char_p, sz], i32),
+        "qgref_write_matrix": ([vp, sz, sz, u32, ctypes.c_char_p, sz], sz),
         "qgref_mul_left": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
         "qgref_mul_full": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
         "qgref_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp], i32),

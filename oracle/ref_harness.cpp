@@ -10,6 +10,7 @@
 // threads exactly as SURVEY.md §6 did (each thread runs the unmodified
 // routines on its row shard; CB is packed once).
 #include <chrono>
+#include <sstream>
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -289,6 +290,31 @@ int qgref_mul_full(const qgo_full_plan* fp, const uint32_t* a, const uint32_t* b
     const auto r = mul_full_compressed<DoubleWord>(wrap(a, m, k), wrap(b, k, n), f);
     std::memcpy(c, r.data.data(), r.data.size() * sizeof(uint32_t));
   });
+}
+
+// read_matrix / write_matrix, matrix_io.hpp:27-75 (to pin the file format).
+int qgref_parse_matrix(const char* text, size_t len, uint32_t* p, size_t* rows, size_t* cols, uint32_t* data,
+                       size_t cap, char* msg, size_t msglen) {
+  try {
+    std::istringstream in(std::string(text, len));
+    const MatrixFile mf = read_matrix(in);
+    *p = mf.p;
+    *rows = mf.matrix.rows;
+    *cols = mf.matrix.cols;
+    for (size_t i = 0; i < mf.matrix.data.size() && i < cap; ++i) data[i] = mf.matrix.data[i];
+    return QGO_OK;
+  } catch (const std::exception& ex) {
+    std::snprintf(msg, msglen, "%s", ex.what());
+    return status_of(ex);
+  }
+}
+
+size_t qgref_write_matrix(const uint32_t* data, size_t rows, size_t cols, uint32_t p, char* out, size_t cap) {
+  std::ostringstream os;
+  write_matrix(os, wrap(data, rows, cols), p);
+  const std::string s = os.str();
+  if (s.size() <= cap) std::memcpy(out, s.data(), s.size());
+  return s.size();
 }
 
 int qgref_blocked_accumulate(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,

@@ -195,6 +195,15 @@ def _load():
         "qg_host_mul_left_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_mul_right_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_mul_full": ([P(_FullPlan), u64, vp, vp, sz, sz, sz, vp], i32),
+        "qg_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_host_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_uncompress": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp], i32),
+        "qg_host_random_residue_matrix": ([sz, sz, u32, u64, vp], i32),
+        "qg_last_phase_seconds": ([P(ctypes.c_double), P(ctypes.c_double)], None),
+        "qg_parse_matrix": ([ctypes.c_char_p, sz, P(u32), P(sz), P(sz), P(P(u32))], i32),
+        "qg_read_matrix_file": ([ctypes.c_char_p, P(u32), P(sz), P(sz), P(P(u32))], i32),
+        "qg_write_matrix_file": ([ctypes.c_char_p, u32, vp, sz, sz], i32),
+        "qg_free": ([vp], None),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),
@@ -931,3 +940,44 @@ def mul_full_compressed_host(a, b, fp: FullPlan, kblock_words: int = 0, out=None
     _check(lib.qg_host_mul_full(ctypes.byref(f), kblock_words, a.ctypes.data_as(ctypes.c_void_p),
                                 b.ctypes.data_as(ctypes.c_void_p), m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
     return c
+
+
+# ----------------------------------------------------------------- matrix files
+def _check_parse(status: int) -> None:
+    if status == 8:  # ParseError carries the reference's message (matrix_io.hpp:27-62)
+        raise ParseError(lib.qg_last_error().decode())
+    _check(status)
+
+
+def _adopt(p, rows, cols, data):
+    n = rows.value * cols.value
+    out = np.ctypeslib.as_array(data, shape=(max(n, 1),))[:n].copy().reshape(rows.value, cols.value)
+    lib.qg_free(ctypes.cast(data, ctypes.c_void_p))
+    return p.value, out
+
+
+def parse_matrix(text: str):
+    """read_matrix, matrix_io.hpp:27-52: (p, uint32 rows x cols array)."""
+    raw = text.encode()
+    p, rows, cols, data = ctypes.c_uint32(), ctypes.c_size_t(), ctypes.c_size_t(), ctypes.POINTER(ctypes.c_uint32)()
+    _check_parse(lib.qg_parse_matrix(raw, len(raw), ctypes.byref(p), ctypes.byref(rows), ctypes.byref(cols),
+                                     ctypes.byref(data)))
+    return _adopt(p, rows, cols, data)
+
+
+def read_matrix_file(path: str):
+    """read_matrix_file, matrix_io.hpp:54-62: (p, uint32 array)."""
+    p, rows, cols, data = ctypes.c_uint32(), ctypes.c_size_t(), ctypes.c_size_t(), ctypes.POINTER(ctypes.c_uint32)()
+    _check_parse(lib.qg_read_matrix_file(os.fsencode(path), ctypes.byref(p), ctypes.byref(rows), ctypes.byref(cols),
+                                         ctypes.byref(data)))
+    return _adopt(p, rows, cols, data)
+
+
+def write_matrix_file(path: str, m, p: int) -> None:
+    """write_matrix_file, matrix_io.hpp:64-75."""
+    m = _host_u32(m)
+    rows, cols = m.shape
+    _check_parse(lib.qg_write_matrix_file(os.fsencode(path), p, m.ctypes.data_as(ctypes.c_void_p), rows, cols))
+
+
+CLI_PATH = os.path.join(_HERE, "_lib", "qgemm_b200")

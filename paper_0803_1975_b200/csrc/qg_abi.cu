@@ -3,12 +3,14 @@
 // Every computation is a kernel launch on the caller's stream; nothing here
 // computes results on the CPU.
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
 
 #include "../../include/qgemm_b200.h"
+#include "qg_internal.h"
 #include "qg_kernels.h"
 
 namespace qg {
@@ -33,6 +35,7 @@ thread_local cudaError_t g_last_cuda_error = cudaSuccess;
 int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return QG_OK;
   g_last_cuda_error = e;
+  qg::last_message() = cudaGetErrorString(e);
   return QG_CUDA_ERROR;
 }
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -412,7 +415,10 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
 
 
 uint64_t qg_kernel_launches(void) { return qgk::g_launches.load(); }
-const char* qg_last_error(void) { return cudaGetErrorString(g_last_cuda_error); }
+const char* qg_last_error(void) {
+  const std::string& m = qg::last_message();
+  return m.empty() ? cudaGetErrorString(g_last_cuda_error) : m.c_str();
+}
 const char* qg_last_kernel(void) { return g_last_kernel; }
 
 int qg_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols, void* dst,
@@ -618,6 +624,47 @@ struct DevBuf {
     if (p) cudaFreeAsync(p, s);
   }
 };
+
+// Phase split of the last host-data call, the reference's PhaseSeconds
+// (gemm.hpp, bench.hpp:67-152): multiply = device time of the contraction
+// kernels (event pairs on the stream they run on), convert = the rest of the
+// call's wall time (transfers, packing, extraction, reduction).
+struct PhaseLog {
+  double multiply = 0, convert = 0;
+};
+thread_local PhaseLog g_phase;
+
+struct PhaseScope {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  cudaEvent_t ev[2 * 64] = {};
+  int n = 0;
+  void begin(cudaStream_t s) {
+    if (n + 2 > 2 * 64) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventCreate(&ev[n + 1]);
+    cudaEventRecord(ev[n], s);
+  }
+  void end(cudaStream_t s) {
+    if (n + 2 > 2 * 64) return;
+    cudaEventRecord(ev[n + 1], s);
+    n += 2;
+  }
+  void finish() {  // after the call's final synchronize
+    double mul = 0;
+    for (int i = 0; i < n; i += 2) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) mul += ms * 1e-3;
+    }
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    g_phase.multiply = mul;
+    g_phase.convert = wall > mul ? wall - mul : 0.0;
+  }
+  ~PhaseScope() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 #define QG_TRY(x)                       \
   do {                                  \
     cudaError_t e_ = (x);               \
@@ -666,6 +713,7 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
   if (tiled && m * n > 0) {
     thread_local HostPipe hp;
     if (!hp.ok) return QG_CUDA_ERROR;
+    PhaseScope ps;
     const size_t chunk = 512;  // rows per pipeline chunk (a multiple of the 128-row tile)
     size_t nchunks = ceil_div(m, chunk);
     const size_t rows_per = nchunks > (size_t)HostPipe::kMaxChunks ? ceil_div(ceil_div(m, HostPipe::kMaxChunks), 128) * 128 : chunk;
@@ -693,9 +741,11 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
       QG_TRY(cudaStreamWaitEvent(hp.comp, hp.a_ready[i], 0));
       QG_TRY(qgk::launch_pack_tiled(false, (const uint32_t*)da.p + r0 * k, QG_U32, rows, k, k, pl.t, pl.e, bk,
                                     ca_chunk, hp.comp, pl.p, gp->balanced != 0));
+      ps.begin(hp.comp);
       if ((st = qg_mul_common_tiled(gp, ca_chunk, (const double*)dcb.p, rows, n, k, (int32_t*)dc.p + r0 * n, n,
                                     hp.comp)))
         return st;
+      ps.end(hp.comp);
       QG_TRY(cudaEventRecord(hp.c_ready[i], hp.comp));
       QG_TRY(cudaStreamWaitEvent(hp.out, hp.c_ready[i], 0));
       QG_TRY(cudaMemcpyAsync(c + r0 * n, (const int32_t*)dc.p + r0 * n, rows * n * 4, cudaMemcpyDeviceToHost, hp.out));
@@ -703,6 +753,7 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
     QG_TRY(cudaEventRecord(hp.done, hp.out));
     QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
     QG_TRY(cudaStreamSynchronize(hp.out));
+    ps.finish();
     return QG_OK;
   }
   if (gp->balanced) {  // the row-layout kernels need unsigned words: re-plan
@@ -711,6 +762,7 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
     return host_common(&up, a, b, m, k, n, c);
   }
   cudaStream_t s = nullptr;
+  PhaseScope ps;
   DevBuf da(s), db(s), dca(s), dcb(s), dc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
@@ -722,10 +774,13 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
   QG_TRY(dcb.alloc(K * n * 8));
   QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e, (double*)dca.p, K, 0, 0, s));
   QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e, (double*)dcb.p, n, 0, 0, s));
+  ps.begin(s);
   if ((st = qg_mul_common(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (int32_t*)dc.p, n, s)))
     return st;
+  ps.end(s);
   if (m * n) QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
   return QG_OK;
 }
 
@@ -755,6 +810,7 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
   if (kpanel > plan->kmax) return QG_PLAN_MISMATCH;       // gemm.hpp:456
   cudaStream_t s = nullptr;
   if (m * n == 0) return QG_OK;
+  PhaseScope ps;
   // Each panel is packed on its own (gemm.hpp:471-478) into words padded to a
   // whole number of 4-word k-steps, so k-blocks never straddle two panels.
   const size_t pw = ceil_div(kpanel, plan->e);
@@ -784,6 +840,7 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
                             (double*)dca.p, W, kpanel, pw4, s));
     QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, plan->t, plan->e,
                             (double*)dcb.p, n, kpanel, pw4, s));
+    ps.begin(s);
     if (kb) {
       if ((st = run_common(*plan, kb, (const double*)dca.p, W, (const double*)dcb.p, n, m, n, W,
                            (int32_t*)dc.p, n, s)))
@@ -806,9 +863,11 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
       h.ldc = n;
       if ((st = cuda_status(qgk::launch_dot_highpart(h, s, &g_last_kernel)))) return st;
     }
+    ps.end(s);
   }
   QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
   return QG_OK;
 }
 
@@ -825,6 +884,7 @@ static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* 
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
+  PhaseScope ps;
   DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
@@ -837,10 +897,13 @@ static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* 
     if ((st = qg_pack_residues_tiled((uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
     if ((st = qg_pack_outer_cols_tiled(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
   }
+  ps.begin(s);
   if ((st = qg_mul_right_tiled(gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, H, s)))
     return st;
+  ps.end(s);
   QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
   return QG_OK;
 }
 
@@ -855,6 +918,7 @@ static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
+  PhaseScope ps;
   DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
@@ -867,10 +931,13 @@ static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b
     if ((st = qg_pack_outer_rows_tiled(plan, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
     if ((st = qg_pack_residues_b_tiled((uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
   }
+  ps.begin(s);
   if ((st = qg_mul_left_tiled(gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, n, s)))
     return st;
+  ps.end(s);
   QG_TRY(cudaMemcpyAsync(cc, dcc.p, G * n * 8, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
   return QG_OK;
 }
 
@@ -935,6 +1002,7 @@ int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32
   pb.t = fp->theta_exponent;
   pb.e = ts;
   pb.d = ts - 1;
+  PhaseScope ps;
   DevBuf da(s), db(s), dat(s), dbt(s), dcc(s), dc(s);
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
@@ -951,13 +1019,83 @@ int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32
     if ((st = cuda_status(qgk::launch_pack_outer_tiled(db.p, QG_U32, k, n, n, pb.t, pb.e, bk, (double*)dbt.p, s))))
       return st;
   }
+  ps.begin(s);
   if ((st = qg_mul_full_tiled(fp, gp.kblock_words, (const double*)dat.p, (const double*)dbt.p, m, k, n,
                               (double*)dcc.p, H, s)))
     return st;
+  ps.end(s);
   if ((st = qg_uncompress_full(fp, (const double*)dcc.p, H, m, n, (int32_t*)dc.p, n, s))) return st;
   QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
   QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
   return QG_OK;
+}
+
+
+// naive_gemm, gemm.hpp:80-100, on the device.
+int qg_naive_gemm(uint32_t p, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, int32_t* c,
+                  size_t ldc, void* stream) {
+  if (p < 2 || !qg::is_prime(p)) return QG_INVALID_MODULUS;
+  if (ldc < n) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_naive_gemm(a, b, m, k, n, p, c, ldc, as_stream(stream)));
+}
+
+int qg_host_naive_gemm(uint32_t p, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                       uint32_t* c) {
+  if (p < 2 || !qg::is_prime(p)) return QG_INVALID_MODULUS;
+  if (m * n == 0) return QG_OK;
+  cudaStream_t s = nullptr;
+  PhaseScope ps;
+  DevBuf da(s), db(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  ps.begin(s);
+  int st = qg_naive_gemm(p, (const uint32_t*)da.p, (const uint32_t*)db.p, m, k, n, (int32_t*)dc.p, n, s);
+  if (st) return st;
+  ps.end(s);
+  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
+  return QG_OK;
+}
+
+int qg_host_uncompress(const qg_plan* plan, qg_orientation o, const double* words, size_t stored_rows,
+                       size_t stored_cols, size_t logical_rows, size_t logical_cols, uint32_t* out) {
+  int st = check_plan(plan);
+  if (st) return st;
+  cudaStream_t s = nullptr;
+  DevBuf dw(s), dout(s);
+  QG_TRY(dw.alloc(stored_rows * stored_cols * 8));
+  QG_TRY(dout.alloc(logical_rows * logical_cols * 4));
+  if (stored_rows * stored_cols)
+    QG_TRY(cudaMemcpyAsync(dw.p, words, stored_rows * stored_cols * 8, cudaMemcpyHostToDevice, s));
+  if ((st = qg_uncompress(plan, o, (const double*)dw.p, stored_rows, stored_cols, logical_rows, logical_cols,
+                          (int32_t*)dout.p, s)))
+    return st;
+  if (logical_rows * logical_cols)
+    QG_TRY(cudaMemcpyAsync(out, dout.p, logical_rows * logical_cols * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+int qg_host_random_residue_matrix(size_t rows, size_t cols, uint32_t p, uint64_t seed, uint32_t* out) {
+  if (rows * cols == 0) return (p < 2 || !qg::is_prime(p)) ? QG_INVALID_MODULUS : QG_OK;
+  cudaStream_t s = nullptr;
+  DevBuf d(s);
+  QG_TRY(d.alloc(rows * cols * 4));
+  int st = qg_gen_residues(seed, p, 0, rows, cols, d.p, QG_U32, s);
+  if (st) return st;
+  QG_TRY(cudaMemcpyAsync(out, d.p, rows * cols * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+void qg_last_phase_seconds(double* multiply, double* convert) {
+  if (multiply) *multiply = g_phase.multiply;
+  if (convert) *convert = g_phase.convert;
 }
 
 }  // extern "C"

@@ -299,6 +299,48 @@ __global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, un
   }
 }
 
+// naive_gemm, gemm.hpp:80-100, on the device: the independent checker behind
+// the CLI's verify and --algo naive. 16 x 16 output tiles, 64-bit sums of
+// products reduced mod p every `spill` products so they never wrap.
+__global__ void __launch_bounds__(256) k_naive_gemm(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                                    unsigned m, unsigned k, unsigned n, uint32_t p, unsigned spill,
+                                                    int32_t* __restrict__ c, size_t ldc) {
+  __shared__ uint32_t sa[16][17], sb[16][17];
+  const unsigned tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const unsigned row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  uint64_t acc = 0;
+  unsigned cnt = 0;
+  for (unsigned k0 = 0; k0 < k; k0 += 16) {
+    sa[ty][tx] = (row < m && k0 + tx < k) ? a[(size_t)row * k + k0 + tx] : 0u;
+    sb[ty][tx] = (k0 + ty < k && col < n) ? b[(size_t)(k0 + ty) * n + col] : 0u;
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      acc += (uint64_t)sa[ty][l] * sb[l][tx];
+      if (++cnt == spill) {
+        acc %= p;
+        cnt = 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (row < m && col < n) c[(size_t)row * ldc + col] = (int32_t)(acc % p);
+}
+
+cudaError_t launch_naive_gemm(const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, uint32_t p,
+                              int32_t* c, size_t ldc, cudaStream_t s) {
+  if (m * n == 0) return cudaSuccess;
+  if (m > 0xFFFF0ull || n >= (1ull << 31) || k >= (1ull << 32)) return cudaErrorInvalidValue;
+  const unsigned __int128 pm = (unsigned __int128)(p - 1) * (p - 1);
+  unsigned __int128 room = ((unsigned __int128)1 << 64) - 1 - (p - 1);
+  unsigned __int128 sp = pm ? room / pm : ((unsigned __int128)1 << 31);
+  const unsigned spill = sp > (1u << 31) ? (1u << 31) : (unsigned)sp;
+  const dim3 grid((unsigned)((n + 15) / 16), (unsigned)((m + 15) / 16));
+  k_naive_gemm<<<grid, 256, 0, s>>>(a, b, (unsigned)m, (unsigned)k, (unsigned)n, p, spill ? spill : 1, c, ldc);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // redq over a buffer, pack.hpp:124-137: every base-Q digit replaced by itself
 // mod p. A word outside [0, 2^(t e)) raises the DigitOverflow flag.
 __global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint32_t p,

@@ -4,6 +4,7 @@
 // Built by tests/test_cpp_shim.py; run on a GPU (it calls the CUDA path).
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "qgemm_b200.hpp"
 
@@ -18,8 +19,8 @@ static int failures = 0;
     }                                                              \
   } while (0)
 
-// SplitMix64 stream of prng.hpp:12-38 (the seeded inputs of run_bench).
-static ResidueMatrix random_residue_matrix(std::size_t r, std::size_t c, std::uint32_t p, std::uint64_t seed) {
+// SplitMix64 stream of prng.hpp:12-38 (the seeded inputs of run_bench), on the host.
+static ResidueMatrix host_random_matrix(std::size_t r, std::size_t c, std::uint32_t p, std::uint64_t seed) {
   ResidueMatrix m(r, c);
   std::uint64_t s = seed;
   for (auto& v : m.data) {
@@ -31,7 +32,7 @@ static ResidueMatrix random_residue_matrix(std::size_t r, std::size_t c, std::ui
   return m;
 }
 
-static ResidueMatrix naive(const ResidueMatrix& a, const ResidueMatrix& b, std::uint32_t p) {
+static ResidueMatrix host_naive(const ResidueMatrix& a, const ResidueMatrix& b, std::uint32_t p) {
   ResidueMatrix c(a.rows, b.cols);
   for (std::size_t i = 0; i < a.rows; ++i)
     for (std::size_t j = 0; j < b.cols; ++j) {
@@ -59,8 +60,9 @@ int main() {
   CHECK(blocked_accumulate(kA, kB, p5, 1) == kC);
 
   // README.md:97-99: p=3, 512^3, seed 42 -> checksum 262622
-  const auto a = random_residue_matrix(512, 512, 3, 42);
-  const auto b = random_residue_matrix(512, 512, 3, 43);
+  const auto a = host_random_matrix(512, 512, 3, 42);
+  const auto b = host_random_matrix(512, 512, 3, 43);
+  CHECK(random_residue_matrix(512, 512, 3, 42) == a);  // the device generator, same stream
   const auto plan = plan_compression(3, 512);
   CHECK(plan.t() == 12 && plan.e() == 4);
   const auto c = mul_common_compressed(a, b, plan);
@@ -68,9 +70,9 @@ int main() {
   CHECK(mul_common_compressed(a, b, plan_gpu(3, 512)) == c);
 
   // panel blocking (test_gemm.cpp:503-523): k twice past kmax
-  const auto a14 = random_residue_matrix(3, 14, 3, 31);
-  const auto b14 = random_residue_matrix(14, 5, 3, 32);
-  CHECK(blocked_accumulate(a14, b14, p5, 7) == naive(a14, b14, 3));
+  const auto a14 = host_random_matrix(3, 14, 3, 31);
+  const auto b14 = host_random_matrix(14, 5, 3, 32);
+  CHECK(blocked_accumulate(a14, b14, p5, 7) == host_naive(a14, b14, 3));
   bool threw = false;
   try {
     blocked_accumulate(a14, b14, p5, 8);
@@ -80,14 +82,59 @@ int main() {
   CHECK(threw);
 
   // k beyond any single plan: the GPU planner blocks it (p=7, k=4096)
-  const auto a7 = random_residue_matrix(64, 4096, 7, 5);
-  const auto b7 = random_residue_matrix(4096, 48, 7, 6);
-  CHECK(mul_common_compressed(a7, b7, plan_gpu(7, 4096)) == naive(a7, b7, 7));
+  const auto a7 = host_random_matrix(64, 4096, 7, 5);
+  const auto b7 = host_random_matrix(4096, 48, 7, 6);
+  CHECK(mul_common_compressed(a7, b7, plan_gpu(7, 4096)) == host_naive(a7, b7, 7));
 
   // right compression (test_gemm.cpp:417-443): CB = [[2],[33]], C = kC
   const auto cc = mul_right_compressed(kA, kB, p5);
   // C = kC: row 0 digits (1, 2) -> 1 + 2*32 = 65; row 1 digits (1, 1) -> 33
   CHECK(cc.stored_cols == 1 && cc.data[0] == 65.0 && cc.data[1] == 33.0);
+
+  CHECK(uncompress(cc) == kC);
+
+  // left compression (test_gemm.cpp:177-199): CC digits [1,1] and [2,1]
+  const auto cl = mul_left_compressed(kA, kB, p5);
+  CHECK(cl.stored_rows == 1 && cl.data[0] == 33.0 && cl.data[1] == 34.0);
+  CHECK(uncompress(cl) == kC);
+  CHECK(uncompress(mul_left_compressed(kA, from_rows(2, 2, {1, 0, 0, 1}), p5)) == kA);
+
+  // full compression (test_gemm.cpp:201-214): dq = dtheta = 1, Q = 32, Theta = 2^10
+  FullPlan fp;
+  fp.c.base = {3, 5, 3, 4, 53, 7, 1.0 / 32768, 0};
+  fp.c.dq = fp.c.dtheta = 1;
+  fp.c.theta_exponent = 10;
+  CHECK(mul_full_compressed(kA, kB, fp) == kC);
+  CHECK(mul_full_compressed(ResidueMatrix(2, 2), kB, fp) == ResidueMatrix(2, 2));
+  const auto f250 = plan_full(3, 250);  // test_plan.cpp:96-104
+  CHECK(f250.base().t() == 10 && f250.q_slots() == 2 && f250.theta_slots() == 2 && f250.theta_exponent() == 20);
+  CHECK(mul_full_compressed(a14, b14, plan_full(3, 14)) == host_naive(a14, b14, 3));
+
+  // naive_gemm on the device
+  CHECK(naive_gemm(kA, kB, 3) == kC);
+  CHECK(naive_gemm(a7, b7, 7) == host_naive(a7, b7, 7));
+
+  // matrix files (test_io.cpp:11-37) and timing CSV rows (test_io.cpp:44-55)
+  const std::string path = "/tmp/qgemm_b200_shim.mtx";
+  write_matrix_file(path, a14, 3);
+  const MatrixFile mf = read_matrix_file(path);
+  CHECK(mf.p == 3 && mf.matrix == a14);
+  threw = false;
+  try {
+    read_matrix_text("M 3 1 2\n0 3\n");
+  } catch (const ParseError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  CHECK(std::string(timing_csv_header()) == "algorithm,p,m,k,n,t,e,seconds_multiply,seconds_convert,checksum");
+  TimingRecord r;
+  r.algorithm = "common";
+  r.p = 3; r.m = 4; r.k = 5; r.n = 6; r.t = 7; r.e = 2;
+  r.seconds_multiply = 0.25;
+  r.seconds_convert = 0.125;
+  r.checksum = 99;
+  CHECK(to_csv_row(r) == "common,3,4,5,6,7,2,0.250000,0.125000,99");
+  CHECK(std::string(algorithm_name(Algorithm::FullCompressed)) == "full");
 
   // errors: invalid modulus, dimension mismatch
   threw = false;

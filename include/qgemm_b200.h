@@ -294,6 +294,16 @@ int qg_host_mul_left_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint
 int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32_t* a, const uint32_t* b,
                      size_t m, size_t k, size_t n, uint32_t* c);
 
+/* extract_coefficient (DoubleWord), pack.hpp:78-100, elementwise over count
+ * words, in the plan's extraction mode (ReciprocalMul or AddHighBits), bit
+ * for bit the reference's result on any word. out: int32 residues. */
+int qg_extract_coefficients(const qg_plan* plan, const double* words, size_t count, int32_t* out, void* stream);
+/* reduce_and_compress, pack.hpp:141-155, on each of `rows` rows of `cols`
+ * accumulated words (ldw): extract every entry, pack groups of e forward.
+ * out: rows x ceil(cols/e) words (ldo). */
+int qg_reduce_and_compress(const qg_plan* plan, const double* words, size_t rows, size_t cols, size_t ldw,
+                           double* out, size_t ldo, void* stream);
+
 /* naive_gemm, gemm.hpp:80-100: C = A B mod p with 64-bit sums, no packing.
  * The independent device checker of the CLI's verify / --algo naive. */
 int qg_naive_gemm(uint32_t p, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, int32_t* c,

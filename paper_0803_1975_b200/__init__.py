@@ -196,6 +196,8 @@ def _load():
         "qg_host_mul_right_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_mul_full": ([P(_FullPlan), u64, vp, vp, sz, sz, sz, vp], i32),
         "qg_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_extract_coefficients": ([P(_Plan), vp, sz, vp, vp], i32),
+        "qg_reduce_and_compress": ([P(_Plan), vp, sz, sz, sz, vp, sz, vp], i32),
         "qg_host_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp], i32),
         "qg_host_uncompress": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp], i32),
         "qg_host_random_residue_matrix": ([sz, sz, u32, u64, vp], i32),
@@ -839,6 +841,33 @@ def mul_full_compressed(a, b, fp: FullPlan, kblock_words: int = 0):
     c = torch.empty((m, n), dtype=torch.int32, device=a.device)
     _check(lib.qg_uncompress_full(ctypes.byref(f), _ptr(cc), H, m, n, _ptr(c), n, _stream()))
     return c
+
+
+def extract_coefficients(words, plan: CompressionPlan):
+    """extract_coefficient, pack.hpp:78-100, elementwise (float64 CUDA tensor
+    -> int32 residues) in the plan's extraction mode."""
+    torch = _torch()
+    _require_cuda(words)
+    w = words if words.dtype == torch.float64 else words.to(torch.float64)
+    out = torch.empty(w.shape, dtype=torch.int32, device=w.device)
+    pl = plan._c()
+    _check(lib.qg_extract_coefficients(ctypes.byref(pl), _ptr(w), w.numel(), _ptr(out), _stream()))
+    return out
+
+
+def reduce_and_compress(words, plan: CompressionPlan) -> CompressedMatrix:
+    """reduce_and_compress, pack.hpp:141-155, on every row of a 2-D tensor of
+    accumulated words: rows x ceil(cols/e) words, {Forward, Column, e}."""
+    torch = _torch()
+    _require_cuda(words)
+    w = words if words.dtype == torch.float64 else words.to(torch.float64)
+    rows, cols = w.shape
+    groups = (cols + plan.e - 1) // plan.e
+    out = torch.empty((rows, groups), dtype=torch.float64, device=w.device)
+    pl = plan._c()
+    _check(lib.qg_reduce_and_compress(ctypes.byref(pl), _ptr(w), rows, cols, cols, _ptr(out), groups, _stream()))
+    return CompressedMatrix(rows, cols, rows, groups, PackOrientation(PackDirection.Forward, PackAxis.Column, plan.e),
+                            plan, out)
 
 
 def residue_checksum(c) -> int:

@@ -1032,6 +1032,27 @@ int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32
 }
 
 
+// extract_coefficient, pack.hpp:78-100, over a buffer of words (both modes).
+int qg_extract_coefficients(const qg_plan* plan, const double* words, size_t count, int32_t* out, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (plan->extraction != 0 && plan->extraction != 1) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_extract_coefficients(words, count, plan->t, plan->d, plan->e, plan->inv_qd,
+                                                      plan->extraction, plan->p, out, as_stream(stream)));
+}
+
+// reduce_and_compress, pack.hpp:141-155, on every row of a words matrix.
+int qg_reduce_and_compress(const qg_plan* plan, const double* words, size_t rows, size_t cols, size_t ldw,
+                           double* out, size_t ldo, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (plan->extraction != 0 && plan->extraction != 1) return QG_INVALID_ARGUMENT;
+  if (ldw < cols || ldo < ceil_div(cols, (size_t)plan->e)) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_reduce_and_compress(words, rows, cols, ldw, plan->t, plan->d, plan->e,
+                                                     plan->inv_qd, plan->extraction, plan->p, out, ldo,
+                                                     as_stream(stream)));
+}
+
 // naive_gemm, gemm.hpp:80-100, on the device.
 int qg_naive_gemm(uint32_t p, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, int32_t* c,
                   size_t ldc, void* stream) {

@@ -61,6 +61,10 @@ cudaError_t launch_right_tiled(const GemmArgs& a, int bk, bool redq, cudaStream_
 // CBo_t[tn][kt][r][c] = compress_outer_cols(B)[BK kt + c][128 tn + r].
 cudaError_t launch_pack_outer_rows_tiled(const void* src, int dtype, size_t m, size_t k, size_t ld, int t, int e,
                                          int bk, double* dst, cudaStream_t s);
+cudaError_t launch_extract_coefficients(const double* w, size_t count, int t, int d, int e, double inv_qd, int mode,
+                                        uint32_t p, int32_t* out, cudaStream_t s);
+cudaError_t launch_reduce_and_compress(const double* w, size_t rows, size_t cols, size_t ldw, int t, int d, int e,
+                                       double inv_qd, int mode, uint32_t p, double* out, size_t ldo, cudaStream_t s);
 cudaError_t launch_naive_gemm(const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, uint32_t p,
                               int32_t* c, size_t ldc, cudaStream_t s);
 cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size_t n, int t, int qs, int ts,

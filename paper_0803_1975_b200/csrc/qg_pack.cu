@@ -299,6 +299,73 @@ __global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, un
   }
 }
 
+// extract_coefficient (DoubleWord), pack.hpp:78-100, bit for bit on any word:
+// ReciprocalMul truncates w * inv_qd (an exact power-of-two scale) to int64
+// with the reference's x86 conversion (out of range or NaN -> INT64_MIN);
+// AddHighBits adds Q^(2d+1) (round to nearest) and reads the digit from the
+// mantissa at bit 52 - t e (shift count taken mod 64, as x86 does).
+__device__ __forceinline__ uint32_t extract_coefficient_dev(double w, int t, int d, int e, double inv_qd, int mode,
+                                                            uint64_t qmask, uint32_t p) {
+  uint64_t digit;
+  if (mode == 1) {
+    const double anchor = ldexp(1.0, t * (2 * d + 1));
+    const uint64_t mant = (uint64_t)__double_as_longlong(__dadd_rn(w, anchor)) & ((1ull << 52) - 1);
+    digit = (mant >> ((52 - t * e) & 63)) & qmask;
+  } else {
+    const double high = __dmul_rn(w, inv_qd);
+    const long long v = (high >= -9223372036854775808.0 && high < 9223372036854775808.0)
+                            ? __double2ll_rz(high)
+                            : (long long)0x8000000000000000ull;
+    digit = (uint64_t)v & qmask;
+  }
+  return (uint32_t)(digit % p);
+}
+
+__global__ void k_extract_coefficients(const double* __restrict__ w, size_t count, int t, int d, int e,
+                                       double inv_qd, int mode, uint32_t p, int32_t* __restrict__ out) {
+  const uint64_t qmask = t >= 64 ? ~0ull : (1ull << t) - 1;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)extract_coefficient_dev(w[i], t, d, e, inv_qd, mode, qmask, p);
+}
+
+// reduce_and_compress, pack.hpp:141-155, on every row of a words matrix: each
+// group of e consecutive entries is extracted and packed forward into one word
+// (the last group zero-padded). One thread per output word.
+__global__ void k_reduce_and_compress(const double* __restrict__ w, size_t rows, size_t cols, size_t ldw, int t,
+                                      int d, int e, double inv_qd, int mode, uint32_t p, double* __restrict__ out,
+                                      size_t ldo) {
+  const uint64_t qmask = t >= 64 ? ~0ull : (1ull << t) - 1;
+  const size_t groups = (cols + e - 1) / e, count = rows * groups;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / groups, g = i % groups;
+    const size_t c0 = g * e;
+    const int len = (int)((cols - c0) < (size_t)e ? (cols - c0) : (size_t)e);
+    uint64_t word = 0;
+    for (int s = len - 1; s >= 0; --s)
+      word = (word << t) | extract_coefficient_dev(w[r * ldw + c0 + s], t, d, e, inv_qd, mode, qmask, p);
+    out[r * ldo + g] = __ull2double_rn(word);
+  }
+}
+
+static unsigned grid1d(size_t work, int threads);
+
+cudaError_t launch_extract_coefficients(const double* w, size_t count, int t, int d, int e, double inv_qd, int mode,
+                                        uint32_t p, int32_t* out, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  k_extract_coefficients<<<grid1d(count, 256), 256, 0, s>>>(w, count, t, d, e, inv_qd, mode, p, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_and_compress(const double* w, size_t rows, size_t cols, size_t ldw, int t, int d, int e,
+                                       double inv_qd, int mode, uint32_t p, double* out, size_t ldo, cudaStream_t s) {
+  const size_t count = rows * ((cols + e - 1) / e);
+  if (count == 0) return cudaSuccess;
+  k_reduce_and_compress<<<grid1d(count, 256), 256, 0, s>>>(w, rows, cols, ldw, t, d, e, inv_qd, mode, p, out, ldo);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // naive_gemm, gemm.hpp:80-100, on the device: the independent checker behind
 // the CLI's verify and --algo naive. 16 x 16 output tiles, 64-bit sums of
 // products reduced mod p every `spill` products so they never wrap.

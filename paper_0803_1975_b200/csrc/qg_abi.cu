@@ -19,6 +19,7 @@ uint64_t max_exact_block(uint32_t p, int t, int e);
 uint64_t stage_block(uint64_t limit, int* bk);
 uint64_t stage_block_tiled(uint64_t limit, int* bk);
 uint64_t stage_block_redq(uint64_t limit, int* bk);
+int stage_single(uint64_t K);
 uint64_t max_exact_block_balanced(uint32_t p, int t, int e);
 }  // namespace qg
 
@@ -139,9 +140,9 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
   return cuda_status(qgk::launch_dot_highpart(h, s, &g_last_kernel));
 }
 
-// Tiled path: stage depth and blocks for a plan. Single-block plans stream
-// BK = 28 stages (4 in flight); blocked plans use the deepest stage that
-// divides the (Eq. G / Eq. 3) block.
+// Tiled path: stage depth and blocks for a plan. Single-block plans take the
+// stage depth with the least padded work (qg::stage_single); blocked plans use
+// the deepest stage that divides the (Eq. G / Eq. 3) block.
 int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
   const qg_plan& pl = gp->plan;
   const uint64_t exact = gp->balanced ? qg::max_exact_block_balanced(pl.p, pl.t, pl.e)
@@ -149,8 +150,8 @@ int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
   uint64_t kb = gp->kblock_words < K ? gp->kblock_words : K;
   if (kb > exact) kb = exact;
   if (kb >= K) {
-    const char* e = getenv("QG_TILED_SINGLE_BK");
-    *bk = e ? atoi(e) : 28;
+    const char* e = getenv("QG_TILED_SINGLE_BK");  // experiments
+    *bk = e ? atoi(e) : qg::stage_single(K);
     *kb_stages = 0;
     return QG_OK;
   }

@@ -148,21 +148,26 @@ __global__ void k_pack_a_tiled(const TIn* __restrict__ a, size_t m, size_t k, si
   }
 }
 
+// compress_cols_forward (gemm.hpp:122-140) words in the tiled transposed
+// layout: CB_t[tn][kt][r][c] = word (BK kt + c) of column 128 tn + r. One CTA
+// per 32 columns x 16 consecutive words (thousands of CTAs, so no partial last
+// wave): lane = column (each residue load is a coalesced 256-byte row
+// segment), the 8 warps split the 16 words; the 32 x 16 words then leave
+// through shared memory as 128-byte row runs of the output blocks. The grid
+// covers the zero padding of the layout too.
 template <typename TIn, int BK, bool BAL>
 __global__ void __launch_bounds__(256) k_pack_b_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
                                                       int t, int e, unsigned Kt, double* __restrict__ cb_t,
                                                       uint32_t p) {
-  // one block = 64 of the 128 rows (n) of one CB_t chunk (tn, kt); 4 thread
-  // rows split the BK words. Reads are coalesced along n, the chunk half is
-  // written contiguously through shared memory.
-  __shared__ double tile[64 * (BK + 1)];
+  __shared__ double tile[32][17];
   const size_t K = (k + e - 1) / e;
-  const size_t blk = blockIdx.x >> 1, half = blockIdx.x & 1;
-  const size_t kt = blk % Kt, tn = blk / Kt;
-  const int r = threadIdx.x & 63, cg = threadIdx.x >> 6;
-  const size_t col = tn * 128 + half * 64 + r;
-  for (int c = cg; c < BK; c += 4) {
-    const size_t gw = kt * BK + c;
+  const size_t w0 = (size_t)blockIdx.x * 16, n0 = (size_t)blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t col = n0 + lane;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cl = warp + 8 * h;
+    const size_t gw = w0 + cl;
     double wd;
     if (BAL) {
       long long w = 0;
@@ -181,11 +186,20 @@ __global__ void __launch_bounds__(256) k_pack_b_tiled(const TIn* __restrict__ b,
       }
       wd = __ull2double_rn(w);
     }
-    tile[r * (BK + 1) + c] = wd;
+    tile[lane][cl] = wd;
   }
   __syncthreads();
-  double* out = cb_t + blk * (size_t)(128 * BK) + half * (size_t)(64 * BK);
-  for (int i = threadIdx.x; i < 64 * BK; i += 256) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
+  const size_t Wpad = (size_t)Kt * BK;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = threadIdx.x + 256 * h;
+    const int r = i >> 4, cl = i & 15;
+    const size_t nn = n0 + r, w = w0 + cl;
+    if (w < Wpad) {
+      const size_t kt = w / BK, c = w % BK;
+      cb_t[(((nn >> 7) * Kt + kt) * 128 + (nn & 127)) * BK + c] = tile[r][cl];
+    }
+  }
 }
 
 // compress_outer_cols (gemm.hpp:145-158) words in the tiled transposed layout
@@ -562,7 +576,9 @@ static cudaError_t pack_tiled_t(bool b_operand, const TIn* src, size_t rows, siz
     const unsigned Kt = (unsigned)((K + BK - 1) / BK);
     const size_t Nt = (cols + 127) / 128;
     if (Kt == 0 || Nt == 0) return cudaSuccess;
-    k_pack_b_tiled<TIn, BK, BAL><<<(unsigned)(Nt * Kt * 2), 256, 0, s>>>(src, rows, cols, ld, t, e, Kt, dst, p);
+    const dim3 grid((unsigned)(((size_t)Kt * BK + 15) / 16), (unsigned)(Nt * 4));
+    if (grid.y > 65535) return cudaErrorInvalidValue;
+    k_pack_b_tiled<TIn, BK, BAL><<<grid, 256, 0, s>>>(src, rows, cols, ld, t, e, Kt, dst, p);
   } else {  // src is m x k
     const size_t K = (cols + e - 1) / e;
     const unsigned Kt = (unsigned)((K + BK - 1) / BK);

@@ -242,12 +242,32 @@ uint64_t stage_block_redq(uint64_t limit, int* bk) {
   return stage_block_set(limit, bk, kSet, 5);
 }
 
+// Stage depth for a single-block contraction of K words: least padded work
+// ceil(K/BK) BK x stage cost (config 3, K = 52: BK = 52, no padding; long K:
+// 28/36-word stages, which keep 3-4 stages in flight).
+int stage_single(uint64_t K) {
+  static const int kSet[] = {52, 44, 36, 28, 20, 12, 4};
+  int best = 28;
+  double best_cost = 1e300;
+  for (int b : kSet) {
+    const double cost = double((K + b - 1) / b * b) * stage_cost(b);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = b;
+    }
+  }
+  return best;
+}
+
 // Predicted relative cost of a blocked plan, in packed-word units: words
 // rounded up to the stage depth times the stage's per-word overhead, plus a
 // per-block flush cost.
 double blocked_cost(uint64_t k, int e, uint64_t kb_words, double flush_words) {
   const uint64_t K = (k + e - 1) / e;
-  if (kb_words >= K) return double((K + 27) / 28 * 28);  // single block: 28-word stages
+  if (kb_words >= K) {  // single block
+    const int b = stage_single(K);
+    return double((K + b - 1) / b * b) * stage_cost(b);
+  }
   int bk = 4;
   const uint64_t blk = stage_block_tiled(kb_words, &bk);
   if (blk == 0) return 1e300;

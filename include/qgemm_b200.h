@@ -319,7 +319,10 @@ int qg_host_random_residue_matrix(size_t rows, size_t cols, uint32_t p, uint64_t
 /* PhaseSeconds of the last host-data call on this thread (gemm.hpp
  * PhaseSeconds, reported by bench.hpp:67-152): multiply = device time of the
  * contraction kernels, convert = the rest of the call (transfers, packing,
- * extraction). */
+ * extraction). The split is measured only while qg_set_phase_timing(1) is in
+ * effect (timing events slow the pipelined host path); otherwise multiply is 0
+ * and convert the whole call. */
+void qg_set_phase_timing(int enable);
 void qg_last_phase_seconds(double* multiply, double* convert);
 
 /* ----------------------------------------------- matrix files (matrix_io.hpp)

@@ -256,6 +256,7 @@ struct PhaseSeconds {
   double multiply = 0;
   double convert = 0;
 };
+inline void set_phase_timing(bool enable) { qg_set_phase_timing(enable ? 1 : 0); }
 inline PhaseSeconds last_phase_seconds() {
   PhaseSeconds ph;
   qg_last_phase_seconds(&ph.multiply, &ph.convert);

@@ -202,6 +202,7 @@ def _load():
         "qg_host_uncompress": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp], i32),
         "qg_host_random_residue_matrix": ([sz, sz, u32, u64, vp], i32),
         "qg_last_phase_seconds": ([P(ctypes.c_double), P(ctypes.c_double)], None),
+        "qg_set_phase_timing": ([i32], None),
         "qg_parse_matrix": ([ctypes.c_char_p, sz, P(u32), P(sz), P(sz), P(P(u32))], i32),
         "qg_read_matrix_file": ([ctypes.c_char_p, P(u32), P(sz), P(sz), P(P(u32))], i32),
         "qg_write_matrix_file": ([ctypes.c_char_p, u32, vp, sz, sz], i32),

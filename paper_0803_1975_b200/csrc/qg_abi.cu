@@ -634,24 +634,41 @@ struct PhaseLog {
   double multiply = 0, convert = 0;
 };
 thread_local PhaseLog g_phase;
+// Recording timing events between the pipelined path's kernels costs ~0.36 ms
+// of a config-2 host call (measured), so the split is measured only on request.
+std::atomic<int> g_phase_timing{0};
 
 struct PhaseScope {
+  static constexpr int kPairs = 64;
+  // timing events created once per thread: creating them per call stalls the
+  // host's enqueue loop of the pipelined path (measured +0.36 ms on config 2)
+  static cudaEvent_t* pool() {
+    if (!g_phase_timing.load(std::memory_order_relaxed)) return nullptr;
+    static thread_local cudaEvent_t ev[2 * kPairs] = {};
+    static thread_local bool made = false;
+    if (!made) {
+      made = true;
+      for (auto& e : ev)
+        if (cudaEventCreate(&e) != cudaSuccess) e = nullptr;
+    }
+    return ev;
+  }
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  cudaEvent_t ev[2 * 64] = {};
+  cudaEvent_t* ev = pool();
   int n = 0;
+  const bool on = g_phase_timing.load(std::memory_order_relaxed) != 0;
   void begin(cudaStream_t s) {
-    if (n + 2 > 2 * 64) return;
-    cudaEventCreate(&ev[n]);
-    cudaEventCreate(&ev[n + 1]);
+    if (!on || n + 2 > 2 * kPairs || !ev[n] || !ev[n + 1]) return;
     cudaEventRecord(ev[n], s);
   }
   void end(cudaStream_t s) {
-    if (n + 2 > 2 * 64) return;
+    if (!on || n + 2 > 2 * kPairs || !ev[n] || !ev[n + 1]) return;
     cudaEventRecord(ev[n + 1], s);
     n += 2;
   }
   void finish() {  // after the call's final synchronize
     double mul = 0;
+    if (!on) n = 0;
     for (int i = 0; i < n; i += 2) {
       float ms = 0;
       if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) mul += ms * 1e-3;
@@ -659,10 +676,6 @@ struct PhaseScope {
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     g_phase.multiply = mul;
     g_phase.convert = wall > mul ? wall - mul : 0.0;
-  }
-  ~PhaseScope() {
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -715,7 +728,8 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
     thread_local HostPipe hp;
     if (!hp.ok) return QG_CUDA_ERROR;
     PhaseScope ps;
-    const size_t chunk = 512;  // rows per pipeline chunk (a multiple of the 128-row tile)
+    const char* ce = getenv("QG_HOST_CHUNK");  // experiments
+    const size_t chunk = ce ? (size_t)atoi(ce) : 512;  // rows per pipeline chunk (a multiple of 128)
     size_t nchunks = ceil_div(m, chunk);
     const size_t rows_per = nchunks > (size_t)HostPipe::kMaxChunks ? ceil_div(ceil_div(m, HostPipe::kMaxChunks), 128) * 128 : chunk;
     nchunks = ceil_div(m, rows_per);
@@ -1114,6 +1128,8 @@ int qg_host_random_residue_matrix(size_t rows, size_t cols, uint32_t p, uint64_t
   QG_TRY(cudaStreamSynchronize(s));
   return QG_OK;
 }
+
+void qg_set_phase_timing(int enable) { g_phase_timing.store(enable ? 1 : 0); }
 
 void qg_last_phase_seconds(double* multiply, double* convert) {
   if (multiply) *multiply = g_phase.multiply;

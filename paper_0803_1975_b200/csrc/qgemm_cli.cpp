@@ -299,6 +299,7 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
   const auto kpanel = number<std::uint64_t>(o, "kpanel", 0, false);
   check_modulus(p);
   const Algorithm algo = parse_algorithm(o.values.at("algo"));
+  set_phase_timing(true);  // seconds_multiply / seconds_convert per record
   const ResidueMatrix a = random_residue_matrix(m, k, p, seed);
   const ResidueMatrix b = random_residue_matrix(k, n, p, seed + 1);
   std::vector<TimingRecord> out;

@@ -440,7 +440,7 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
   const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
   uint32_t slot = 0, phase = 0;
   int nflush = 0;
-  if (MULTI && warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise SMSP warp pairs
+  if (warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise SMSP warp pairs
   for (int ts = 0; ts < my_tiles; ++ts) {
     int tm, tn;
     tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
@@ -547,8 +547,31 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
             for (int h = 0; h < 2; ++h) acc[mi][ni][h] = redq_word(acc[mi][ni][h], args.t, args.e, modp);
       }
     }
+    // interior tiles without accumulation (nearly all of them): no per-element
+    // bounds or accumulate checks, one int2 store per accumulator pair
+    const bool fast = EPI == EPI_DIGIT && !args.accumulate && m0 + BM <= M && n0 + BN <= N;
+    if (EPI == EPI_DIGIT && fast) {
+      int32_t* cbase = args.c + (size_t)(m0 + warp_m * WM + g) * args.ldc + n0 + warp_n * WN + 2 * t;
 #pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
+      for (int mi = 0; mi < MI; ++mi) {
+        int32_t* crow = cbase + (size_t)(mi * 8) * args.ldc;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          uint32_t r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t x = block_digit_t<BAL>(acc[mi][ni][h], args.anchor, args.qmask) + ds.get(mi, ni, h) +
+                               (BAL ? args.corr : 0u);
+            const uint32_t r0 = x - __umulhi(x, modp.magic) * modp.p;
+            r[h] = min(r0, r0 - modp.p);
+          }
+          *reinterpret_cast<int2*>(crow + ni * 8) = make_int2((int)r[0], (int)r[1]);
+          acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
+      }
+    }
+#pragma unroll
+    for (int mi = 0; mi < MI && !(EPI == EPI_DIGIT && fast); ++mi) {
       const int row = m0 + warp_m * WM + mi * 8 + g;
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {

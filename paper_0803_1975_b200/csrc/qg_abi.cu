@@ -56,11 +56,15 @@ int check_dtype(qg_dtype d) { return (d == QG_F64 || d == QG_U32 || d == QG_I32)
 
 // Device flag for DigitOverflow (redq / extract_all throw it in the reference).
 struct DeviceFlag {
+  // one persistent device int per host thread: a stream-ordered allocation
+  // per call costs a pool map/unmap round trip on every uncompress / redq
   int* ptr = nullptr;
   cudaStream_t s;
   explicit DeviceFlag(cudaStream_t st) : s(st) {
-    if (cudaMallocAsync(&ptr, sizeof(int), s) == cudaSuccess) cudaMemsetAsync(ptr, 0, sizeof(int), s);
-    else ptr = nullptr;
+    static thread_local int* flag = nullptr;
+    if (!flag && cudaMalloc(&flag, sizeof(int)) != cudaSuccess) flag = nullptr;
+    ptr = flag;
+    if (ptr && cudaMemsetAsync(ptr, 0, sizeof(int), s) != cudaSuccess) ptr = nullptr;
   }
   int read(int* value) {
     int v = 0;
@@ -68,9 +72,6 @@ struct DeviceFlag {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     *value = v;
     return cuda_status(e);
-  }
-  ~DeviceFlag() {
-    if (ptr) cudaFreeAsync(ptr, s);
   }
 };
 

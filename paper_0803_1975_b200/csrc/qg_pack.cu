@@ -424,11 +424,18 @@ cudaError_t launch_naive_gemm(const uint32_t* a, const uint32_t* b, size_t m, si
 
 // redq over a buffer, pack.hpp:124-137: every base-Q digit replaced by itself
 // mod p. A word outside [0, 2^(t e)) raises the DigitOverflow flag.
-__global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint32_t p,
+__device__ __forceinline__ uint32_t digit_mod(uint64_t x, int t, uint32_t p, uint32_t magic) {
+  if (t > 31) return (uint32_t)(x % p);  // one wide digit (e = 1 plans)
+  const uint32_t x32 = (uint32_t)x;
+  const uint32_t r = x32 - __umulhi(x32, magic) * p;
+  return min(r, r - p);
+}
+
+__global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint32_t p, uint32_t magic,
                        int* __restrict__ overflow) {
   const int total_bits = t * e;
   const double limit = (double)(1ull << total_bits);
-  const uint64_t mask = (1ull << t) - 1;
+  const uint64_t mask = t >= 64 ? ~0ull : (1ull << t) - 1;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x) {
     const double v = w[i];
@@ -438,38 +445,38 @@ __global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint3
     }
     const uint64_t bits = __double2ull_rz(v);
     uint64_t r = 0;
-    for (int s = 0; s < total_bits; s += t) r |= (((bits >> s) & mask) % p) << s;
+    for (int s = 0; s < total_bits; s += t) r |= (uint64_t)digit_mod((bits >> s) & mask, t, p, magic) << s;
     w[i] = __ull2double_rn(r);
   }
 }
 
 // uncompress, gemm.hpp:182-204 (+ extract_all, pack.hpp:104-119): every
 // stored word is split into its digits, each reduced mod p and scattered back
-// to its logical position; positions past the logical shape are dropped.
+// to its logical position; positions past the logical shape are dropped. 2-D
+// grid (stored rows on y, stored columns across threads): no index division.
 __global__ void k_uncompress(const double* __restrict__ w, size_t srows, size_t scols,
                              size_t lrows, size_t lcols, int t, int e, int slots, int reversed,
-                             int column_axis, uint32_t p, int32_t* __restrict__ out,
+                             int column_axis, uint32_t p, uint32_t magic, int32_t* __restrict__ out,
                              int* __restrict__ overflow) {
   const int total_bits = t * e;
   const double limit = (double)(1ull << total_bits);
-  const uint64_t mask = (1ull << t) - 1;
-  const size_t count = srows * scols;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < count;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t si = idx / scols, sj = idx % scols;
-    const double v = w[idx];
-    if (!(v >= 0.0) || !(v < limit)) {
-      atomicExch(overflow, 1);
-      continue;
-    }
-    const uint64_t bits = __double2ull_rz(v);
-    for (int s = 0; s < slots; ++s) {
-      const int di = reversed ? slots - 1 - s : s;
-      const uint64_t digit = di < e ? (bits >> (t * di)) & mask : 0;
-      size_t i = si, j = sj;
-      if (column_axis) j = sj * slots + s;
-      else i = si * slots + s;
-      if (i < lrows && j < lcols) out[i * lcols + j] = (int32_t)(digit % p);
+  const uint64_t mask = t >= 64 ? ~0ull : (1ull << t) - 1;
+  for (size_t si = blockIdx.y; si < srows; si += gridDim.y) {
+    for (size_t sj = blockIdx.x * (size_t)blockDim.x + threadIdx.x; sj < scols; sj += (size_t)gridDim.x * blockDim.x) {
+      const double v = w[si * scols + sj];
+      if (!(v >= 0.0) || !(v < limit)) {
+        atomicExch(overflow, 1);
+        continue;
+      }
+      const uint64_t bits = __double2ull_rz(v);
+      for (int s = 0; s < slots; ++s) {
+        const int di = reversed ? slots - 1 - s : s;
+        const uint64_t digit = di < e ? (bits >> (t * di)) & mask : 0;
+        size_t i = si, j = sj;
+        if (column_axis) j = sj * slots + s;
+        else i = si * slots + s;
+        if (i < lrows && j < lcols) out[i * lcols + j] = (int32_t)digit_mod(digit, t, p, magic);
+      }
     }
   }
 }
@@ -682,7 +689,7 @@ cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size
 cudaError_t launch_redq(double* w, size_t count, int t, int e, uint32_t p, int* overflow,
                         cudaStream_t s) {
   if (count == 0) return cudaSuccess;
-  k_redq<<<grid1d(count, 256), 256, 0, s>>>(w, count, t, e, p, overflow);
+  k_redq<<<grid1d(count, 256), 256, 0, s>>>(w, count, t, e, p, (uint32_t)(0x100000000ull / p), overflow);
   count_launch();
   return cudaGetLastError();
 }
@@ -690,12 +697,16 @@ cudaError_t launch_redq(double* w, size_t count, int t, int e, uint32_t p, int* 
 cudaError_t launch_uncompress(const double* w, size_t srows, size_t scols, size_t lrows,
                               size_t lcols, int t, int e, int slots, int reversed, int column_axis,
                               uint32_t p, int32_t* out, int* overflow, cudaStream_t s) {
-  if (lrows * lcols)
-    cudaMemsetAsync(out, 0, lrows * lcols * sizeof(int32_t), s);
+  // zero only what no stored word covers (ResidueMatrix's zero fill)
+  const bool covered = column_axis ? (srows >= lrows && scols * (size_t)slots >= lcols)
+                                   : (scols >= lcols && srows * (size_t)slots >= lrows);
+  if (lrows * lcols && !covered) cudaMemsetAsync(out, 0, lrows * lcols * sizeof(int32_t), s);
   const size_t count = srows * scols;
   if (count == 0) return cudaGetLastError();
-  k_uncompress<<<grid1d(count, 256), 256, 0, s>>>(w, srows, scols, lrows, lcols, t, e, slots,
-                                                   reversed, column_axis, p, out, overflow);
+  const size_t gx = (scols + 255) / 256;
+  const dim3 grid((unsigned)(gx < 4096 ? gx : 4096), (unsigned)(srows < 65535 ? srows : 65535));
+  k_uncompress<<<grid, 256, 0, s>>>(w, srows, scols, lrows, lcols, t, e, slots, reversed, column_axis, p,
+                                    (uint32_t)(0x100000000ull / p), out, overflow);
   count_launch();
   return cudaGetLastError();
 }

@@ -325,6 +325,60 @@ int qg_host_random_residue_matrix(size_t rows, size_t cols, uint32_t p, uint64_t
 void qg_set_phase_timing(int enable);
 void qg_last_phase_seconds(double* multiply, double* convert);
 
+/* ------------------------------------------------- Int64Word backend
+ * word.hpp:36-54: packed words are uint64, word products wrap mod 2^64, plans
+ * may use beta up to 63 (t e <= 62). Same entry points as the DoubleWord ones
+ * with uint64 word buffers; the common product adds Int64Word::high_part =
+ * ((a b) >> t d) & (Q-1) per term. Integer kernels on the CUDA cores (no FP64
+ * tensor path for 64-bit words); bit-identical to the reference's Int64Word
+ * results. */
+int qg_compress_rows_reversed_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t m, size_t k, size_t lda,
+                                  uint64_t* ca, size_t ldca, void* stream);
+int qg_compress_cols_forward_u64(const qg_plan* plan, const void* b, qg_dtype dtype, size_t k, size_t n, size_t ldb,
+                                 uint64_t* cb, size_t ldcb, void* stream);
+int qg_compress_outer_cols_u64(const qg_plan* plan, const void* b, qg_dtype dtype, size_t rows, size_t cols,
+                               size_t ldb, uint64_t* out, size_t ldo, void* stream);
+int qg_compress_outer_rows_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t rows, size_t cols,
+                               size_t lda, uint64_t* out, size_t ldo, void* stream);
+/* packed_common_product<Int64Word> gemm.hpp:210-244 (groups = packed words per row) */
+int qg_packed_common_product_u64(const qg_plan* plan, const uint64_t* ca, const uint64_t* cb, size_t m, size_t n,
+                                 size_t groups, uint64_t* acc, void* stream);
+int qg_reduce_common_u64(const qg_plan* plan, const uint64_t* acc, size_t count, int32_t* c, void* stream);
+int qg_extract_coefficients_u64(const qg_plan* plan, const uint64_t* words, size_t count, int32_t* out, void* stream);
+int qg_reduce_and_compress_u64(const qg_plan* plan, const uint64_t* words, size_t rows, size_t cols, size_t ldw,
+                               uint64_t* out, size_t ldo, void* stream);
+int qg_redq_u64(const qg_plan* plan, uint64_t* words, size_t count, void* stream);
+int qg_uncompress_u64(const qg_plan* plan, qg_orientation o, const uint64_t* words, size_t stored_rows,
+                      size_t stored_cols, size_t logical_rows, size_t logical_cols, int32_t* out, void* stream);
+/* packed_right_product / mul_right_compressed <Int64Word>, gemm.hpp:285-325;
+ * a: m x k residues (dtype, lda), cbo: k x ceil(n/e) words, cc: m x ceil(n/e) */
+int qg_packed_right_product_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t lda, const uint64_t* cbo,
+                                size_t m, size_t k, size_t n, uint64_t* cc, void* stream);
+int qg_mul_right_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t lda, const uint64_t* cbo, size_t m,
+                     size_t k, size_t n, uint64_t* cc, void* stream);
+/* packed_left_product / mul_left_compressed <Int64Word>, gemm.hpp:340-371;
+ * ca: ceil(m/e) x k words, b: k x n residues (dtype, ldb), cc: ceil(m/e) x n */
+int qg_packed_left_product_u64(const qg_plan* plan, const uint64_t* ca, const void* b, qg_dtype dtype, size_t ldb,
+                               size_t m, size_t k, size_t n, uint64_t* cc, void* stream);
+int qg_mul_left_u64(const qg_plan* plan, const uint64_t* ca, const void* b, qg_dtype dtype, size_t ldb, size_t m,
+                    size_t k, size_t n, uint64_t* cc, void* stream);
+/* mul_full_compressed<Int64Word>, gemm.hpp:377-445 (device residues in, int32 C) */
+int qg_mul_full_u64(const qg_full_plan* fp, const void* a, qg_dtype adt, const void* b, qg_dtype bdt, size_t m,
+                    size_t k, size_t n, int32_t* c, size_t ldc, void* stream);
+/* host-data entries (value semantics) */
+int qg_host_mul_common_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                           uint32_t* c);
+int qg_host_blocked_accumulate_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                                   size_t n, size_t kpanel, uint32_t* c);
+int qg_host_mul_right_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                          uint64_t* cc);
+int qg_host_mul_left_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                         uint64_t* cc);
+int qg_host_mul_full_i64(const qg_full_plan* fp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                         uint32_t* c);
+int qg_host_uncompress_u64(const qg_plan* plan, qg_orientation o, const uint64_t* words, size_t stored_rows,
+                           size_t stored_cols, size_t logical_rows, size_t logical_cols, uint32_t* out);
+
 /* ----------------------------------------------- matrix files (matrix_io.hpp)
  * "M <p> <rows> <cols>" then rows*cols whitespace-separated residues in
  * [0, p-1], row-major (matrix_io.hpp:14-22). Readers return QG_PARSE_ERROR

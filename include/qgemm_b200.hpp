@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -356,6 +357,101 @@ inline std::string to_csv_row(const TimingRecord& r) {
                   ',' + std::to_string(r.n) + ',' + std::to_string(r.t) + ',' + std::to_string(r.e) + ',';
   std::snprintf(buf, sizeof buf, "%.6f,%.6f,", r.seconds_multiply, r.seconds_convert);
   return s + buf + std::to_string(r.checksum);
+}
+
+// ------------------------------------------------------------ word backends
+// word.hpp:10-54. Without a template argument every entry point above runs
+// the DoubleWord backend (the FP64 tensor-core path); mul_*<Int64Word>(...)
+// runs the reference's Int64Word semantics (uint64 words, wrapping products,
+// beta up to 63) on the device's integer pipes.
+struct DoubleWord {
+  static constexpr int exact_bits = 53;
+};
+struct Int64Word {
+  static constexpr int exact_bits = 63;
+};
+
+// Words of an Int64Word right/left product (CompressedMatrix<Int64Word>).
+struct CompressedWords64 {
+  std::size_t logical_rows = 0, logical_cols = 0, stored_rows = 0, stored_cols = 0;
+  qg_orientation orientation{QG_FORWARD, QG_COLUMN, 1};
+  CompressionPlan plan;
+  std::vector<std::uint64_t> data;
+};
+
+template <class B>
+inline ResidueMatrix mul_common_compressed(const ResidueMatrix& a, const ResidueMatrix& b, const CompressionPlan& plan) {
+  if constexpr (std::is_same_v<B, Int64Word>) {
+    detail::check_inner_dims(a, b);
+    ResidueMatrix c(a.rows, b.cols);
+    check(qg_host_mul_common_i64(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, c.data.data()),
+          "mul_common_compressed<Int64Word>");
+    return c;
+  } else {
+    return mul_common_compressed(a, b, plan);
+  }
+}
+template <class B>
+inline ResidueMatrix blocked_accumulate(const ResidueMatrix& a, const ResidueMatrix& b, const CompressionPlan& plan,
+                                        std::size_t kpanel) {
+  if constexpr (std::is_same_v<B, Int64Word>) {
+    detail::check_inner_dims(a, b);
+    ResidueMatrix c(a.rows, b.cols);
+    check(qg_host_blocked_accumulate_i64(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, kpanel,
+                                         c.data.data()),
+          "blocked_accumulate<Int64Word>");
+    return c;
+  } else {
+    return blocked_accumulate(a, b, plan, kpanel);
+  }
+}
+template <class B>
+inline ResidueMatrix mul_full_compressed(const ResidueMatrix& a, const ResidueMatrix& b, const FullPlan& fp) {
+  if constexpr (std::is_same_v<B, Int64Word>) {
+    detail::check_inner_dims(a, b);
+    ResidueMatrix c(a.rows, b.cols);
+    check(qg_host_mul_full_i64(&fp.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, c.data.data()),
+          "mul_full_compressed<Int64Word>");
+    return c;
+  } else {
+    return mul_full_compressed(a, b, fp);
+  }
+}
+// mul_right_compressed / mul_left_compressed <Int64Word>: post-REDQ uint64 words
+inline CompressedWords64 mul_right_compressed_i64(const ResidueMatrix& a, const ResidueMatrix& b,
+                                                  const CompressionPlan& plan) {
+  detail::check_inner_dims(a, b);
+  CompressedWords64 cc;
+  cc.logical_rows = cc.stored_rows = a.rows;
+  cc.logical_cols = b.cols;
+  cc.stored_cols = (b.cols + plan.e() - 1) / plan.e();
+  cc.orientation = qg_orientation{QG_FORWARD, QG_COLUMN, plan.e()};
+  cc.plan = plan;
+  cc.data.resize(cc.stored_rows * cc.stored_cols);
+  check(qg_host_mul_right_i64(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, cc.data.data()),
+        "mul_right_compressed<Int64Word>");
+  return cc;
+}
+inline CompressedWords64 mul_left_compressed_i64(const ResidueMatrix& a, const ResidueMatrix& b,
+                                                 const CompressionPlan& plan) {
+  detail::check_inner_dims(a, b);
+  CompressedWords64 cc;
+  cc.logical_rows = a.rows;
+  cc.logical_cols = cc.stored_cols = b.cols;
+  cc.stored_rows = (a.rows + plan.e() - 1) / plan.e();
+  cc.orientation = qg_orientation{QG_FORWARD, QG_ROW, plan.e()};
+  cc.plan = plan;
+  cc.data.resize(cc.stored_rows * cc.stored_cols);
+  check(qg_host_mul_left_i64(&plan.c, a.data.data(), b.data.data(), a.rows, a.cols, b.cols, cc.data.data()),
+        "mul_left_compressed<Int64Word>");
+  return cc;
+}
+inline ResidueMatrix uncompress(const CompressedWords64& cm) {
+  ResidueMatrix c(cm.logical_rows, cm.logical_cols);
+  check(qg_host_uncompress_u64(&cm.plan.c, cm.orientation, cm.data.data(), cm.stored_rows, cm.stored_cols,
+                               cm.logical_rows, cm.logical_cols, c.data.data()),
+        "uncompress<Int64Word>");
+  return c;
 }
 
 // residue_checksum, bench.hpp:43-47.

@@ -96,6 +96,21 @@ def _load_c():
         "qgo_packed_left_product": ([P(Plan), vp, vp, sz, sz, sz, vp, i32], i32),
         "qgo_mul_left_compressed": ([P(Plan), vp, vp, sz, sz, sz, vp, i32], i32),
         "qgo_mul_full_compressed": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qgo_compress_rows_reversed_i64": ([P(Plan), vp, sz, sz, vp], i32),
+        "qgo_compress_cols_forward_i64": ([P(Plan), vp, sz, sz, vp], i32),
+        "qgo_compress_outer_cols_i64": ([P(Plan), vp, sz, sz, vp], i32),
+        "qgo_compress_outer_rows_i64": ([P(Plan), vp, sz, sz, vp], i32),
+        "qgo_packed_common_product_i64": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qgo_reduce_common_entry_i64": ([u64, P(Plan)], u32),
+        "qgo_extract_coefficient_i64": ([u64, P(Plan)], u32),
+        "qgo_redq_i64": ([u64, P(Plan), P(u64)], i32),
+        "qgo_redq_in_place_i64": ([P(Plan), vp, sz], i32),
+        "qgo_uncompress_i64": ([P(Plan), Orientation, vp, sz, sz, sz, sz, vp], i32),
+        "qgo_packed_right_product_i64": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qgo_packed_left_product_i64": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qgo_mul_full_compressed_i64": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qgo_blocked_accumulate_i64": ([P(Plan), vp, vp, sz, sz, sz, sz, vp], i32),
+        "qgo_reduce_and_compress_i64": ([vp, sz, P(Plan), vp], i32),
         "qgo_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp, i32], i32),
         "qgo_residue_checksum": ([vp, sz], u32),
     }
@@ -139,6 +154,14 @@ def _load_ref():
         "qgref_write_matrix": ([vp, sz, sz, u32, ctypes.c_char_p, sz], sz),
         "qgref_mul_left": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
         "qgref_mul_full": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qgref_pack_i64": ([i32, P(Plan), vp, sz, sz, vp], i32),
+        "qgref_common_i64": ([P(Plan), vp, vp, sz, sz, sz, vp, vp], i32),
+        "qgref_right_i64": ([P(Plan), vp, vp, sz, sz, sz, vp, vp], i32),
+        "qgref_left_i64": ([P(Plan), vp, vp, sz, sz, sz, vp, vp], i32),
+        "qgref_full_i64": ([P(FullPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qgref_blocked_i64": ([P(Plan), vp, vp, sz, sz, sz, sz, vp], i32),
+        "qgref_extract_i64": ([P(Plan), u64, P(u32)], i32),
+        "qgref_redq_i64": ([P(Plan), u64, P(u64)], i32),
         "qgref_naive_gemm": ([u32, vp, vp, sz, sz, sz, vp], i32),
     }
     for name, (args, res) in sig.items():

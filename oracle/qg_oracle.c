@@ -667,3 +667,230 @@ uint32_t qgo_residue_checksum(const uint32_t* c, size_t count) {
   for (size_t i = 0; i < count; ++i) s += c[i];
   return s;
 }
+
+/* ================================================ Int64Word (word.hpp:36-54)
+ * The same routines over uint64 words: products wrap modulo 2^64, the common
+ * product adds high_part = ((a b) >> t d) & (Q-1) per term (word.hpp:51-53),
+ * extraction is ((w >> t d) & (Q-1)) mod p (pack.hpp:96-98). Plans may use
+ * beta up to 63. */
+static int check_backend_i64(const qgo_plan* plan) { return plan->beta > 63 ? QGO_PLAN_MISMATCH : QGO_OK; }
+
+static uint64_t i64_forward(const uint32_t* v, size_t len, int t) { /* pack.hpp:27-32 */
+  uint64_t r = 0;
+  for (size_t i = len; i-- > 0;) r = (r << t) | v[i];
+  return r;
+}
+static uint64_t i64_reverse(const uint32_t* v, size_t len, int t, int e) { /* pack.hpp:59-70 */
+  uint64_t r = 0;
+  for (size_t i = 0; i < len; ++i) r = (r << t) | v[i];
+  return r << (t * (e - (int)len));
+}
+
+int qgo_compress_rows_reversed_i64(const qgo_plan* plan, const uint32_t* a, size_t m, size_t k, uint64_t* ca) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  if (k > plan->kmax) return QGO_PLAN_MISMATCH;
+  const size_t groups = group_count(k, plan->e);
+  for (size_t i = 0; i < m; ++i)
+    for (size_t g = 0; g < groups; ++g) {
+      const size_t base = g * plan->e, len = k - base < (size_t)plan->e ? k - base : (size_t)plan->e;
+      ca[i * groups + g] = i64_reverse(a + i * k + base, len, plan->t, plan->e);
+    }
+  return QGO_OK;
+}
+
+int qgo_compress_cols_forward_i64(const qgo_plan* plan, const uint32_t* b, size_t k, size_t n, uint64_t* cb) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  if (k > plan->kmax) return QGO_PLAN_MISMATCH;
+  const size_t groups = group_count(k, plan->e);
+  uint32_t column[64];
+  for (size_t g = 0; g < groups; ++g) {
+    const size_t base = g * plan->e, len = k - base < (size_t)plan->e ? k - base : (size_t)plan->e;
+    for (size_t j = 0; j < n; ++j) {
+      for (size_t s = 0; s < len; ++s) column[s] = b[(base + s) * n + j];
+      cb[g * n + j] = i64_forward(column, len, plan->t);
+    }
+  }
+  return QGO_OK;
+}
+
+int qgo_compress_outer_cols_i64(const qgo_plan* plan, const uint32_t* b, size_t k, size_t n, uint64_t* cb) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  const size_t groups = group_count(n, plan->e);
+  for (size_t i = 0; i < k; ++i)
+    for (size_t g = 0; g < groups; ++g) {
+      const size_t base = g * plan->e, len = n - base < (size_t)plan->e ? n - base : (size_t)plan->e;
+      cb[i * groups + g] = i64_forward(b + i * n + base, len, plan->t);
+    }
+  return QGO_OK;
+}
+
+int qgo_compress_outer_rows_i64(const qgo_plan* plan, const uint32_t* a, size_t m, size_t k, uint64_t* ca) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  const size_t groups = group_count(m, plan->e);
+  uint32_t column[64];
+  for (size_t g = 0; g < groups; ++g) {
+    const size_t base = g * plan->e, len = m - base < (size_t)plan->e ? m - base : (size_t)plan->e;
+    for (size_t j = 0; j < k; ++j) {
+      for (size_t s = 0; s < len; ++s) column[s] = a[(base + s) * k + j];
+      ca[g * k + j] = i64_forward(column, len, plan->t);
+    }
+  }
+  return QGO_OK;
+}
+
+/* packed_common_product<Int64Word>, gemm.hpp:210-244 */
+int qgo_packed_common_product_i64(const qgo_plan* plan, const uint64_t* ca, const uint64_t* cb, size_t m, size_t n,
+                                  size_t groups, uint64_t* acc) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  const int sh = plan->t * plan->d;
+  const uint64_t mask = qmask(plan);
+  for (size_t i = 0; i < m; ++i)
+    for (size_t j = 0; j < n; ++j) {
+      uint64_t s = 0;
+      for (size_t g = 0; g < groups; ++g) s += ((ca[i * groups + g] * cb[g * n + j]) >> sh) & mask;
+      acc[i * n + j] = s;
+    }
+  return QGO_OK;
+}
+
+uint32_t qgo_reduce_common_entry_i64(uint64_t w, const qgo_plan* plan) { return (uint32_t)((w & qmask(plan)) % plan->p); }
+
+uint32_t qgo_extract_coefficient_i64(uint64_t w, const qgo_plan* plan) {
+  return (uint32_t)(((w >> (plan->t * plan->d)) & qmask(plan)) % plan->p);
+}
+
+/* redq<Int64Word>, pack.hpp:124-137 */
+int qgo_redq_i64(uint64_t w, const qgo_plan* plan, uint64_t* out) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  const int total = plan->t * plan->e;
+  if (total < 64 && w >= (UINT64_C(1) << total)) return QGO_DIGIT_OVERFLOW;
+  uint64_t r = 0;
+  for (int i = 0; i < total; i += plan->t) r |= (((w >> i) & qmask(plan)) % plan->p) << i;
+  *out = r;
+  return QGO_OK;
+}
+
+int qgo_uncompress_i64(const qgo_plan* plan, qgo_orientation o, const uint64_t* words, size_t stored_rows,
+                       size_t stored_cols, size_t logical_rows, size_t logical_cols, uint32_t* out) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  const int total = plan->t * plan->e;
+  memset(out, 0, logical_rows * logical_cols * sizeof(uint32_t));
+  for (size_t si = 0; si < stored_rows; ++si)
+    for (size_t sj = 0; sj < stored_cols; ++sj) {
+      const uint64_t w = words[si * stored_cols + sj];
+      if (total < 64 && w >= (UINT64_C(1) << total)) return QGO_DIGIT_OVERFLOW;
+      for (int s = 0; s < o.slots; ++s) {
+        const int di = o.direction == 1 ? o.slots - 1 - s : s;
+        const uint64_t digit = di < plan->e ? (w >> (plan->t * di)) & qmask(plan) : 0;
+        const size_t i = o.axis == 1 ? si : si * o.slots + s, j = o.axis == 1 ? sj * o.slots + s : sj;
+        if (i < logical_rows && j < logical_cols) out[i * logical_cols + j] = (uint32_t)(digit % plan->p);
+      }
+    }
+  return QGO_OK;
+}
+
+/* packed_right_product<Int64Word>, gemm.hpp:285-310: cc = A x CBo, wrapping. */
+int qgo_packed_right_product_i64(const qgo_plan* plan, const uint32_t* a, const uint64_t* cb, size_t m, size_t k,
+                                 size_t n, uint64_t* cc) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  if (k > plan->kmax) return QGO_PLAN_MISMATCH;
+  const size_t h = group_count(n, plan->e);
+  for (size_t i = 0; i < m; ++i)
+    for (size_t g = 0; g < h; ++g) {
+      uint64_t s = 0;
+      for (size_t l = 0; l < k; ++l) s += (uint64_t)a[i * k + l] * cb[l * h + g];
+      cc[i * h + g] = s;
+    }
+  return QGO_OK;
+}
+
+/* packed_left_product<Int64Word>, gemm.hpp:340-364 */
+int qgo_packed_left_product_i64(const qgo_plan* plan, const uint64_t* ca, const uint32_t* b, size_t m, size_t k,
+                                size_t n, uint64_t* cc) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  if (k > plan->kmax) return QGO_PLAN_MISMATCH;
+  const size_t gr = group_count(m, plan->e);
+  for (size_t g = 0; g < gr; ++g)
+    for (size_t j = 0; j < n; ++j) {
+      uint64_t s = 0;
+      for (size_t l = 0; l < k; ++l) s += ca[g * k + l] * (uint64_t)b[l * n + j];
+      cc[g * n + j] = s;
+    }
+  return QGO_OK;
+}
+
+int qgo_redq_in_place_i64(const qgo_plan* plan, uint64_t* words, size_t count) {
+  for (size_t i = 0; i < count; ++i) {
+    int st = qgo_redq_i64(words[i], plan, words + i);
+    if (st) return st;
+  }
+  return QGO_OK;
+}
+
+/* mul_full_compressed<Int64Word>, gemm.hpp:377-445 */
+int qgo_mul_full_compressed_i64(const qgo_full_plan* fp, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                                size_t n, uint32_t* c) {
+  const qgo_plan* pl = &fp->base;
+  if (check_backend_i64(pl)) return QGO_PLAN_MISMATCH;
+  if (k > pl->kmax) return QGO_PLAN_MISMATCH;
+  const int qs = fp->dq + 1, ts = fp->dtheta + 1, t = pl->t;
+  const size_t gr = group_count(m, qs), hc = group_count(n, ts);
+  const uint64_t mask = qmask(pl);
+  for (size_t g = 0; g < gr; ++g)
+    for (size_t h = 0; h < hc; ++h) {
+      uint64_t acc = 0;
+      for (size_t l = 0; l < k; ++l) {
+        uint64_t wa = 0, wb = 0;
+        const size_t la = m - g * qs < (size_t)qs ? m - g * qs : (size_t)qs;
+        for (size_t s = la; s-- > 0;) wa = (wa << t) | a[(g * qs + s) * k + l];
+        const size_t lb = n - h * ts < (size_t)ts ? n - h * ts : (size_t)ts;
+        for (size_t s = lb; s-- > 0;) wb = (wb << fp->theta_exponent) | b[l * n + h * ts + s];
+        acc += wa * wb;
+      }
+      for (int j = 0; j < ts; ++j)
+        for (int i = 0; i < qs; ++i) {
+          const size_t row = g * qs + i, col = h * ts + j;
+          if (row < m && col < n) c[row * n + col] = (uint32_t)(((acc >> (t * (i + j * qs))) & mask) % pl->p);
+        }
+    }
+  return QGO_OK;
+}
+
+/* blocked_accumulate<Int64Word>, gemm.hpp:450-489 */
+int qgo_blocked_accumulate_i64(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                               size_t kpanel, uint32_t* c) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  if (kpanel < 1) return QGO_INVALID_ARGUMENT;
+  if (kpanel > plan->kmax) return QGO_PLAN_MISMATCH;
+  memset(c, 0, m * n * sizeof(uint32_t));
+  const int sh = plan->t * plan->d;
+  const uint64_t mask = qmask(plan);
+  for (size_t k0 = 0; k0 < k; k0 += kpanel) {
+    const size_t len = k - k0 < kpanel ? k - k0 : kpanel, groups = group_count(len, plan->e);
+    for (size_t i = 0; i < m; ++i)
+      for (size_t j = 0; j < n; ++j) {
+        uint64_t acc = 0;
+        uint32_t col[64];
+        for (size_t g = 0; g < groups; ++g) {
+          const size_t base = g * plan->e, gl = len - base < (size_t)plan->e ? len - base : (size_t)plan->e;
+          for (size_t s = 0; s < gl; ++s) col[s] = b[(k0 + base + s) * n + j];
+          const uint64_t wa = i64_reverse(a + i * k + k0 + base, gl, plan->t, plan->e), wb = i64_forward(col, gl, plan->t);
+          acc += ((wa * wb) >> sh) & mask;
+        }
+        c[i * n + j] = (uint32_t)(((uint64_t)c[i * n + j] + (acc & mask) % plan->p) % plan->p);
+      }
+  }
+  return QGO_OK;
+}
+
+/* reduce_and_compress<Int64Word>, pack.hpp:141-155 */
+int qgo_reduce_and_compress_i64(const uint64_t* row, size_t len, const qgo_plan* plan, uint64_t* out) {
+  if (check_backend_i64(plan)) return QGO_PLAN_MISMATCH;
+  uint32_t red[64];
+  for (size_t g = 0; g < len; g += plan->e) {
+    const size_t gl = len - g < (size_t)plan->e ? len - g : (size_t)plan->e;
+    for (size_t s = 0; s < gl; ++s) red[s] = qgo_extract_coefficient_i64(row[g + s], plan);
+    out[g / plan->e] = i64_forward(red, gl, plan->t);
+  }
+  return QGO_OK;
+}

@@ -317,6 +317,82 @@ size_t qgref_write_matrix(const uint32_t* data, size_t rows, size_t cols, uint32
   return s.size();
 }
 
+// ---- Int64Word instantiations (word.hpp:36-54), to pin the i64 restatement
+// kind 0 rows_reversed, 1 cols_forward, 2 outer_cols, 3 outer_rows
+int qgref_pack_i64(int kind, const qgo_plan* plan, const uint32_t* src, size_t rows, size_t cols, uint64_t* out) {
+  return guarded([&] {
+    const CompressionPlan pl = import_plan(plan);
+    const ResidueMatrix m = wrap(src, rows, cols);
+    CompressedMatrix<Int64Word> cm = kind == 0   ? compress_rows_reversed<Int64Word>(m, pl)
+                                     : kind == 1 ? compress_cols_forward<Int64Word>(m, pl)
+                                     : kind == 2 ? compress_outer_cols<Int64Word>(m, pl)
+                                                 : compress_outer_rows<Int64Word>(m, pl);
+    for (size_t i = 0; i < cm.data.size(); ++i) out[i] = cm.data[i].value;
+  });
+}
+
+int qgref_common_i64(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                     uint64_t* acc, uint32_t* c) {
+  return guarded([&] {
+    const CompressionPlan pl = import_plan(plan);
+    const auto ca = compress_rows_reversed<Int64Word>(wrap(a, m, k), pl);
+    const auto cb = compress_cols_forward<Int64Word>(wrap(b, k, n), pl);
+    const auto w = packed_common_product(ca, cb);
+    for (size_t i = 0; i < w.size(); ++i) acc[i] = w[i].value;
+    const ResidueMatrix r = mul_common_compressed<Int64Word>(wrap(a, m, k), wrap(b, k, n), pl);
+    std::memcpy(c, r.data.data(), r.data.size() * sizeof(uint32_t));
+  });
+}
+
+int qgref_right_i64(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                    uint64_t* pre, uint64_t* cc) {
+  return guarded([&] {
+    const CompressionPlan pl = import_plan(plan);
+    const auto cbo = compress_outer_cols<Int64Word>(wrap(b, k, n), pl);
+    const auto p0 = packed_right_product(wrap(a, m, k), cbo);
+    for (size_t i = 0; i < p0.data.size(); ++i) pre[i] = p0.data[i].value;
+    const auto r = mul_right_compressed(wrap(a, m, k), cbo);
+    for (size_t i = 0; i < r.data.size(); ++i) cc[i] = r.data[i].value;
+  });
+}
+
+int qgref_left_i64(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                   uint64_t* pre, uint64_t* cc) {
+  return guarded([&] {
+    const CompressionPlan pl = import_plan(plan);
+    const auto ca = compress_outer_rows<Int64Word>(wrap(a, m, k), pl);
+    const auto p0 = packed_left_product(ca, wrap(b, k, n));
+    for (size_t i = 0; i < p0.data.size(); ++i) pre[i] = p0.data[i].value;
+    const auto r = mul_left_compressed(ca, wrap(b, k, n));
+    for (size_t i = 0; i < r.data.size(); ++i) cc[i] = r.data[i].value;
+  });
+}
+
+int qgref_full_i64(const qgo_full_plan* fp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                   uint32_t* c) {
+  return guarded([&] {
+    FullPlan f{import_plan(&fp->base), fp->dq, fp->dtheta, fp->theta_exponent};
+    const auto r = mul_full_compressed<Int64Word>(wrap(a, m, k), wrap(b, k, n), f);
+    std::memcpy(c, r.data.data(), r.data.size() * sizeof(uint32_t));
+  });
+}
+
+int qgref_blocked_i64(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                      size_t kpanel, uint32_t* c) {
+  return guarded([&] {
+    const auto r = blocked_accumulate<Int64Word>(wrap(a, m, k), wrap(b, k, n), import_plan(plan), kpanel);
+    std::memcpy(c, r.data.data(), r.data.size() * sizeof(uint32_t));
+  });
+}
+
+int qgref_extract_i64(const qgo_plan* plan, uint64_t w, uint32_t* out) {
+  return guarded([&] { *out = extract_coefficient(PackedWord<Int64Word>{w}, import_plan(plan)); });
+}
+
+int qgref_redq_i64(const qgo_plan* plan, uint64_t w, uint64_t* out) {
+  return guarded([&] { *out = redq(PackedWord<Int64Word>{w}, import_plan(plan)).value; });
+}
+
 int qgref_blocked_accumulate(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
                              size_t k, size_t n, size_t kpanel, uint32_t* c) {
   return guarded([&] {

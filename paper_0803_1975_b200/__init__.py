@@ -207,6 +207,26 @@ def _load():
         "qg_read_matrix_file": ([ctypes.c_char_p, P(u32), P(sz), P(sz), P(P(u32))], i32),
         "qg_write_matrix_file": ([ctypes.c_char_p, u32, vp, sz, sz], i32),
         "qg_free": ([vp], None),
+        "qg_compress_rows_reversed_u64": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_compress_cols_forward_u64": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_compress_outer_cols_u64": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_compress_outer_rows_u64": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_packed_common_product_u64": ([P(_Plan), vp, vp, sz, sz, sz, vp, vp], i32),
+        "qg_reduce_common_u64": ([P(_Plan), vp, sz, vp, vp], i32),
+        "qg_extract_coefficients_u64": ([P(_Plan), vp, sz, vp, vp], i32),
+        "qg_reduce_and_compress_u64": ([P(_Plan), vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_redq_u64": ([P(_Plan), vp, sz, vp], i32),
+        "qg_uncompress_u64": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp, vp], i32),
+        "qg_packed_right_product_u64": ([P(_Plan), vp, i32, sz, vp, sz, sz, sz, vp, vp], i32),
+        "qg_mul_right_u64": ([P(_Plan), vp, i32, sz, vp, sz, sz, sz, vp, vp], i32),
+        "qg_packed_left_product_u64": ([P(_Plan), vp, vp, i32, sz, sz, sz, sz, vp, vp], i32),
+        "qg_mul_left_u64": ([P(_Plan), vp, vp, i32, sz, sz, sz, sz, vp, vp], i32),
+        "qg_mul_full_u64": ([P(_FullPlan), vp, i32, vp, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_host_mul_common_i64": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_blocked_accumulate_i64": ([P(_Plan), vp, vp, sz, sz, sz, sz, vp], i32),
+        "qg_host_mul_right_i64": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_left_i64": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_full_i64": ([P(_FullPlan), vp, vp, sz, sz, sz, vp], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),
@@ -1011,3 +1031,173 @@ def write_matrix_file(path: str, m, p: int) -> None:
 
 
 CLI_PATH = os.path.join(_HERE, "_lib", "qgemm_b200")
+
+
+# ----------------------------------------------------------------- Int64Word
+class Int64Word:
+    """The Int64Word backend (word.hpp:36-54) on the device: packed words are
+    uint64 (held bit for bit in int64 tensors), word products wrap modulo
+    2^64, plans may use beta up to 63. Same routines as the DoubleWord API."""
+
+    KINDS = {"rows_reversed": 0, "cols_forward": 1, "outer_cols": 2, "outer_rows": 3}
+
+    @staticmethod
+    def compress(x, plan: CompressionPlan, kind: str):
+        """compress_rows_reversed / cols_forward / outer_cols / outer_rows
+        (gemm.hpp:104-178) into uint64 words."""
+        torch = _torch()
+        _require_cuda(x)
+        rows, cols = x.shape
+        e = plan.e
+        shape = {"rows_reversed": (rows, -(-cols // e)), "cols_forward": (-(-rows // e), cols),
+                 "outer_cols": (rows, -(-cols // e)), "outer_rows": (-(-rows // e), cols)}[kind]
+        out = torch.empty(shape, dtype=torch.int64, device=x.device)
+        fn = {"rows_reversed": lib.qg_compress_rows_reversed_u64, "cols_forward": lib.qg_compress_cols_forward_u64,
+              "outer_cols": lib.qg_compress_outer_cols_u64, "outer_rows": lib.qg_compress_outer_rows_u64}[kind]
+        pl = plan._c()
+        _check(fn(ctypes.byref(pl), _ptr(x), _dtype_code(x), rows, cols, cols, _ptr(out), shape[1], _stream()))
+        return out
+
+    @staticmethod
+    def packed_common_product(ca, cb, plan: CompressionPlan):
+        torch = _torch()
+        m, groups = ca.shape
+        n = cb.shape[1]
+        acc = torch.empty((m, n), dtype=torch.int64, device=ca.device)
+        pl = plan._c()
+        _check(lib.qg_packed_common_product_u64(ctypes.byref(pl), _ptr(ca), _ptr(cb), m, n, groups, _ptr(acc),
+                                                _stream()))
+        return acc
+
+    @staticmethod
+    def reduce_common(acc, plan: CompressionPlan):
+        torch = _torch()
+        out = torch.empty(acc.shape, dtype=torch.int32, device=acc.device)
+        pl = plan._c()
+        _check(lib.qg_reduce_common_u64(ctypes.byref(pl), _ptr(acc), acc.numel(), _ptr(out), _stream()))
+        return out
+
+    @staticmethod
+    def extract_coefficients(words, plan: CompressionPlan):
+        torch = _torch()
+        out = torch.empty(words.shape, dtype=torch.int32, device=words.device)
+        pl = plan._c()
+        _check(lib.qg_extract_coefficients_u64(ctypes.byref(pl), _ptr(words), words.numel(), _ptr(out), _stream()))
+        return out
+
+    @staticmethod
+    def reduce_and_compress(words, plan: CompressionPlan):
+        torch = _torch()
+        rows, cols = words.shape
+        g = -(-cols // plan.e)
+        out = torch.empty((rows, g), dtype=torch.int64, device=words.device)
+        pl = plan._c()
+        _check(lib.qg_reduce_and_compress_u64(ctypes.byref(pl), _ptr(words), rows, cols, cols, _ptr(out), g, _stream()))
+        return out
+
+    @staticmethod
+    def redq_in_place(words, plan: CompressionPlan) -> None:
+        pl = plan._c()
+        _check(lib.qg_redq_u64(ctypes.byref(pl), _ptr(words), words.numel(), _stream()))
+
+    @staticmethod
+    def uncompress(words, plan: CompressionPlan, orientation: PackOrientation, logical_rows: int, logical_cols: int):
+        torch = _torch()
+        out = torch.empty((logical_rows, logical_cols), dtype=torch.int32, device=words.device)
+        pl = plan._c()
+        o = _Orientation(int(orientation.direction), int(orientation.axis), int(orientation.slots))
+        _check(lib.qg_uncompress_u64(ctypes.byref(pl), o, _ptr(words), words.shape[0], words.shape[1], logical_rows,
+                                     logical_cols, _ptr(out), _stream()))
+        return out
+
+    @staticmethod
+    def right_product(a, cbo, plan: CompressionPlan, n: int, redq: bool = True):
+        """packed_right_product / mul_right_compressed (gemm.hpp:285-325)."""
+        torch = _torch()
+        m, k = a.shape
+        H = cbo.shape[1]
+        cc = torch.empty((m, H), dtype=torch.int64, device=a.device)
+        fn = lib.qg_mul_right_u64 if redq else lib.qg_packed_right_product_u64
+        pl = plan._c()
+        _check(fn(ctypes.byref(pl), _ptr(a), _dtype_code(a), k, _ptr(cbo), m, k, n, _ptr(cc), _stream()))
+        return cc
+
+    @staticmethod
+    def left_product(ca, b, plan: CompressionPlan, m: int, redq: bool = True):
+        """packed_left_product / mul_left_compressed (gemm.hpp:340-371)."""
+        torch = _torch()
+        G, k = ca.shape
+        n = b.shape[1]
+        cc = torch.empty((G, n), dtype=torch.int64, device=b.device)
+        fn = lib.qg_mul_left_u64 if redq else lib.qg_packed_left_product_u64
+        pl = plan._c()
+        _check(fn(ctypes.byref(pl), _ptr(ca), _ptr(b), _dtype_code(b), n, m, k, n, _ptr(cc), _stream()))
+        return cc
+
+    @staticmethod
+    def mul_full_compressed(a, b, fp: FullPlan):
+        torch = _torch()
+        m, k = a.shape
+        n = b.shape[1]
+        c = torch.empty((m, n), dtype=torch.int32, device=a.device)
+        f = fp._c()
+        _check(lib.qg_mul_full_u64(ctypes.byref(f), _ptr(a), _dtype_code(a), _ptr(b), _dtype_code(b), m, k, n, _ptr(c),
+                                   n, _stream()))
+        return c
+
+    # host data (value semantics)
+    @staticmethod
+    def mul_common_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+        a, b = _host_u32(a), _host_u32(b)
+        m, k = a.shape
+        n = b.shape[1]
+        c = np.empty((m, n), dtype=np.uint32)
+        pl = plan._c()
+        _check(lib.qg_host_mul_common_i64(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p),
+                                          b.ctypes.data_as(ctypes.c_void_p), m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
+        return c
+
+    @staticmethod
+    def blocked_accumulate_host(a, b, plan: CompressionPlan, kpanel: int) -> np.ndarray:
+        a, b = _host_u32(a), _host_u32(b)
+        m, k = a.shape
+        n = b.shape[1]
+        c = np.empty((m, n), dtype=np.uint32)
+        pl = plan._c()
+        _check(lib.qg_host_blocked_accumulate_i64(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p),
+                                                  b.ctypes.data_as(ctypes.c_void_p), m, k, n, kpanel,
+                                                  c.ctypes.data_as(ctypes.c_void_p)))
+        return c
+
+    @staticmethod
+    def mul_right_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+        a, b = _host_u32(a), _host_u32(b)
+        m, k = a.shape
+        n = b.shape[1]
+        cc = np.empty((m, -(-n // plan.e)), dtype=np.uint64)
+        pl = plan._c()
+        _check(lib.qg_host_mul_right_i64(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p),
+                                         b.ctypes.data_as(ctypes.c_void_p), m, k, n, cc.ctypes.data_as(ctypes.c_void_p)))
+        return cc
+
+    @staticmethod
+    def mul_left_compressed_host(a, b, plan: CompressionPlan) -> np.ndarray:
+        a, b = _host_u32(a), _host_u32(b)
+        m, k = a.shape
+        n = b.shape[1]
+        cc = np.empty((-(-m // plan.e), n), dtype=np.uint64)
+        pl = plan._c()
+        _check(lib.qg_host_mul_left_i64(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p),
+                                        b.ctypes.data_as(ctypes.c_void_p), m, k, n, cc.ctypes.data_as(ctypes.c_void_p)))
+        return cc
+
+    @staticmethod
+    def mul_full_compressed_host(a, b, fp: FullPlan) -> np.ndarray:
+        a, b = _host_u32(a), _host_u32(b)
+        m, k = a.shape
+        n = b.shape[1]
+        c = np.empty((m, n), dtype=np.uint32)
+        f = fp._c()
+        _check(lib.qg_host_mul_full_i64(ctypes.byref(f), a.ctypes.data_as(ctypes.c_void_p),
+                                        b.ctypes.data_as(ctypes.c_void_p), m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
+        return c

@@ -1137,4 +1137,347 @@ void qg_last_phase_seconds(double* multiply, double* convert) {
   if (convert) *convert = g_phase.convert;
 }
 
+// ======================================================== Int64Word backend
+// word.hpp:36-54: uint64 words, products wrap mod 2^64, beta up to 63. The
+// entry points mirror the DoubleWord ones with uint64 word buffers.
+static int check_plan_i64(const qg_plan* plan) {
+  if (!plan) return QG_INVALID_ARGUMENT;
+  if (plan->p < 2 || !qg::is_prime(plan->p)) return QG_INVALID_MODULUS;
+  if (plan->beta > 63) return QG_PLAN_MISMATCH;  // check_backend<Int64Word>, pack.hpp:19-24
+  if (plan->t < 1 || plan->e < 1 || plan->d != plan->e - 1 || plan->t * plan->e > 63) return QG_PLAN_MISMATCH;
+  return QG_OK;
+}
+
+static int pack_u64(int kind, const qg_plan* plan, const void* src, qg_dtype dtype, size_t rows, size_t cols,
+                    size_t ld, uint64_t* out, size_t ldo, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  return cuda_status(qgk::launch_pack_u64(kind, src, dtype, rows, cols, ld, plan->t, plan->e, out, ldo, 0, 0,
+                                          as_stream(stream)));
+}
+
+int qg_compress_rows_reversed_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t m, size_t k, size_t lda,
+                                  uint64_t* ca, size_t ldca, void* stream) {
+  if (!plan) return QG_INVALID_ARGUMENT;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:106
+  if (lda < k || ldca < ceil_div(k, (size_t)plan->e)) return QG_INVALID_ARGUMENT;
+  return pack_u64(qgk::PACK_ROWS_REVERSED, plan, a, dtype, m, k, lda, ca, ldca, stream);
+}
+int qg_compress_cols_forward_u64(const qg_plan* plan, const void* b, qg_dtype dtype, size_t k, size_t n, size_t ldb,
+                                 uint64_t* cb, size_t ldcb, void* stream) {
+  if (plan && k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:125
+  if (ldb < n || ldcb < n) return QG_INVALID_ARGUMENT;
+  return pack_u64(qgk::PACK_COLS_FORWARD, plan, b, dtype, k, n, ldb, cb, ldcb, stream);
+}
+int qg_compress_outer_cols_u64(const qg_plan* plan, const void* b, qg_dtype dtype, size_t rows, size_t cols,
+                               size_t ldb, uint64_t* out, size_t ldo, void* stream) {
+  if (ldb < cols || ldo < ceil_div(cols, (size_t)(plan ? plan->e : 1))) return QG_INVALID_ARGUMENT;
+  return pack_u64(qgk::PACK_OUTER_COLS, plan, b, dtype, rows, cols, ldb, out, ldo, stream);
+}
+int qg_compress_outer_rows_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t rows, size_t cols,
+                               size_t lda, uint64_t* out, size_t ldo, void* stream) {
+  if (lda < cols || ldo < cols) return QG_INVALID_ARGUMENT;
+  return pack_u64(qgk::PACK_OUTER_ROWS, plan, a, dtype, rows, cols, lda, out, ldo, stream);
+}
+
+// packed_common_product<Int64Word>, gemm.hpp:210-244: acc = sum of high parts.
+int qg_packed_common_product_u64(const qg_plan* plan, const uint64_t* ca, const uint64_t* cb, size_t m, size_t n,
+                                 size_t groups, uint64_t* acc, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  const uint64_t mask = (1ull << plan->t) - 1;
+  return cuda_status(qgk::launch_gemm_u64(0, ca, -1, groups, cb, -1, n, m, n, groups, plan->t * plan->d, mask, acc, n,
+                                          as_stream(stream)));
+}
+// reduce_common_entry<Int64Word>, gemm.hpp:247-250
+int qg_reduce_common_u64(const qg_plan* plan, const uint64_t* acc, size_t count, int32_t* c, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  return cuda_status(qgk::launch_word_reduce_u64(acc, count, 0, 0, (1ull << plan->t) - 1, plan->p, c, 0,
+                                                 as_stream(stream)));
+}
+// extract_coefficient<Int64Word>, pack.hpp:96-98
+int qg_extract_coefficients_u64(const qg_plan* plan, const uint64_t* words, size_t count, int32_t* out, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  return cuda_status(qgk::launch_word_reduce_u64(words, count, 1, plan->t * plan->d, (1ull << plan->t) - 1, plan->p,
+                                                 out, 0, as_stream(stream)));
+}
+int qg_reduce_and_compress_u64(const qg_plan* plan, const uint64_t* words, size_t rows, size_t cols, size_t ldw,
+                               uint64_t* out, size_t ldo, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if (ldw < cols || ldo < ceil_div(cols, (size_t)plan->e)) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_reduce_and_compress_u64(words, rows, cols, ldw, plan->t, plan->d, plan->e, plan->p,
+                                                         out, ldo, as_stream(stream)));
+}
+// redq_in_place<Int64Word>, gemm.hpp:313-316
+int qg_redq_u64(const qg_plan* plan, uint64_t* words, size_t count, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  DeviceFlag flag(s);
+  if (!flag.ptr) return QG_CUDA_ERROR;
+  if ((st = cuda_status(qgk::launch_redq_u64(words, count, plan->t, plan->e, plan->p, flag.ptr, s)))) return st;
+  int over = 0;
+  if ((st = flag.read(&over))) return st;
+  return over ? QG_DIGIT_OVERFLOW : QG_OK;
+}
+// uncompress<Int64Word>, gemm.hpp:182-204
+int qg_uncompress_u64(const qg_plan* plan, qg_orientation o, const uint64_t* words, size_t stored_rows,
+                      size_t stored_cols, size_t logical_rows, size_t logical_cols, int32_t* out, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if (o.slots < 1 || o.slots > plan->e) return QG_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  DeviceFlag flag(s);
+  if (!flag.ptr) return QG_CUDA_ERROR;
+  if ((st = cuda_status(qgk::launch_uncompress_u64(words, stored_rows, stored_cols, logical_rows, logical_cols,
+                                                   plan->t, plan->e, o.slots, o.direction == 1, o.axis == 1,
+                                                   plan->p, out, flag.ptr, s))))
+    return st;
+  int over = 0;
+  if ((st = flag.read(&over))) return st;
+  return over ? QG_DIGIT_OVERFLOW : QG_OK;
+}
+// packed_right_product<Int64Word> (gemm.hpp:285-310) and + REDQ (:320-325)
+int qg_packed_right_product_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t lda, const uint64_t* cbo,
+                                size_t m, size_t k, size_t n, uint64_t* cc, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295
+  if (lda < k) return QG_INVALID_ARGUMENT;
+  const size_t H = ceil_div(n, (size_t)plan->e);
+  if (k == 0) return m * H ? cuda_status(cudaMemsetAsync(cc, 0, m * H * 8, as_stream(stream))) : QG_OK;
+  return cuda_status(qgk::launch_gemm_u64(1, a, dtype, lda, cbo, -1, H, m, H, k, 0, 0, cc, H, as_stream(stream)));
+}
+int qg_mul_right_u64(const qg_plan* plan, const void* a, qg_dtype dtype, size_t lda, const uint64_t* cbo, size_t m,
+                     size_t k, size_t n, uint64_t* cc, void* stream) {
+  int st = qg_packed_right_product_u64(plan, a, dtype, lda, cbo, m, k, n, cc, stream);
+  if (st) return st;
+  return qg_redq_u64(plan, cc, m * ceil_div(n, (size_t)plan->e), stream);
+}
+// packed_left_product<Int64Word> (gemm.hpp:340-364) and + REDQ (:366-371)
+int qg_packed_left_product_u64(const qg_plan* plan, const uint64_t* ca, const void* b, qg_dtype dtype, size_t ldb,
+                               size_t m, size_t k, size_t n, uint64_t* cc, void* stream) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:349
+  if (ldb < n) return QG_INVALID_ARGUMENT;
+  const size_t G = ceil_div(m, (size_t)plan->e);
+  if (k == 0) return G * n ? cuda_status(cudaMemsetAsync(cc, 0, G * n * 8, as_stream(stream))) : QG_OK;
+  return cuda_status(qgk::launch_gemm_u64(1, ca, -1, k, b, dtype, ldb, G, n, k, 0, 0, cc, n, as_stream(stream)));
+}
+int qg_mul_left_u64(const qg_plan* plan, const uint64_t* ca, const void* b, qg_dtype dtype, size_t ldb, size_t m,
+                    size_t k, size_t n, uint64_t* cc, void* stream) {
+  int st = qg_packed_left_product_u64(plan, ca, b, dtype, ldb, m, k, n, cc, stream);
+  if (st) return st;
+  return qg_redq_u64(plan, cc, ceil_div(m, (size_t)plan->e) * n, stream);
+}
+// mul_full_compressed<Int64Word>, gemm.hpp:377-445, on device residues.
+int qg_mul_full_u64(const qg_full_plan* fp, const void* a, qg_dtype adt, const void* b, qg_dtype bdt, size_t m,
+                    size_t k, size_t n, int32_t* c, size_t ldc, void* stream) {
+  if (!fp) return QG_INVALID_ARGUMENT;
+  int st = check_plan_i64(&fp->base);
+  if (st) return st;
+  if ((st = check_dtype(adt)) || (st = check_dtype(bdt))) return st;
+  const int qs = fp->dq + 1, ts = fp->dtheta + 1;
+  if (qs < 1 || ts < 1 || fp->base.e != qs * ts || fp->theta_exponent != fp->base.t * qs) return QG_PLAN_MISMATCH;
+  if (k > fp->base.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:384
+  if (ldc < n) return QG_INVALID_ARGUMENT;
+  if (m * n == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  const size_t G = ceil_div(m, (size_t)qs), H = ceil_div(n, (size_t)ts);
+  DevBuf ma(s), mb(s), acc(s);
+  QG_TRY(ma.alloc(G * k * 8));
+  QG_TRY(mb.alloc(k * H * 8));
+  QG_TRY(acc.alloc(G * H * 8));
+  if (k) {
+    QG_TRY(qgk::launch_pack_u64(qgk::PACK_OUTER_ROWS, a, adt, m, k, k, fp->base.t, qs, (uint64_t*)ma.p, k, 0, 0, s));
+    QG_TRY(qgk::launch_pack_u64(qgk::PACK_OUTER_COLS, b, bdt, k, n, n, fp->theta_exponent, ts, (uint64_t*)mb.p, H, 0,
+                                0, s));
+    QG_TRY(qgk::launch_gemm_u64(1, ma.p, -1, k, mb.p, -1, H, G, H, k, 0, 0, (uint64_t*)acc.p, H, s));
+  } else {
+    QG_TRY(cudaMemsetAsync(acc.p, 0, G * H * 8, s));
+  }
+  return cuda_status(qgk::launch_uncompress_full_u64((const uint64_t*)acc.p, H, m, n, fp->base.t, qs, ts, fp->base.p,
+                                                     c, ldc, s));
+}
+
+// ---- host-data entries of the Int64Word backend (value semantics)
+int qg_host_mul_common_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                           uint32_t* c) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:106
+  if (m * n == 0) return QG_OK;
+  cudaStream_t s = nullptr;
+  PhaseScope ps;
+  const size_t K = ceil_div(k, (size_t)plan->e);
+  DevBuf da(s), db(s), dca(s), dcb(s), dacc(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dca.alloc(m * K * 8));
+  QG_TRY(dcb.alloc(K * n * 8));
+  QG_TRY(dacc.alloc(m * n * 8));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  if (K) {
+    QG_TRY(qgk::launch_pack_u64(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, plan->t, plan->e, (uint64_t*)dca.p, K,
+                                0, 0, s));
+    QG_TRY(qgk::launch_pack_u64(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, plan->t, plan->e, (uint64_t*)dcb.p, n,
+                                0, 0, s));
+  }
+  ps.begin(s);
+  if (K) {
+    if ((st = qg_packed_common_product_u64(plan, (const uint64_t*)dca.p, (const uint64_t*)dcb.p, m, n, K,
+                                           (uint64_t*)dacc.p, s)))
+      return st;
+  } else {
+    QG_TRY(cudaMemsetAsync(dacc.p, 0, m * n * 8, s));
+  }
+  ps.end(s);
+  if ((st = qg_reduce_common_u64(plan, (const uint64_t*)dacc.p, m * n, (int32_t*)dc.p, s))) return st;
+  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
+  return QG_OK;
+}
+
+int qg_host_blocked_accumulate_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                                   size_t n, size_t kpanel, uint32_t* c) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if (kpanel < 1) return QG_INVALID_ARGUMENT;        // gemm.hpp:455
+  if (kpanel > plan->kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:456
+  if (m * n == 0) return QG_OK;
+  cudaStream_t s = nullptr;
+  PhaseScope ps;
+  const size_t Kp = ceil_div(kpanel, (size_t)plan->e);
+  DevBuf da(s), db(s), dca(s), dcb(s), dacc(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dca.alloc(m * Kp * 8));
+  QG_TRY(dcb.alloc(Kp * n * 8));
+  QG_TRY(dacc.alloc(m * n * 8));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  QG_TRY(cudaMemsetAsync(dc.p, 0, m * n * 4, s));
+  // one panel at a time (gemm.hpp:460-487): pack, common product, reduce, add mod p
+  for (size_t k0 = 0; k0 < k; k0 += kpanel) {
+    const size_t len = k - k0 < kpanel ? k - k0 : kpanel;
+    const size_t W = ceil_div(len, (size_t)plan->e);
+    QG_TRY(qgk::launch_pack_u64(qgk::PACK_ROWS_REVERSED, (const uint32_t*)da.p + k0, QG_U32, m, len, k, plan->t,
+                                plan->e, (uint64_t*)dca.p, W, 0, 0, s));
+    QG_TRY(qgk::launch_pack_u64(qgk::PACK_COLS_FORWARD, (const uint32_t*)db.p + k0 * n, QG_U32, len, n, n, plan->t,
+                                plan->e, (uint64_t*)dcb.p, n, 0, 0, s));
+    ps.begin(s);
+    QG_TRY(qgk::launch_gemm_u64(0, dca.p, -1, W, dcb.p, -1, n, m, n, W, plan->t * plan->d, (1ull << plan->t) - 1,
+                                (uint64_t*)dacc.p, n, s));
+    ps.end(s);
+    QG_TRY(qgk::launch_word_reduce_u64((const uint64_t*)dacc.p, m * n, 0, 0, (1ull << plan->t) - 1, plan->p,
+                                       (int32_t*)dc.p, 1, s));
+  }
+  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
+  return QG_OK;
+}
+
+static int host_right_left_i64(bool left, const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
+                               size_t k, size_t n, uint64_t* cc) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;
+  const size_t e = plan->e;
+  const size_t rows = left ? ceil_div(m, e) : m, cols = left ? n : ceil_div(n, e);
+  if (rows * cols == 0) return QG_OK;
+  cudaStream_t s = nullptr;
+  PhaseScope ps;
+  DevBuf da(s), db(s), dw(s), dcc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dw.alloc((left ? ceil_div(m, e) * k : k * ceil_div(n, e)) * 8));
+  QG_TRY(dcc.alloc(rows * cols * 8));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  if (left) {
+    if (k) QG_TRY(qgk::launch_pack_u64(qgk::PACK_OUTER_ROWS, da.p, QG_U32, m, k, k, plan->t, plan->e,
+                                       (uint64_t*)dw.p, k, 0, 0, s));
+    ps.begin(s);
+    if ((st = qg_packed_left_product_u64(plan, (const uint64_t*)dw.p, db.p, QG_U32, n, m, k, n, (uint64_t*)dcc.p, s)))
+      return st;
+    ps.end(s);
+  } else {
+    if (k) QG_TRY(qgk::launch_pack_u64(qgk::PACK_OUTER_COLS, db.p, QG_U32, k, n, n, plan->t, plan->e,
+                                       (uint64_t*)dw.p, ceil_div(n, e), 0, 0, s));
+    ps.begin(s);
+    if ((st = qg_packed_right_product_u64(plan, da.p, QG_U32, k, (const uint64_t*)dw.p, m, k, n, (uint64_t*)dcc.p, s)))
+      return st;
+    ps.end(s);
+  }
+  if ((st = qg_redq_u64(plan, (uint64_t*)dcc.p, rows * cols, s))) return st;
+  QG_TRY(cudaMemcpyAsync(cc, dcc.p, rows * cols * 8, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
+  return QG_OK;
+}
+
+int qg_host_mul_right_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                          uint64_t* cc) {
+  return host_right_left_i64(false, plan, a, b, m, k, n, cc);
+}
+int qg_host_mul_left_i64(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                         uint64_t* cc) {
+  return host_right_left_i64(true, plan, a, b, m, k, n, cc);
+}
+
+int qg_host_uncompress_u64(const qg_plan* plan, qg_orientation o, const uint64_t* words, size_t stored_rows,
+                           size_t stored_cols, size_t logical_rows, size_t logical_cols, uint32_t* out) {
+  int st = check_plan_i64(plan);
+  if (st) return st;
+  cudaStream_t s = nullptr;
+  DevBuf dw(s), dout(s);
+  QG_TRY(dw.alloc(stored_rows * stored_cols * 8));
+  QG_TRY(dout.alloc(logical_rows * logical_cols * 4));
+  if (stored_rows * stored_cols)
+    QG_TRY(cudaMemcpyAsync(dw.p, words, stored_rows * stored_cols * 8, cudaMemcpyHostToDevice, s));
+  if ((st = qg_uncompress_u64(plan, o, (const uint64_t*)dw.p, stored_rows, stored_cols, logical_rows, logical_cols,
+                              (int32_t*)dout.p, s)))
+    return st;
+  if (logical_rows * logical_cols)
+    QG_TRY(cudaMemcpyAsync(out, dout.p, logical_rows * logical_cols * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  return QG_OK;
+}
+
+int qg_host_mul_full_i64(const qg_full_plan* fp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
+                         uint32_t* c) {
+  if (!fp) return QG_INVALID_ARGUMENT;
+  int st = check_plan_i64(&fp->base);
+  if (st) return st;
+  if (k > fp->base.kmax) return QG_PLAN_MISMATCH;
+  if (m * n == 0) return QG_OK;
+  cudaStream_t s = nullptr;
+  PhaseScope ps;
+  DevBuf da(s), db(s), dc(s);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dc.alloc(m * n * 4));
+  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+  ps.begin(s);
+  if ((st = qg_mul_full_u64(fp, da.p, QG_U32, db.p, QG_U32, m, k, n, (int32_t*)dc.p, n, s))) return st;
+  ps.end(s);
+  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
+  QG_TRY(cudaStreamSynchronize(s));
+  ps.finish();
+  return QG_OK;
+}
+
 }  // extern "C"

@@ -16,6 +16,22 @@ cudaError_t launch_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t r
 cudaError_t launch_pack(int kind, const void* src, int dtype, size_t rows, size_t cols, size_t ld,
                         int t, int e, double* dst, size_t ldd, size_t panel_len,
                         size_t panel_words, cudaStream_t s);
+cudaError_t launch_pack_u64(int kind, const void* src, int dtype, size_t rows, size_t cols, size_t ld, int t, int e,
+                            uint64_t* dst, size_t ldd, size_t panel_len, size_t panel_words, cudaStream_t s);
+// Int64Word backend (qg_word64.cu); a_dtype / b_dtype -1 = uint64 words
+cudaError_t launch_gemm_u64(int mode, const void* a, int a_dtype, size_t lda, const void* b, int b_dtype, size_t ldb,
+                            size_t M, size_t N, size_t K, int sh, uint64_t mask, uint64_t* d, size_t ldd,
+                            cudaStream_t s);
+cudaError_t launch_word_reduce_u64(const uint64_t* w, size_t count, int op, int shift, uint64_t mask, uint32_t p,
+                                   int32_t* out, int accumulate, cudaStream_t s);
+cudaError_t launch_redq_u64(uint64_t* w, size_t count, int t, int e, uint32_t p, int* overflow, cudaStream_t s);
+cudaError_t launch_uncompress_u64(const uint64_t* w, size_t srows, size_t scols, size_t lrows, size_t lcols, int t,
+                                  int e, int slots, int reversed, int column_axis, uint32_t p, int32_t* out,
+                                  int* overflow, cudaStream_t s);
+cudaError_t launch_reduce_and_compress_u64(const uint64_t* w, size_t rows, size_t cols, size_t ldw, int t, int d, int e,
+                                           uint32_t p, uint64_t* out, size_t ldo, cudaStream_t s);
+cudaError_t launch_uncompress_full_u64(const uint64_t* cc, size_t ldcc, size_t m, size_t n, int t, int qs, int ts,
+                                       uint32_t p, int32_t* c, size_t ldc, cudaStream_t s);
 cudaError_t launch_redq(double* w, size_t count, int t, int e, uint32_t p, int* overflow,
                         cudaStream_t s);
 cudaError_t launch_uncompress(const double* w, size_t srows, size_t scols, size_t lrows,

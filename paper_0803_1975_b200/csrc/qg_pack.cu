@@ -40,12 +40,17 @@ struct Panels {
   }
 };
 
+// A packed word in the backend's representation: DoubleWord (an exact double)
+// or Int64Word (the uint64 itself), word.hpp:10-54.
+__device__ __forceinline__ void store_word(double* p, uint64_t r) { *p = __ull2double_rn(r); }
+__device__ __forceinline__ void store_word(uint64_t* p, uint64_t r) { *p = r; }
+
 // K1: compress_rows_reversed, gemm.hpp:104-118 + compress_reverse,
 // pack.hpp:59-70. Word (i, g) = sum_s a[i][g e + s] Q^(d - s); a short final
 // group is shifted up by Q^(e - len).
-template <typename TIn>
+template <typename TIn, typename TOut>
 __global__ void k_pack_rows_reversed(const TIn* __restrict__ a, size_t m, size_t lda, int t, int e,
-                                     Panels pn, double* __restrict__ ca, size_t ldca) {
+                                     Panels pn, TOut* __restrict__ ca, size_t ldca) {
   const unsigned W = pn.panel_words * pn.npanels;
   for (size_t i = blockIdx.y; i < m; i += gridDim.y) {
     const TIn* row = a + i * lda;
@@ -57,7 +62,7 @@ __global__ void k_pack_rows_reversed(const TIn* __restrict__ a, size_t m, size_t
         for (int s = 0; s < len; ++s) r = (r << t) | residue_bits(row[base + s]);
         r <<= t * (e - len);
       }
-      ca[i * ldca + g] = __ull2double_rn(r);
+      store_word(ca + i * ldca + g, r);
     }
   }
 }
@@ -65,9 +70,9 @@ __global__ void k_pack_rows_reversed(const TIn* __restrict__ a, size_t m, size_t
 // K2: compress_cols_forward, gemm.hpp:122-140 + compress_forward,
 // pack.hpp:47-54. Word (g, j) = sum_s b[g e + s][j] Q^s; lanes run along j so
 // every load and store is coalesced.
-template <typename TIn>
+template <typename TIn, typename TOut>
 __global__ void k_pack_cols_forward(const TIn* __restrict__ b, size_t n, size_t ldb, int t, int e,
-                                    Panels pn, double* __restrict__ cb, size_t ldcb) {
+                                    Panels pn, TOut* __restrict__ cb, size_t ldcb) {
   const unsigned W = pn.panel_words * pn.npanels;
   for (unsigned g = blockIdx.y; g < W; g += gridDim.y) {
     size_t base;
@@ -78,15 +83,15 @@ __global__ void k_pack_cols_forward(const TIn* __restrict__ b, size_t n, size_t 
       uint64_t r = 0;
       if (live)
         for (int s = len - 1; s >= 0; --s) r = (r << t) | residue_bits(b[(base + s) * ldb + j]);
-      cb[g * ldcb + j] = __ull2double_rn(r);
+      store_word(cb + g * ldcb + j, r);
     }
   }
 }
 
 // K3: compress_outer_cols, gemm.hpp:145-158: word (i, h) = sum_s b[i][h e + s] Q^s.
-template <typename TIn>
+template <typename TIn, typename TOut>
 __global__ void k_pack_outer_cols(const TIn* __restrict__ b, size_t rows, size_t cols, size_t ldb,
-                                  int t, int e, double* __restrict__ cb, size_t ldcb) {
+                                  int t, int e, TOut* __restrict__ cb, size_t ldcb) {
   const size_t H = (cols + e - 1) / e;
   for (size_t i = blockIdx.y; i < rows; i += gridDim.y) {
     const TIn* row = b + i * ldb;
@@ -96,7 +101,7 @@ __global__ void k_pack_outer_cols(const TIn* __restrict__ b, size_t rows, size_t
       const int len = (int)((cols - base) < (size_t)e ? (cols - base) : (size_t)e);
       uint64_t r = 0;
       for (int s = len - 1; s >= 0; --s) r = (r << t) | residue_bits(row[base + s]);
-      cb[i * ldcb + h] = __ull2double_rn(r);
+      store_word(cb + i * ldcb + h, r);
     }
   }
 }
@@ -530,32 +535,32 @@ cudaError_t launch_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t r
   return cudaGetLastError();
 }
 
-template <typename TIn>
+template <typename TIn, typename TOut>
 static cudaError_t pack_dispatch(int kind, const TIn* src, size_t rows, size_t cols, size_t ld,
-                                 int t, int e, double* dst, size_t ldd, size_t panel_len,
+                                 int t, int e, TOut* dst, size_t ldd, size_t panel_len,
                                  size_t panel_words, cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
   switch (kind) {
     case PACK_ROWS_REVERSED: {  // common dimension = cols
       const Panels pn = make_panels(cols, e, panel_len, panel_words);
-      k_pack_rows_reversed<TIn><<<grid2d((size_t)pn.panel_words * pn.npanels, rows, 128), 128, 0, s>>>(
+      k_pack_rows_reversed<TIn, TOut><<<grid2d((size_t)pn.panel_words * pn.npanels, rows, 128), 128, 0, s>>>(
           src, rows, ld, t, e, pn, dst, ldd);
       break;
     }
     case PACK_COLS_FORWARD: {  // common dimension = rows
       const Panels pn = make_panels(rows, e, panel_len, panel_words);
-      k_pack_cols_forward<TIn><<<grid2d(cols, (size_t)pn.panel_words * pn.npanels, 128), 128, 0, s>>>(
+      k_pack_cols_forward<TIn, TOut><<<grid2d(cols, (size_t)pn.panel_words * pn.npanels, 128), 128, 0, s>>>(
           src, cols, ld, t, e, pn, dst, ldd);
       break;
     }
     case PACK_OUTER_COLS: {
       const size_t H = (cols + e - 1) / e;
-      k_pack_outer_cols<TIn><<<grid2d(H, rows, 128), 128, 0, s>>>(src, rows, cols, ld, t, e, dst, ldd);
+      k_pack_outer_cols<TIn, TOut><<<grid2d(H, rows, 128), 128, 0, s>>>(src, rows, cols, ld, t, e, dst, ldd);
       break;
     }
     case PACK_OUTER_ROWS: {  // compress_outer_rows, gemm.hpp:161-178: forward words down columns
       const Panels pn = make_panels(rows, e, rows, 0);
-      k_pack_cols_forward<TIn><<<grid2d(cols, (size_t)pn.panel_words, 128), 128, 0, s>>>(
+      k_pack_cols_forward<TIn, TOut><<<grid2d(cols, (size_t)pn.panel_words, 128), 128, 0, s>>>(
           src, cols, ld, t, e, pn, dst, ldd);
       break;
     }
@@ -567,6 +572,16 @@ static cudaError_t pack_dispatch(int kind, const TIn* src, size_t rows, size_t c
 cudaError_t launch_pack(int kind, const void* src, int dtype, size_t rows, size_t cols, size_t ld,
                         int t, int e, double* dst, size_t ldd, size_t panel_len,
                         size_t panel_words, cudaStream_t s) {
+  switch (dtype) {
+    case 0: return pack_dispatch<double>(kind, (const double*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
+    case 1: return pack_dispatch<uint32_t>(kind, (const uint32_t*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
+    default: return pack_dispatch<int32_t>(kind, (const int32_t*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
+  }
+}
+
+// The same four packings into Int64Word (uint64) words.
+cudaError_t launch_pack_u64(int kind, const void* src, int dtype, size_t rows, size_t cols, size_t ld, int t, int e,
+                            uint64_t* dst, size_t ldd, size_t panel_len, size_t panel_words, cudaStream_t s) {
   switch (dtype) {
     case 0: return pack_dispatch<double>(kind, (const double*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);
     case 1: return pack_dispatch<uint32_t>(kind, (const uint32_t*)src, rows, cols, ld, t, e, dst, ldd, panel_len, panel_words, s);

@@ -4,9 +4,9 @@
 // subcommands, options, output text and exit codes:
 //   0 success, 1 verification failure, 2 usage or parse error, 3 plan infeasible.
 // Every product runs through libqgemm_b200 (sm_100a kernels); the checker of
-// `verify` is the library's plain naive_gemm kernel. Int64Word (--bits 54..63)
-// has no GPU backend: such runs use the DoubleWord path with beta = 53 plans
-// (identical C; `plan` still prints the requested-beta plan).
+// `verify` is the library's plain naive_gemm kernel. --bits up to 53 runs the
+// DoubleWord backend (FP64 tensor cores), 54..63 the Int64Word backend (uint64
+// words, integer pipes), as qgemm_main.cpp:253-266 does.
 #include <cerrno>
 #include <chrono>
 #include <cstdint>
@@ -163,9 +163,10 @@ int cmd_plan(const Options& o) {  // qgemm_main.cpp:66-97
 }
 
 // One algorithm on host matrices, with the plans the reference chooses for it
-// in `gemm` and `verify` (qgemm_main.cpp:118-145, verify.hpp:29-68).
+// in `gemm` and `verify` (qgemm_main.cpp:118-145, verify.hpp:29-68), on the
+// DoubleWord (i64 = false) or the Int64Word backend.
 ResidueMatrix run_algorithm(Algorithm algo, const ResidueMatrix& a, const ResidueMatrix& b, std::uint32_t p,
-                            int beta, std::uint64_t kpanel, bool verify_mode) {
+                            int beta, std::uint64_t kpanel, bool verify_mode, bool i64) {
   const std::uint64_t k = a.cols;
   switch (algo) {
     case Algorithm::Naive:
@@ -178,14 +179,19 @@ ResidueMatrix run_algorithm(Algorithm algo, const ResidueMatrix& a, const Residu
         if (!verify_mode || k > 1) throw;
         plan = uncompressed_plan(p, k, beta);  // verify.hpp:37-44
       }
-      return mul_common_compressed(a, b, plan);
+      return i64 ? mul_common_compressed<Int64Word>(a, b, plan) : mul_common_compressed(a, b, plan);
     }
-    case Algorithm::RightCompressed:
-      return uncompress(mul_right_compressed(a, b, plan_packed_axis(p, k, b.cols, beta)));
-    case Algorithm::LeftCompressed:
-      return uncompress(mul_left_compressed(a, b, plan_packed_axis(p, k, a.rows, beta)));
+    case Algorithm::RightCompressed: {
+      const CompressionPlan plan = plan_packed_axis(p, k, b.cols, beta);
+      return i64 ? uncompress(mul_right_compressed_i64(a, b, plan)) : uncompress(mul_right_compressed(a, b, plan));
+    }
+    case Algorithm::LeftCompressed: {
+      const CompressionPlan plan = plan_packed_axis(p, k, a.rows, beta);
+      return i64 ? uncompress(mul_left_compressed_i64(a, b, plan)) : uncompress(mul_left_compressed(a, b, plan));
+    }
     case Algorithm::FullCompressed:
-      return mul_full_compressed(a, b, plan_full(p, k, beta));
+      return i64 ? mul_full_compressed<Int64Word>(a, b, plan_full(p, k, beta))
+                 : mul_full_compressed(a, b, plan_full(p, k, beta));
     case Algorithm::Blocked: {
       std::uint64_t kp;
       if (verify_mode) {
@@ -195,15 +201,16 @@ ResidueMatrix run_algorithm(Algorithm algo, const ResidueMatrix& a, const Residu
         if (kp == 0) kp = k;
       }
       const CompressionPlan plan = kp >= 2 ? plan_compression(p, kp, beta) : uncompressed_plan(p, 1, beta);
-      return blocked_accumulate(a, b, plan, kp);
+      return i64 ? blocked_accumulate<Int64Word>(a, b, plan, kp) : blocked_accumulate(a, b, plan, kp);
     }
   }
   throw std::invalid_argument("unknown algorithm");
 }
 
-int effective_bits(int bits) {
+// qgemm_main.cpp:253-266: the word backend follows --bits
+bool backend_i64(int bits) {
   if (bits > 63) throw std::invalid_argument("--bits must be at most 63");
-  return bits <= kDoubleBits ? bits : kDoubleBits;
+  return bits > kDoubleBits;
 }
 
 int cmd_gemm(const Options& o) {  // qgemm_main.cpp:99-148
@@ -212,7 +219,8 @@ int cmd_gemm(const Options& o) {  // qgemm_main.cpp:99-148
     if (!o.has(req)) throw UsageError(std::string("--") + req + " is required");
   const std::string a_path = o.values.at("a"), b_path = o.values.at("b"), out_path = o.values.at("out");
   const auto want_p = number<std::uint32_t>(o, "p", 0, false);
-  const int beta = effective_bits(number<int>(o, "bits", 53, false));
+  const int beta = number<int>(o, "bits", 53, false);
+  const bool i64 = backend_i64(beta);
   const auto kpanel = number<std::uint64_t>(o, "kpanel", 0, false);
   const MatrixFile fa = read_matrix_file(a_path);
   const MatrixFile fb = read_matrix_file(b_path);
@@ -229,7 +237,7 @@ int cmd_gemm(const Options& o) {  // qgemm_main.cpp:99-148
                             std::to_string(a.cols) + ", " + b_path + " is " + std::to_string(b.rows) + "x" +
                             std::to_string(b.cols));
   const Algorithm algo = parse_algorithm(o.values.at("algo"));
-  const ResidueMatrix c = run_algorithm(algo, a, b, fa.p, beta, kpanel, false);
+  const ResidueMatrix c = run_algorithm(algo, a, b, fa.p, beta, kpanel, false, i64);
   write_matrix_file(out_path, c, fa.p);
   return kExitOk;
 }
@@ -238,12 +246,19 @@ int cmd_verify(const Options& o) {  // qgemm_main.cpp:150-170, verify.hpp:70-140
   const auto p = number<std::uint32_t>(o, "p", 0, true);
   const auto max_dim = number<std::uint64_t>(o, "max-dim", 32, false);
   const auto seeds = number<std::uint64_t>(o, "seeds", 100, false);
-  const int beta = effective_bits(number<int>(o, "bits", 53, false));
+  const int beta = number<int>(o, "bits", 53, false);
+  if (beta > 63) throw std::invalid_argument("--bits must be at most 63");
   check_modulus(p);
   if (max_dim < 1) throw std::invalid_argument("--max-dim must be >= 1");
+  // verify.hpp:128-137: both word backends, DoubleWord at min(beta, 53),
+  // Int64Word at 63 unless a wider beta was asked for
+  const int beta_double = beta < kDoubleBits ? beta : kDoubleBits;
+  const int beta_int = beta <= kDoubleBits ? 63 : beta;
   bool all_ok = true;
   for (Algorithm algo : {Algorithm::CommonCompressed, Algorithm::RightCompressed, Algorithm::LeftCompressed,
-                         Algorithm::FullCompressed, Algorithm::Blocked}) {
+                         Algorithm::FullCompressed, Algorithm::Blocked})
+  for (const bool i64 : {false, true}) {
+    const int bb = i64 ? beta_int : beta_double;
     std::size_t cases = 0, skipped = 0;
     bool passed = true;
     std::string detail;
@@ -256,7 +271,7 @@ int cmd_verify(const Options& o) {  // qgemm_main.cpp:150-170, verify.hpp:70-140
       const ResidueMatrix b = random_residue_matrix(k, n, p, seed * 2 + 2);
       ResidueMatrix got;
       try {
-        got = run_algorithm(algo, a, b, p, beta, 0, true);
+        got = run_algorithm(algo, a, b, p, bb, 0, true, i64);
       } catch (const NoCompression&) {
         ++skipped;
         continue;
@@ -274,7 +289,7 @@ int cmd_verify(const Options& o) {  // qgemm_main.cpp:150-170, verify.hpp:70-140
                        std::to_string(want.at(i, j));
       }
     }
-    std::cout << algorithm_name(algo) << "\tdouble\t";
+    std::cout << algorithm_name(algo) << "\t" << (i64 ? "int64" : "double") << "\t";
     if (passed) {
       std::cout << "ok (" << cases << " cases";
       if (skipped) std::cout << ", " << skipped << " skipped";
@@ -295,7 +310,8 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
   if (!o.has("algo")) throw UsageError("--algo is required");
   const int reps = number<int>(o, "reps", 1, false);
   const auto seed = number<std::uint64_t>(o, "seed", 0, false);
-  const int beta = effective_bits(number<int>(o, "bits", 53, false));
+  const int beta = number<int>(o, "bits", 53, false);
+  const bool i64 = backend_i64(beta);
   const auto kpanel = number<std::uint64_t>(o, "kpanel", 0, false);
   check_modulus(p);
   const Algorithm algo = parse_algorithm(o.values.at("algo"));
@@ -320,7 +336,7 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
         const CompressionPlan plan = plan_compression(p, k, beta);
         rec.t = plan.t();
         rec.e = plan.e();
-        c = mul_common_compressed(a, b, plan);
+        c = i64 ? mul_common_compressed<Int64Word>(a, b, plan) : mul_common_compressed(a, b, plan);
         break;
       }
       case Algorithm::RightCompressed:
@@ -328,11 +344,21 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
         const CompressionPlan plan = plan_compression(p, k, beta);
         rec.t = plan.t();
         rec.e = plan.e();
-        const CompressedWords cc = algo == Algorithm::RightCompressed ? mul_right_compressed(a, b, plan)
-                                                                      : mul_left_compressed(a, b, plan);
-        const PhaseSeconds ph = last_phase_seconds();
-        const auto t0 = std::chrono::steady_clock::now();
-        c = uncompress(cc);
+        PhaseSeconds ph;
+        std::chrono::steady_clock::time_point t0;
+        if (i64) {
+          const CompressedWords64 cc = algo == Algorithm::RightCompressed ? mul_right_compressed_i64(a, b, plan)
+                                                                          : mul_left_compressed_i64(a, b, plan);
+          ph = last_phase_seconds();
+          t0 = std::chrono::steady_clock::now();
+          c = uncompress(cc);
+        } else {
+          const CompressedWords cc = algo == Algorithm::RightCompressed ? mul_right_compressed(a, b, plan)
+                                                                        : mul_left_compressed(a, b, plan);
+          ph = last_phase_seconds();
+          t0 = std::chrono::steady_clock::now();
+          c = uncompress(cc);
+        }
         extra_convert = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         rec.seconds_multiply = ph.multiply;
         rec.seconds_convert = ph.convert + extra_convert;
@@ -342,7 +368,7 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
         const FullPlan fp = plan_full(p, k, beta);
         rec.t = fp.base().t();
         rec.e = fp.base().e();
-        c = mul_full_compressed(a, b, fp);
+        c = i64 ? mul_full_compressed<Int64Word>(a, b, fp) : mul_full_compressed(a, b, fp);
         break;
       }
       case Algorithm::Blocked: {
@@ -351,7 +377,7 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
         const CompressionPlan plan = kp >= 2 ? plan_compression(p, kp, beta) : uncompressed_plan(p, 1, beta);
         rec.t = plan.t();
         rec.e = plan.e();
-        c = blocked_accumulate(a, b, plan, kp);
+        c = i64 ? blocked_accumulate<Int64Word>(a, b, plan, kp) : blocked_accumulate(a, b, plan, kp);
         break;
       }
     }

@@ -136,6 +136,16 @@ int main() {
   CHECK(to_csv_row(r) == "common,3,4,5,6,7,2,0.250000,0.125000,99");
   CHECK(std::string(algorithm_name(Algorithm::FullCompressed)) == "full");
 
+  // Int64Word backend (word.hpp:36-54) at beta = 63: same C, reference words
+  const auto p63 = plan_compression(3, 14, 63);
+  CHECK(mul_common_compressed<Int64Word>(a14, b14, p63) == host_naive(a14, b14, 3));
+  CHECK(blocked_accumulate<Int64Word>(a14, b14, plan_compression(3, 7, 63), 7) == host_naive(a14, b14, 3));
+  CHECK(uncompress(mul_right_compressed_i64(a14, b14, plan_packed_axis(3, 14, 5, 63))) == host_naive(a14, b14, 3));
+  CHECK(uncompress(mul_left_compressed_i64(a14, b14, plan_packed_axis(3, 14, 3, 63))) == host_naive(a14, b14, 3));
+  CHECK(mul_full_compressed<Int64Word>(a14, b14, plan_full(3, 14, 63)) == host_naive(a14, b14, 3));
+  const auto l64 = mul_left_compressed_i64(kA, kB, p5);  // test_gemm.cpp:183-185 for Int64Word
+  CHECK(l64.data[0] == 33u && l64.data[1] == 34u);
+
   // errors: invalid modulus, dimension mismatch
   threw = false;
   try {

@@ -199,7 +199,7 @@ def test_cli_verify():  # test_cli.cpp:120-127
     assert rc == 0 and "common" in out and "blocked" in out and "ok" in out and "FAIL" not in out
     assert run_cli("verify", "--p", "2", "--max-dim", "4", "--seeds", "3")[0] == 0
     rc, out = run_cli("verify", "--p", "7", "--max-dim", "40", "--seeds", "30")
-    assert rc == 0 and out.count("ok") == 5, out
+    assert rc == 0 and out.count("ok") == 10, out  # 5 algorithms x {double, int64}
 
 
 @pytest.mark.gpu
@@ -222,3 +222,33 @@ def test_cli_bench():  # test_cli.cpp:129-154
         assert int(out.strip().split("\n")[1].split(",")[9]) == want, algo
     assert run_cli("bench", "--p", "100003", "--m", "8", "--k", "8", "--n", "8", "--algo", "common", "--reps", "1",
                    "--seed", "1")[0] == 3
+
+
+@pytest.mark.gpu
+def test_cli_int64_backend(tmp_path):
+    """--bits 54..63 runs the Int64Word backend (qgemm_main.cpp:253-266); verify
+    checks both backends (verify.hpp:128-137)."""
+    rc, out = run_cli("verify", "--p", "3", "--max-dim", "12", "--seeds", "8")
+    assert rc == 0, out
+    lines = [l for l in out.strip().split("\n") if l]
+    assert len(lines) == 10 and sum("\tint64\t" in l for l in lines) == 5, out
+    assert all("\tok (" in l for l in lines)
+    a = O.random_residue_matrix(9, 300, 3, 1)
+    b = O.random_residue_matrix(300, 7, 3, 2)
+    ap, bp = str(tmp_path / "a.mtx"), str(tmp_path / "b.mtx")
+    qg.write_matrix_file(ap, a, 3)
+    qg.write_matrix_file(bp, b, 3)
+    want = O.naive_gemm(3, a, b)
+    for algo in ("common", "right", "left", "full", "blocked"):
+        out = str(tmp_path / f"{algo}64.mtx")
+        rc, msg = run_cli("gemm", "--algo", algo, "--a", ap, "--b", bp, "--out", out, "--bits", "63")
+        assert rc == 0, (algo, msg)
+        assert np.array_equal(qg.read_matrix_file(out)[1], want), algo
+    rc, out = run_cli("bench", "--p", "3", "--m", "16", "--k", "200", "--n", "16", "--algo", "common", "--bits", "63",
+                      "--seed", "9")
+    assert rc == 0, out
+    pl = O.plan_compression(3, 200, 63)
+    f = out.strip().split("\n")[1].split(",")
+    assert f[5:7] == [str(pl.t), str(pl.e)]
+    assert int(f[9]) == O.residue_checksum(O.naive_gemm(3, O.random_residue_matrix(16, 200, 3, 9),
+                                                        O.random_residue_matrix(200, 16, 3, 10)))

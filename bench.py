@@ -348,6 +348,9 @@ def redq_arm(args):
             gp = qg.GpuPlan(base, k, k, 0)
         else:
             gp = qg.plan_right_gpu(p, k, n if variant == "right" else m)
+        if args.redq_plan:  # experiments: "t:e:kblock:balanced"
+            t_, e_, kb_, bal_ = (int(x) for x in args.redq_plan.split(":"))
+            gp = qg.GpuPlan(qg.make_plan(p, t_, e_), kb_, kb_, bal_)
         plan = gp.plan
         g = gp._c()
         bk_c = ctypes.c_uint32()
@@ -357,7 +360,7 @@ def redq_arm(args):
         else:
             rows_a, rows_b = -(-m // plan.e), n
         out_shape = (rows_a, rows_b)
-        plan_desc = {"t": plan.t, "e": plan.e, "kblock_residues": gp.kblock_words}
+        plan_desc = {"t": plan.t, "e": plan.e, "kblock_residues": gp.kblock_words, "balanced": bool(gp.balanced)}
     bk = bk_c.value
     kt = -(-k // bk)
     a = qg.random_residue_matrix(m, k, p, SEED)
@@ -374,10 +377,20 @@ def redq_arm(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
+    bal = variant != "full" and bool(gp.balanced)
+
     def step(ev=None):
-        if variant == "right":
+        if variant == "right" and bal:
+            qg._check(qg.lib.qg_pack_residues_tiled_bal(p, bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
+            qg._check(qg.lib.qg_pack_outer_cols_tiled_bal(ctypes.byref(pl), bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t),
+                                                          sp()))
+        elif variant == "right":
             qg._check(qg.lib.qg_pack_residues_tiled(bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
             qg._check(qg.lib.qg_pack_outer_cols_tiled(ctypes.byref(pl), bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t), sp()))
+        elif variant == "left" and bal:
+            qg._check(qg.lib.qg_pack_outer_rows_tiled_bal(ctypes.byref(pl), bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t),
+                                                          sp()))
+            qg._check(qg.lib.qg_pack_residues_b_tiled_bal(p, bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t), sp()))
         elif variant == "left":
             qg._check(qg.lib.qg_pack_outer_rows_tiled(ctypes.byref(pl), bk, qg._ptr(a), 0, m, k, k, qg._ptr(a_t), sp()))
             qg._check(qg.lib.qg_pack_residues_b_tiled(bk, qg._ptr(b), 0, k, n, n, qg._ptr(b_t), sp()))
@@ -736,6 +749,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step's kernels directly (no CUDA graph)")
+    ap.add_argument("--redq-plan", default="", help="experiments: right/left plan 't:e:kblock_residues:balanced'")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -215,6 +215,19 @@ int qg_pack_residues_b_tiled(uint32_t bk, const void* b, qg_dtype dtype, size_t 
                              double* b_t, void* stream);
 int qg_mul_left_tiled(const qg_gpu_plan* gplan, const double* ao_t, const double* b_t, size_t m, size_t k,
                       size_t n, double* cc, size_t ldcc, void* stream);
+/* Balanced-digit operands of the right/left contractions, for plans with
+ * gplan->balanced (qg_plan_right_gpu picks them for odd p): residue v enters
+ * as v - p when v > p/2, halving every digit's bound, so k-blocks between
+ * in-place REDQs are about twice as long. The CC words out are the same
+ * canonical (unsigned) words. */
+int qg_pack_residues_tiled_bal(uint32_t p, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k, size_t lda,
+                               double* a_t, void* stream);
+int qg_pack_residues_b_tiled_bal(uint32_t p, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+                                 size_t ldb, double* b_t, void* stream);
+int qg_pack_outer_cols_tiled_bal(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+                                 size_t ldb, double* bo_t, void* stream);
+int qg_pack_outer_rows_tiled_bal(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
+                                 size_t lda, double* ao_t, void* stream);
 
 /* Full (mul_full_compressed, gemm.hpp:377-445): rows of A packed in base Q
  * with dq+1 slots (qg_pack_outer_rows_tiled under {t, e = dq+1}), columns of

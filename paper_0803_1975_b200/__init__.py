@@ -186,6 +186,10 @@ def _load():
         "qg_pack_outer_rows_tiled": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_pack_residues_b_tiled": ([u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_mul_left_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_pack_residues_tiled_bal": ([u32, u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_residues_b_tiled_bal": ([u32, u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_outer_cols_tiled_bal": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
+        "qg_pack_outer_rows_tiled_bal": ([P(_Plan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_plan_full": ([u32, u64, i32, P(_FullPlan)], i32),
         "qg_plan_full_gpu": ([u32, u64, P(_FullPlan), P(u64)], i32),
         "qg_full_tiled_stage": ([P(_FullPlan), u64, u64, P(u32)], i32),
@@ -732,9 +736,15 @@ def mul_right_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMa
     kt = -(-k // bk)
     a_t = torch.empty(-(-m // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
     bo_t = torch.empty(-(-H // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
-    _check(lib.qg_pack_residues_tiled(bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(a_t), _stream()))
     c_pl = pl._c()
-    _check(lib.qg_pack_outer_cols_tiled(ctypes.byref(c_pl), bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(bo_t), _stream()))
+    if gp.balanced:  # balanced digits: twice the k-block between in-place REDQs
+        _check(lib.qg_pack_residues_tiled_bal(pl.p, bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(a_t), _stream()))
+        _check(lib.qg_pack_outer_cols_tiled_bal(ctypes.byref(c_pl), bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(bo_t),
+                                                _stream()))
+    else:
+        _check(lib.qg_pack_residues_tiled(bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(a_t), _stream()))
+        _check(lib.qg_pack_outer_cols_tiled(ctypes.byref(c_pl), bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(bo_t),
+                                            _stream()))
     cc = torch.empty((m, H), dtype=torch.float64, device=a.device)
     _check(lib.qg_mul_right_tiled(ctypes.byref(g), _ptr(a_t), _ptr(bo_t), m, k, n, _ptr(cc), H, _stream()))
     return CompressedMatrix(m, n, m, H, PackOrientation(PackDirection.Forward, PackAxis.Column, pl.e), pl, cc)
@@ -764,8 +774,14 @@ def mul_left_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMat
     ao_t = torch.empty(-(-G // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
     b_t = torch.empty(-(-n // 128) * 128 * kt * bk, dtype=torch.float64, device=a.device)
     c_pl = pl._c()
-    _check(lib.qg_pack_outer_rows_tiled(ctypes.byref(c_pl), bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(ao_t), _stream()))
-    _check(lib.qg_pack_residues_b_tiled(bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(b_t), _stream()))
+    if gp.balanced:
+        _check(lib.qg_pack_outer_rows_tiled_bal(ctypes.byref(c_pl), bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(ao_t),
+                                                _stream()))
+        _check(lib.qg_pack_residues_b_tiled_bal(pl.p, bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(b_t), _stream()))
+    else:
+        _check(lib.qg_pack_outer_rows_tiled(ctypes.byref(c_pl), bk, _ptr(a), _dtype_code(a), m, k, k, _ptr(ao_t),
+                                            _stream()))
+        _check(lib.qg_pack_residues_b_tiled(bk, _ptr(b), _dtype_code(b), k, n, n, _ptr(b_t), _stream()))
     cc = torch.empty((G, n), dtype=torch.float64, device=a.device)
     _check(lib.qg_mul_left_tiled(ctypes.byref(g), _ptr(ao_t), _ptr(b_t), m, k, n, _ptr(cc), n, _stream()))
     return CompressedMatrix(m, n, G, n, PackOrientation(PackDirection.Forward, PackAxis.Row, pl.e), pl, cc)

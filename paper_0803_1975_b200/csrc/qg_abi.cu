@@ -262,13 +262,16 @@ static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const doubl
   int st = check_plan(&pl);
   if (st) return st;
   if (pl.t * pl.e > 53) return QG_PLAN_MISMATCH;  // sums must stay exact
-  const uint64_t pm = (uint64_t)(pl.p - 1) * (pl.p - 1);
-  const uint64_t Q = 1ull << pl.t;
+  const bool bal = gplan->balanced != 0;
+  if (bal && (pl.t > 31 || pl.t * pl.e > 52 || pl.t < 2)) return QG_PLAN_MISMATCH;
+  const uint64_t h = bal ? pl.p / 2 : pl.p - 1;  // largest |digit| of an operand
+  const uint64_t pm = h * h;
+  const uint64_t Q = 1ull << pl.t, lim = bal ? Q / 2 : Q;  // digits stay in (-Q/2, Q/2) resp. [0, Q)
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gplan, k, &bk, &kbs))) return st;
   if (kbs == 0) {
-    if (k > pl.kmax) return QG_PLAN_MISMATCH;
-  } else if ((pl.p - 1) + (uint64_t)kbs * bk * pm >= Q) {
+    if (bal ? (uint64_t)k * pm >= lim : k > pl.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295 for unsigned
+  } else if (h + (uint64_t)kbs * bk * pm >= lim) {
     return QG_PLAN_MISMATCH;  // a block would overflow a digit after the in-place REDQ
   }
   if (ldcc < N) return QG_INVALID_ARGUMENT;
@@ -292,6 +295,14 @@ static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const doubl
   r.p = pl.p;
   r.cc = cc;
   r.ldcc = ldcc;
+  if (bal) {  // constants of the balanced in-place REDQ (qg_dot.cu, redq_words_inplace_bal)
+    r.balanced = 1;
+    const uint64_t half = Q / 2;
+    uint64_t off = 0;
+    for (int d = 0; d < pl.e; ++d) off |= half << (pl.t * d);
+    r.redq_off2 = (double)off + 4503599627370496.0;  // exact: off < 2^52
+    r.redq_ybias = (uint32_t)((half + pl.p - 1) / pl.p * pl.p - half);
+  }
   return cuda_status(qgk::launch_right_tiled(r, bk, true, s, &g_last_kernel));
 }
 
@@ -321,6 +332,43 @@ int qg_pack_residues_b_tiled(uint32_t bk, const void* b, qg_dtype dtype, size_t 
   if (ldb < n) return QG_INVALID_ARGUMENT;
   return cuda_status(qgk::launch_pack_tiled(true, b, dtype, k, n, ldb, 1, 1, (int)bk, b_t, as_stream(stream), 2,
                                             false));
+}
+
+// Balanced-digit operands for plans with gplan->balanced (residue v enters as
+// v - p when v > p/2): the same layouts as the entries above.
+int qg_pack_residues_tiled_bal(uint32_t p, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k, size_t lda,
+                               double* a_t, void* stream) {
+  int st = check_dtype(dtype);
+  if (st) return st;
+  if (p < 2 || !qg::is_prime(p)) return QG_INVALID_MODULUS;
+  if (lda < k) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_tiled(false, a, dtype, m, k, lda, 1, 1, (int)bk, a_t, as_stream(stream), p, true));
+}
+int qg_pack_residues_b_tiled_bal(uint32_t p, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n, size_t ldb,
+                                 double* b_t, void* stream) {
+  int st = check_dtype(dtype);
+  if (st) return st;
+  if (p < 2 || !qg::is_prime(p)) return QG_INVALID_MODULUS;
+  if (ldb < n) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_tiled(true, b, dtype, k, n, ldb, 1, 1, (int)bk, b_t, as_stream(stream), p, true));
+}
+int qg_pack_outer_cols_tiled_bal(const qg_plan* plan, uint32_t bk, const void* b, qg_dtype dtype, size_t k, size_t n,
+                                 size_t ldb, double* bo_t, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (ldb < n || !redq_stage_ok(bk)) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_outer_tiled_bal(b, dtype, k, n, ldb, plan->t, plan->e, (int)bk, bo_t, plan->p,
+                                                      as_stream(stream)));
+}
+int qg_pack_outer_rows_tiled_bal(const qg_plan* plan, uint32_t bk, const void* a, qg_dtype dtype, size_t m, size_t k,
+                                 size_t lda, double* ao_t, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (lda < k || !redq_stage_ok(bk)) return QG_INVALID_ARGUMENT;
+  return cuda_status(qgk::launch_pack_outer_rows_tiled_bal(a, dtype, m, k, lda, plan->t, plan->e, (int)bk, ao_t,
+                                                           plan->p, as_stream(stream)));
 }
 
 int qg_mul_left_tiled(const qg_gpu_plan* gplan, const double* ao_t, const double* b_t, size_t m, size_t k,
@@ -909,7 +957,10 @@ static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* 
   QG_TRY(dcc.alloc(m * H * 8));
   if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if (k) {
+  if (k && gp->balanced) {
+    if ((st = qg_pack_residues_tiled_bal(plan->p, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
+    if ((st = qg_pack_outer_cols_tiled_bal(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
+  } else if (k) {
     if ((st = qg_pack_residues_tiled((uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
     if ((st = qg_pack_outer_cols_tiled(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
   }
@@ -943,7 +994,10 @@ static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b
   QG_TRY(dcc.alloc(G * n * 8));
   if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if (k) {
+  if (k && gp->balanced) {
+    if ((st = qg_pack_outer_rows_tiled_bal(plan, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
+    if ((st = qg_pack_residues_b_tiled_bal(plan->p, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
+  } else if (k) {
     if ((st = qg_pack_outer_rows_tiled(plan, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
     if ((st = qg_pack_residues_b_tiled((uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
   }

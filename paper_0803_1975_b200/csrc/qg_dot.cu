@@ -200,6 +200,37 @@ __device__ __forceinline__ void redq_words_inplace(double* w, int t, int e, cons
   for (int i = 0; i < NW; ++i) w[i] = __longlong_as_double((long long)u[i]) - 4503599627370496.0;
 }
 
+// The same in-place REDQ on balanced (signed) digits: w = sum_s D_s Q^s with
+// |D_s| < Q/2. Adding OFF = sum_s (Q/2) Q^s makes every digit D_s + Q/2 an
+// unsigned base-Q digit (no borrows), so the digits can be read as above;
+// x + ybias is >= 0 and = D_s (mod p). Between k-blocks a digit becomes its
+// centred residue (|r| <= p/2) offset by Q/2 and w = u - OFF - 2^52 keeps the
+// signed form; FINAL replaces it by the canonical residue in [0, p) and drops
+// the offset, giving exactly the unsigned REDQ words (pack.hpp:124-137).
+template <int NW, bool FINAL>
+__device__ __forceinline__ void redq_words_inplace_bal(double* w, int t, int e, const ModP& modp, double off2,
+                                                       uint32_t ybias) {
+  const uint32_t qmask = (1u << t) - 1, half = 1u << (t - 1), h = modp.p >> 1;
+  uint64_t u[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) u[i] = (uint64_t)__double_as_longlong(w[i] + off2);
+  const int total = t * e;
+  for (int o = 0; o < total; o += t) {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const uint32_t x = (uint32_t)(u[i] >> o) & qmask;
+      const uint32_t y = x + ybias;
+      const uint32_t r1 = y - __umulhi(y, modp.magic) * modp.p;
+      const uint32_t r0 = min(r1, r1 - modp.p);  // D mod p in [0, p)
+      const uint32_t nd = FINAL ? r0 : (r0 > h ? r0 - modp.p : r0) + half;
+      u[i] -= (uint64_t)((long long)x - (long long)nd) << o;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NW; ++i)
+    w[i] = __longlong_as_double((long long)u[i]) - (FINAL ? 4503599627370496.0 : off2);
+}
+
 template <int BK, int VEC, int EPI, bool MULTI>
 __global__ void __launch_bounds__(NT, 1) k_gemm_dmma(GemmArgs args) {
   using G = Geo<BK>;
@@ -501,6 +532,9 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
           kst = 0;
           if (args.debug & 8) {
             // debug bit 3: timing without the in-place REDQ (wrong results)
+          } else if (BAL) {
+            redq_words_inplace_bal<MI * NI * 2, false>(&acc[0][0][0], args.t, args.e, modp, args.redq_off2,
+                                                       args.redq_ybias);
           } else if (args.t <= 31 && args.t * args.e <= 52) {
             redq_words_inplace<MI * NI * 2>(&acc[0][0][0], args.t, args.e, modp);
           } else {
@@ -536,7 +570,10 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
     }
     // epilogue of this tile (the producer is already filling the next tile's stages)
     if (EPI == EPI_REDQ) {  // redq, pack.hpp:124-137, on the whole warp tile
-      if (args.t <= 31 && args.t * args.e <= 52) {
+      if (BAL) {
+        redq_words_inplace_bal<MI * NI * 2, true>(&acc[0][0][0], args.t, args.e, modp, args.redq_off2,
+                                                  args.redq_ybias);
+      } else if (args.t <= 31 && args.t * args.e <= 52) {
         redq_words_inplace<MI * NI * 2>(&acc[0][0][0], args.t, args.e, modp);
       } else {
 #pragma unroll
@@ -987,6 +1024,9 @@ cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const ch
 template <int BK>
 static cudaError_t launch_right_tiled_bk(const GemmArgs& a, bool redq, cudaStream_t s) {
   if (!redq) return launch_tiled_one<BK, EPI_RAW, false, 0, false>(a, s);
+  if (a.balanced)
+    return a.kb_stages ? launch_tiled_one<BK, EPI_REDQ, true, 0, true>(a, s)
+                       : launch_tiled_one<BK, EPI_REDQ, false, 0, true>(a, s);
   if (a.kb_stages) return launch_tiled_one<BK, EPI_REDQ, true, 0, false>(a, s);
   return launch_tiled_one<BK, EPI_REDQ, false, 0, false>(a, s);
 }
@@ -994,7 +1034,8 @@ static cudaError_t launch_right_tiled_bk(const GemmArgs& a, bool redq, cudaStrea
 cudaError_t launch_right_tiled(const GemmArgs& a, int bk, bool redq, cudaStream_t s, const char** variant) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
   static thread_local char name[64];
-  snprintf(name, sizeof name, "right_tiled_bk%d_%s%s", bk, redq ? "redq" : "raw", a.kb_stages ? "_blocked" : "");
+  snprintf(name, sizeof name, "right_tiled_bk%d_%s%s%s", bk, redq ? "redq" : "raw", a.kb_stages ? "_blocked" : "",
+           a.balanced ? "_balanced" : "");
   *variant = name;
   switch (bk) {
     case 36: return launch_right_tiled_bk<36>(a, redq, s);

@@ -65,6 +65,8 @@ struct GemmArgs {
   unsigned skew_ns;     // start delay of warps 4..7 (desynchronises the flushes of SMSP warp pairs)
   int balanced;         // balanced (signed) digits: round-to-nearest extraction, biased by Q/2
   uint32_t corr;        // balanced: (p - (#extractions * Q/2) mod p) mod p, added in the epilogue
+  double redq_off2;     // balanced REDQ: sum_s (Q/2) Q^s + 2^52 (makes every signed digit an unsigned one)
+  uint32_t redq_ybias;  // balanced REDQ: p ceil(Q/2 / p) - Q/2, so x + ybias = D (mod p) and >= 0
 };
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
@@ -74,6 +76,11 @@ cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const ch
 // CBo_t (compress_outer_cols words, transposed blocks); REDQ between k-blocks
 // (kb_stages) and in the epilogue, CC m x N (N = ceil(n/e)).
 cudaError_t launch_right_tiled(const GemmArgs& a, int bk, bool redq, cudaStream_t s, const char** variant);
+// balanced operands (a.balanced): signed residues / words in, canonical CC out
+cudaError_t launch_pack_outer_tiled_bal(const void* src, int dtype, size_t k, size_t n, size_t ld, int t, int e, int bk,
+                                        double* dst, uint32_t p, cudaStream_t s);
+cudaError_t launch_pack_outer_rows_tiled_bal(const void* src, int dtype, size_t m, size_t k, size_t ld, int t, int e,
+                                             int bk, double* dst, uint32_t p, cudaStream_t s);
 // CBo_t[tn][kt][r][c] = compress_outer_cols(B)[BK kt + c][128 tn + r].
 cudaError_t launch_pack_outer_rows_tiled(const void* src, int dtype, size_t m, size_t k, size_t ld, int t, int e,
                                          int bk, double* dst, cudaStream_t s);

@@ -210,9 +210,10 @@ __global__ void __launch_bounds__(256) k_pack_b_tiled(const TIn* __restrict__ b,
 // compress_outer_cols (gemm.hpp:145-158) words in the tiled transposed layout
 // of the mixed-variant contraction: CBo_t[tn][kt][r][c] = word (row BK kt + c,
 // group 128 tn + r) = sum_s B[BK kt + c][(128 tn + r) e + s] Q^s.
-template <typename TIn, int BK>
+template <typename TIn, int BK, bool BAL = false>
 __global__ void __launch_bounds__(256) k_pack_outer_tiled(const TIn* __restrict__ b, size_t k, size_t n, size_t ldb,
-                                                          int t, int e, unsigned Kt, double* __restrict__ bo_t) {
+                                                          int t, int e, unsigned Kt, double* __restrict__ bo_t,
+                                                          uint32_t p = 0) {
   __shared__ double tile[64 * (BK + 1)];
   const size_t H = (n + e - 1) / e;
   const size_t blk = blockIdx.x >> 1, half = blockIdx.x & 1;
@@ -221,40 +222,52 @@ __global__ void __launch_bounds__(256) k_pack_outer_tiled(const TIn* __restrict_
   const size_t hcol = tn * 128 + half * 64 + r;
   for (int c = cg; c < BK; c += 4) {
     const size_t l = kt * BK + c;
-    uint64_t w = 0;
-    if (hcol < H && l < k) {
-      const size_t base = hcol * e;
-      const int len = (int)((n - base) < (size_t)e ? (n - base) : (size_t)e);
-      for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(b[l * ldb + base + s]);
+    double wd;
+    if (BAL) {  // balanced digits (v - p for v > p/2): a signed word, exact in double
+      long long w = 0;
+      if (hcol < H && l < k) {
+        const size_t base = hcol * e;
+        const int len = (int)((n - base) < (size_t)e ? (n - base) : (size_t)e);
+        for (int s = len - 1; s >= 0; --s) w = w * (1ll << t) + balanced_digit(residue_bits(b[l * ldb + base + s]), p);
+      }
+      wd = __ll2double_rn(w);
+    } else {
+      uint64_t w = 0;
+      if (hcol < H && l < k) {
+        const size_t base = hcol * e;
+        const int len = (int)((n - base) < (size_t)e ? (n - base) : (size_t)e);
+        for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(b[l * ldb + base + s]);
+      }
+      wd = __ull2double_rn(w);
     }
-    tile[r * (BK + 1) + c] = __ull2double_rn(w);
+    tile[r * (BK + 1) + c] = wd;
   }
   __syncthreads();
   double* out = bo_t + blk * (size_t)(128 * BK) + half * (size_t)(64 * BK);
   for (int i = threadIdx.x; i < 64 * BK; i += 256) out[i] = tile[(i / BK) * (BK + 1) + i % BK];
 }
 
-template <typename TIn, int BK>
+template <typename TIn, int BK, bool BAL = false>
 static cudaError_t pack_outer_tiled_t(const TIn* src, size_t k, size_t n, size_t ld, int t, int e, double* dst,
-                                      cudaStream_t s) {
+                                      cudaStream_t s, uint32_t p = 0) {
   const size_t H = (n + e - 1) / e;
   const unsigned Kt = (unsigned)((k + BK - 1) / BK);
   const size_t Nt = (H + 127) / 128;
   if (Kt == 0 || Nt == 0) return cudaSuccess;
-  k_pack_outer_tiled<TIn, BK><<<(unsigned)(Nt * Kt * 2), 256, 0, s>>>(src, k, n, ld, t, e, Kt, dst);
+  k_pack_outer_tiled<TIn, BK, BAL><<<(unsigned)(Nt * Kt * 2), 256, 0, s>>>(src, k, n, ld, t, e, Kt, dst, p);
   count_launch();
   return cudaGetLastError();
 }
 
-template <typename TIn>
+template <typename TIn, bool BAL = false>
 static cudaError_t pack_outer_tiled_dt(const TIn* src, size_t k, size_t n, size_t ld, int t, int e, int bk,
-                                       double* dst, cudaStream_t s) {
+                                       double* dst, cudaStream_t s, uint32_t p = 0) {
   switch (bk) {
-    case 36: return pack_outer_tiled_t<TIn, 36>(src, k, n, ld, t, e, dst, s);
-    case 28: return pack_outer_tiled_t<TIn, 28>(src, k, n, ld, t, e, dst, s);
-    case 20: return pack_outer_tiled_t<TIn, 20>(src, k, n, ld, t, e, dst, s);
-    case 12: return pack_outer_tiled_t<TIn, 12>(src, k, n, ld, t, e, dst, s);
-    case 4: return pack_outer_tiled_t<TIn, 4>(src, k, n, ld, t, e, dst, s);
+    case 36: return pack_outer_tiled_t<TIn, 36, BAL>(src, k, n, ld, t, e, dst, s, p);
+    case 28: return pack_outer_tiled_t<TIn, 28, BAL>(src, k, n, ld, t, e, dst, s, p);
+    case 20: return pack_outer_tiled_t<TIn, 20, BAL>(src, k, n, ld, t, e, dst, s, p);
+    case 12: return pack_outer_tiled_t<TIn, 12, BAL>(src, k, n, ld, t, e, dst, s, p);
+    case 4: return pack_outer_tiled_t<TIn, 4, BAL>(src, k, n, ld, t, e, dst, s, p);
   }
   return cudaErrorInvalidValue;
 }
@@ -264,23 +277,33 @@ static cudaError_t pack_outer_tiled_dt(const TIn* src, size_t k, size_t n, size_
 // blocks [g-tile][k-tile][g][l]. One CTA per block; consecutive threads run
 // along l, so each run of BK reads is one contiguous row segment and the
 // block is written contiguously.
-template <typename TIn, int BK>
+template <typename TIn, int BK, bool BAL = false>
 __global__ void __launch_bounds__(256) k_pack_outer_rows_tiled(const TIn* __restrict__ a, size_t m, size_t k,
                                                                size_t lda, int t, int e, unsigned Kt,
-                                                               double* __restrict__ ao_t) {
+                                                               double* __restrict__ ao_t, uint32_t p = 0) {
   const size_t G = (m + e - 1) / e;
   const unsigned kt = blockIdx.x % Kt, tg = blockIdx.x / Kt;
   double* out = ao_t + (size_t)blockIdx.x * (128 * BK);
   for (unsigned idx = threadIdx.x; idx < 128 * BK; idx += 256) {
     const unsigned r = idx / BK, c = idx % BK;
     const size_t g = (size_t)tg * 128 + r, l = (size_t)kt * BK + c;
-    uint64_t w = 0;
-    if (g < G && l < k) {
-      const size_t base = g * e;
-      const int len = (int)((m - base) < (size_t)e ? (m - base) : (size_t)e);
-      for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(a[(base + s) * lda + l]);
+    if (BAL) {  // balanced digits: a signed word
+      long long w = 0;
+      if (g < G && l < k) {
+        const size_t base = g * e;
+        const int len = (int)((m - base) < (size_t)e ? (m - base) : (size_t)e);
+        for (int s = len - 1; s >= 0; --s) w = w * (1ll << t) + balanced_digit(residue_bits(a[(base + s) * lda + l]), p);
+      }
+      out[idx] = __ll2double_rn(w);
+    } else {
+      uint64_t w = 0;
+      if (g < G && l < k) {
+        const size_t base = g * e;
+        const int len = (int)((m - base) < (size_t)e ? (m - base) : (size_t)e);
+        for (int s = len - 1; s >= 0; --s) w = (w << t) | residue_bits(a[(base + s) * lda + l]);
+      }
+      out[idx] = __ull2double_rn(w);
     }
-    out[idx] = __ull2double_rn(w);
   }
 }
 
@@ -654,28 +677,28 @@ cudaError_t launch_pack_outer_tiled(const void* src, int dtype, size_t k, size_t
   }
 }
 
-template <typename TIn, int BK>
+template <typename TIn, int BK, bool BAL = false>
 static cudaError_t pack_outer_rows_tiled_t(const TIn* src, size_t m, size_t k, size_t ld, int t, int e, double* dst,
-                                           cudaStream_t s) {
+                                           cudaStream_t s, uint32_t p = 0) {
   const size_t G = (m + e - 1) / e;
   const unsigned Kt = (unsigned)((k + BK - 1) / BK);
   const size_t blocks = (G + 127) / 128 * Kt;
   if (blocks == 0) return cudaSuccess;
   if (blocks >= (1ull << 31)) return cudaErrorInvalidValue;
-  k_pack_outer_rows_tiled<TIn, BK><<<(unsigned)blocks, 256, 0, s>>>(src, m, k, ld, t, e, Kt, dst);
+  k_pack_outer_rows_tiled<TIn, BK, BAL><<<(unsigned)blocks, 256, 0, s>>>(src, m, k, ld, t, e, Kt, dst, p);
   count_launch();
   return cudaGetLastError();
 }
 
-template <typename TIn>
+template <typename TIn, bool BAL = false>
 static cudaError_t pack_outer_rows_tiled_dt(const TIn* src, size_t m, size_t k, size_t ld, int t, int e, int bk,
-                                            double* dst, cudaStream_t s) {
+                                            double* dst, cudaStream_t s, uint32_t p = 0) {
   switch (bk) {
-    case 36: return pack_outer_rows_tiled_t<TIn, 36>(src, m, k, ld, t, e, dst, s);
-    case 28: return pack_outer_rows_tiled_t<TIn, 28>(src, m, k, ld, t, e, dst, s);
-    case 20: return pack_outer_rows_tiled_t<TIn, 20>(src, m, k, ld, t, e, dst, s);
-    case 12: return pack_outer_rows_tiled_t<TIn, 12>(src, m, k, ld, t, e, dst, s);
-    case 4: return pack_outer_rows_tiled_t<TIn, 4>(src, m, k, ld, t, e, dst, s);
+    case 36: return pack_outer_rows_tiled_t<TIn, 36, BAL>(src, m, k, ld, t, e, dst, s, p);
+    case 28: return pack_outer_rows_tiled_t<TIn, 28, BAL>(src, m, k, ld, t, e, dst, s, p);
+    case 20: return pack_outer_rows_tiled_t<TIn, 20, BAL>(src, m, k, ld, t, e, dst, s, p);
+    case 12: return pack_outer_rows_tiled_t<TIn, 12, BAL>(src, m, k, ld, t, e, dst, s, p);
+    case 4: return pack_outer_rows_tiled_t<TIn, 4, BAL>(src, m, k, ld, t, e, dst, s, p);
   }
   return cudaErrorInvalidValue;
 }
@@ -686,6 +709,24 @@ cudaError_t launch_pack_outer_rows_tiled(const void* src, int dtype, size_t m, s
     case 0: return pack_outer_rows_tiled_dt<double>((const double*)src, m, k, ld, t, e, bk, dst, s);
     case 1: return pack_outer_rows_tiled_dt<uint32_t>((const uint32_t*)src, m, k, ld, t, e, bk, dst, s);
     default: return pack_outer_rows_tiled_dt<int32_t>((const int32_t*)src, m, k, ld, t, e, bk, dst, s);
+  }
+}
+
+cudaError_t launch_pack_outer_tiled_bal(const void* src, int dtype, size_t k, size_t n, size_t ld, int t, int e, int bk,
+                                        double* dst, uint32_t p, cudaStream_t s) {
+  switch (dtype) {
+    case 0: return pack_outer_tiled_dt<double, true>((const double*)src, k, n, ld, t, e, bk, dst, s, p);
+    case 1: return pack_outer_tiled_dt<uint32_t, true>((const uint32_t*)src, k, n, ld, t, e, bk, dst, s, p);
+    default: return pack_outer_tiled_dt<int32_t, true>((const int32_t*)src, k, n, ld, t, e, bk, dst, s, p);
+  }
+}
+
+cudaError_t launch_pack_outer_rows_tiled_bal(const void* src, int dtype, size_t m, size_t k, size_t ld, int t, int e,
+                                             int bk, double* dst, uint32_t p, cudaStream_t s) {
+  switch (dtype) {
+    case 0: return pack_outer_rows_tiled_dt<double, true>((const double*)src, m, k, ld, t, e, bk, dst, s, p);
+    case 1: return pack_outer_rows_tiled_dt<uint32_t, true>((const uint32_t*)src, m, k, ld, t, e, bk, dst, s, p);
+    default: return pack_outer_rows_tiled_dt<int32_t, true>((const int32_t*)src, m, k, ld, t, e, bk, dst, s, p);
   }
 }
 

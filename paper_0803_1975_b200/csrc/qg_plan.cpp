@@ -389,32 +389,44 @@ int qg_plan_right_gpu(uint32_t p, uint64_t k, uint64_t n, qg_gpu_plan* out) {
   bool found = false;
   qg_gpu_plan best;
   std::memset(&best, 0, sizeof best);
-  const uint64_t pm = pm1sq(p);
-  for (int e = 1; e <= 26; ++e) {
-    if (uint64_t(e) > n && e > 1) break;
-    const int t = 52 / e;  // largest t with t e <= 52: words stay below 2^52
-    if (t < 1 || t > 52) continue;
-    const uint64_t Q = uint64_t(1) << t;
-    const uint64_t km = largest_common_dim(p, t);
-    if (km == 0) continue;
-    uint64_t kb;
-    if (k <= km) kb = k;  // one block, the reference's own condition (gemm.hpp:295)
-    else {
-      if (Q <= p) continue;
-      kb = (Q - p) / (pm ? pm : 1);
-      if (kb < 4) continue;
-      kb = stage_block_redq(kb, nullptr);
-      if (kb == 0) continue;
-    }
-    const double H = double((n + e - 1) / e);
-    const double nflush = kb >= k ? 0.0 : double((k + kb - 1) / kb);
-    const double cost = H * (double(k) + 4.0 * e * nflush);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      found = true;
-      fill(&best.plan, p, t, e, 53, std::ldexp(1.0, -t * (e - 1)));
-      best.kblock_words = kb;  // residues of k per block
-      best.max_exact_words = kb;
+  // unsigned digits: a block may add kb residues with (p-1) + kb (p-1)^2 < Q;
+  // balanced digits (|v| <= p/2): h + kb h^2 < Q/2 with h = p/2 — 2x longer
+  // blocks for odd p (qg_dot.cu, redq_words_inplace_bal)
+  for (int bal = 0; bal <= 1; ++bal) {
+    const uint64_t h = bal ? p / 2 : p - 1;
+    const uint64_t pm = h * h ? h * h : 1;
+    for (int e = 1; e <= 26; ++e) {
+      if (uint64_t(e) > n && e > 1) break;
+      const int t = 52 / e;  // largest t with t e <= 52: words stay below 2^52
+      if (t < 2 || t > 52 || (bal && t > 31)) continue;
+      const uint64_t Q = uint64_t(1) << t, lim = bal ? Q / 2 : Q;
+      const uint64_t km = (lim - 1) / pm;  // one block: k h^2 < lim
+      if (km == 0) continue;
+      uint64_t kb;
+      if (k <= km && (bal || k <= largest_common_dim(p, t))) kb = k;  // one block (gemm.hpp:295 for unsigned)
+      else {
+        if (lim <= h + 1) continue;
+        kb = (lim - 1 - h) / pm;
+        if (kb < 4) continue;
+        kb = stage_block_redq(kb, nullptr);
+        if (kb == 0) continue;
+      }
+      // cost in residue-steps of the contraction per output word: stage-padded
+      // k at the stage's cost, plus a calibrated in-place REDQ per block
+      // (config 4 on B200: ~5.5 e unsigned, ~11 e balanced; profiles/r01_notes.md)
+      int bk = 28;
+      if (kb < k) stage_block_redq(kb, &bk);
+      const double H = double((n + e - 1) / e);
+      const double nflush = kb >= k ? 0.0 : double((k + kb - 1) / kb);
+      const double cost = H * (double((k + bk - 1) / bk * bk) * stage_cost(bk) + (bal ? 11.0 : 5.5) * e * nflush);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        found = true;
+        fill(&best.plan, p, t, e, 53, std::ldexp(1.0, -t * (e - 1)));
+        best.kblock_words = kb;  // residues of k per block
+        best.max_exact_words = kb;
+        best.balanced = bal;
+      }
     }
   }
   if (!found) return QG_NO_COMPRESSION;
@@ -481,8 +493,11 @@ int qg_plan_full_gpu(uint32_t p, uint64_t k, qg_full_plan* out, uint64_t* kblock
       kb = stage_block_redq(kb, nullptr);
       if (kb == 0) continue;
     }
+    int bk = 28;
+    if (kb < k) stage_block_redq(kb, &bk);
     const double nflush = kb >= k ? 0.0 : double((k + kb - 1) / kb);
-    const double cost = (double(k) + 4.0 * e * nflush) / double(e);
+    // as qg_plan_right_gpu: stage-padded k at the stage's cost + calibrated REDQ flushes
+    const double cost = (double((k + bk - 1) / bk * bk) * stage_cost(bk) + 5.5 * e * nflush) / double(e);
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
       found = true;

@@ -194,3 +194,36 @@ def test_host_entries_with_gpu_plans(qg, orc, p, k, m, n):
     big = orc.Plan(*orc.plan_of(gl.plan).astuple())
     big.kmax = max(big.kmax, k)
     assert np.array_equal(bits(qg.mul_left_compressed_host(a, b, gl)), bits(orc.compress_outer_rows(big, want)))
+
+
+@pytest.mark.parametrize("p,t,e,kb", [(5, 13, 4, 1008), (7, 13, 4, 448), (3, 10, 5, 252), (11, 12, 4, 72),
+                                      (13, 13, 4, 36), (5, 13, 4, 28)])
+@pytest.mark.parametrize("m,k,n", [(130, 3000, 70), (67, 1001, 129), (5, 37, 9)])
+def test_balanced_redq_plans(qg, orc, cuda, p, t, e, kb, m, k, n):
+    """Balanced-digit right/left products (signed operands, balanced in-place
+    REDQ between k-blocks): the CC words are the canonical REDQ words of C."""
+    import torch
+
+    a, b = orc.random_residue_matrix(m, k, p, 577), orc.random_residue_matrix(k, n, p, 578)
+    want = orc.naive_gemm(p, a, b)
+    gp = qg.GpuPlan(qg.make_plan(p, t, e), kb, kb, 1)
+    big = orc.Plan(*orc.plan_of(gp.plan).astuple())
+    big.kmax = max(big.kmax, k)
+    for dtype in (np.float64, np.int32):
+        ad, bd = _dev(torch, a, cuda, dtype), _dev(torch, b, cuda, dtype)
+        cc = qg.mul_right_tiled(ad, bd, gp)
+        assert np.array_equal(bits(host(cc.data)), bits(orc.compress_outer_cols(big, want)))
+        cl = qg.mul_left_tiled(ad, bd, gp)
+        assert np.array_equal(bits(host(cl.data)), bits(orc.compress_outer_rows(big, want)))
+    assert np.array_equal(bits(qg.mul_right_compressed_host(a, b, gp)), bits(orc.compress_outer_cols(big, want)))
+    assert np.array_equal(bits(qg.mul_left_compressed_host(a, b, gp)), bits(orc.compress_outer_rows(big, want)))
+
+
+def test_balanced_redq_bound_is_enforced(qg, cuda):
+    import torch
+
+    a = torch.zeros((8, 3000), dtype=torch.float64, device=cuda)
+    b = torch.zeros((3000, 8), dtype=torch.float64, device=cuda)
+    # p = 5, t = 13: h + kb h^2 < Q/2 allows 1023 residues per block, not 2016
+    with pytest.raises(qg.PlanMismatch):
+        qg.mul_right_tiled(a, b, qg.GpuPlan(qg.make_plan(5, 13, 4), 2016, 2016, 1))

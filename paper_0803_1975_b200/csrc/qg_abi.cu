@@ -52,6 +52,12 @@ int check_plan(const qg_plan* plan) {
   return QG_OK;
 }
 
+// kernel arguments carry dimensions as int: larger ones are refused, not wrapped
+bool dims_ok(size_t a, size_t b, size_t c = 0) {
+  const size_t lim = 0x7FFFFFFF;
+  return a <= lim && b <= lim && c <= lim;
+}
+
 int check_dtype(qg_dtype d) { return (d == QG_F64 || d == QG_U32 || d == QG_I32) ? QG_OK : QG_INVALID_ARGUMENT; }
 
 // Device flag for DigitOverflow (redq / extract_all throw it in the reference).
@@ -100,6 +106,7 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
     a.lda = ldca;
     a.b = cb;
     a.ldb = ldcb;
+    if (!dims_ok(m, n, K)) return QG_INVALID_ARGUMENT;
     a.M = (int)m;
     a.N = (int)n;
     a.kb_stages = blk >= K ? 0 : (int)(blk / bk);
@@ -128,6 +135,7 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
   h.ldca = ldca;
   h.cb = cb;
   h.ldcb = ldcb;
+  if (!dims_ok(m, n, K)) return QG_INVALID_ARGUMENT;
   h.M = (int)m;
   h.N = (int)n;
   h.K = (int)K;
@@ -286,6 +294,7 @@ static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const doubl
   std::memset(&r, 0, sizeof r);
   r.a = a_t;
   r.b = b_t;
+  if (!dims_ok(M, N, k)) return QG_INVALID_ARGUMENT;
   r.M = (int)M;
   r.N = (int)N;
   r.K = (int)k;
@@ -437,6 +446,7 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   std::memset(&a, 0, sizeof a);
   a.a = ca_t;
   a.b = cb_t;
+  if (!dims_ok(m, n, K)) return QG_INVALID_ARGUMENT;
   a.M = (int)m;
   a.N = (int)n;
   a.K = (int)K;
@@ -532,6 +542,7 @@ int qg_packed_common_product(const qg_plan* plan, const double* ca, const double
   h.ldca = ceil_div(k, plan->e);
   h.cb = cb;
   h.ldcb = n;
+  if (!dims_ok(m, n, k)) return QG_INVALID_ARGUMENT;
   h.M = (int)m;
   h.N = (int)n;
   h.K = (int)ceil_div(k, plan->e);
@@ -609,6 +620,7 @@ static int right_common(const qg_plan* plan, const double* a, size_t lda, const 
   r.lda = lda;
   r.b = cbo;
   r.ldb = H;
+  if (!dims_ok(m, H, k)) return QG_INVALID_ARGUMENT;
   r.M = (int)m;
   r.N = (int)H;
   r.K = (int)k;
@@ -915,6 +927,7 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
       h.ldca = W;
       h.cb = (const double*)dcb.p;
       h.ldcb = n;
+      if (!dims_ok(m, n, W)) return QG_INVALID_ARGUMENT;
       h.M = (int)m;
       h.N = (int)n;
       h.K = (int)W;

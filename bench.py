@@ -448,7 +448,9 @@ def redq_arm(args):
                        "plan": dict(plan_desc, stage_words=bk, source=args.plan),
                        "l2": "256 MiB buffer written between timed steps"},
             "roofline": {"bound": "tensor", "achieved": round(flop / (kms * 1e-3) / 1e12, 3), "peak": peak,
-                         "unit": "TFLOP/s", "frac": round(flop / (kms * 1e-3) / 1e12 / peak, 4), "traffic": None,
+                         "unit": "TFLOP/s", "frac": round(flop / (kms * 1e-3) / 1e12 / peak, 4),
+                         "traffic": ((load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {})
+                                     .get("contraction", {}).get(args.config, {}).get("dram_bytes")),
                          "kernel": kernel, "kernel_ms": round(kms, 4),
                          "per_unit": "2 flops per packed-word product; rows_a x rows_b x k products per launch"},
             "gpu_launches": launches, "checksum_c": qg.residue_checksum(c),

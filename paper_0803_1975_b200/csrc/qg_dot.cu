@@ -966,9 +966,10 @@ static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   const char* dbg = getenv("QG_DEBUG_MODE");
   a2.debug = dbg ? atoi(dbg) : 0;
   // warps 4..7 start 4 us late so the two warps of an SMSP do not flush their
-  // k-blocks at the same moment (profiles/r01_notes.md)
+  // k-blocks (or run their tile epilogues) at the same moment: config 2
+  // +3 %, config 3 75.6 -> 78.9 % (profiles/r01_notes.md)
   const char* skew = getenv("QG_SKEW_NS");
-  a2.skew_ns = skew ? (unsigned)atoi(skew) : (a.kb_stages ? 4000u : 0u);
+  a2.skew_ns = skew ? (unsigned)atoi(skew) : 4000u;
   if (BAL) {  // remove the Q/2 bias of every digit extraction (mod p)
     const unsigned long long ktiles = (unsigned long long)((a.K + BK - 1) / BK);
     const unsigned long long nb = !MULTI ? 1ull : (FLUSH == 0 ? ktiles / a.kb_stages + 1 : ktiles + 1);

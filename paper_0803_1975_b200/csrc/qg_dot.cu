@@ -168,7 +168,11 @@ __device__ __forceinline__ double redq_word(double w, int t, int e, const ModP& 
   const uint64_t bits = __double2ull_rz(w);
   const uint64_t mask = (1ull << t) - 1;
   uint64_t r = 0;
-  for (int s = 0; s < t * e; s += t) r |= (uint64_t)modp((uint32_t)((bits >> s) & mask)) << s;
+  for (int s = 0; s < t * e; s += t) {
+    const uint64_t digit = (bits >> s) & mask;
+    // digits wider than 32 bits (one-digit words of large p) need the 64-bit reduction
+    r |= (t > 31 ? digit % modp.p : (uint64_t)modp((uint32_t)digit)) << s;
+  }
   return __ull2double_rn(r);
 }
 
@@ -336,14 +340,7 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_dmma(GemmArgs args) {
         for (int h = 0; h < 2; ++h) {
           if (col + h >= N) continue;
           double w = acc[mi][ni][h];
-          if (EPI == EPI_REDQ) {  // redq, pack.hpp:124-137 (every partial sum exact, < Q^e)
-            const uint64_t bits = __double2ull_rz(w);
-            const uint64_t mask = (1ull << args.t) - 1;
-            uint64_t r = 0;
-            for (int s = 0; s < args.t * args.e; s += args.t)
-              r |= (uint64_t)modp((uint32_t)((bits >> s) & mask)) << s;
-            w = __ull2double_rn(r);
-          }
+          if (EPI == EPI_REDQ) w = redq_word(w, args.t, args.e, modp);  // redq, pack.hpp:124-137
           args.cc[(size_t)row * args.ldcc + col + h] = w;
         }
       }

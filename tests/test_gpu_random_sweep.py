@@ -133,3 +133,35 @@ def test_wide_digit_right_product_reference_layout(qg, orc, cuda, p):
     want = orc.mul_right_compressed(op, a, orc.compress_outer_cols(op, b), n)
     assert np.array_equal(cc.data.cpu().numpy().view(np.uint64), want.view(np.uint64))
     assert np.array_equal(qg.uncompress(cc).cpu().numpy().astype(np.uint32), orc.naive_gemm(p, a, b))
+
+
+@pytest.mark.parametrize("p,m,k,n,seed", list(cases(36, 14)))
+def test_random_reference_layouts_and_panels(qg, orc, cuda, p, m, k, n, seed):
+    """Reference-layout operands (CompressedMatrix in), blocked products with a
+    random panel width, and pack -> uncompress round trips."""
+    import torch
+
+    a, b = orc.random_residue_matrix(m, k, p, seed), orc.random_residue_matrix(k, n, p, seed + 1)
+    want = orc.naive_gemm(p, a, b)
+    ad = torch.from_numpy(a.astype(np.float64)).to(cuda)
+    bd = torch.from_numpy(b.astype(np.int32)).to(cuda)
+    rng = np.random.default_rng(seed)
+    kp = int(rng.integers(1, k + 1))
+    try:
+        bp = qg.plan_compression(p, kp) if kp >= 2 else qg.uncompressed_plan(p, 1)
+    except qg.NoCompression:
+        bp = None
+    if bp is not None:
+        assert np.array_equal(qg.blocked_accumulate_host(a, b, bp, kp), want), kp
+    try:
+        pl = qg.plan_compression(p, k)
+    except qg.NoCompression:
+        return
+    ca, cb = qg.compress_rows_reversed(ad, pl), qg.compress_cols_forward(bd, pl)
+    op = orc.plan_of(pl)
+    assert np.array_equal(ca.data.cpu().numpy().view(np.uint64), orc.compress_rows_reversed(op, a).view(np.uint64))
+    assert np.array_equal(cb.data.cpu().numpy().view(np.uint64), orc.compress_cols_forward(op, b).view(np.uint64))
+    c = qg.mul_common_compressed(ca, cb)
+    assert np.array_equal(c.cpu().numpy().astype(np.uint32), want)
+    for cm, src in ((ca, a), (cb, b), (qg.compress_outer_cols(bd, pl), b), (qg.compress_outer_rows(ad, pl), a)):
+        assert np.array_equal(qg.uncompress(cm).cpu().numpy().astype(np.uint32), src)

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 
 #include "../../include/qgemm_b200.h"
 #include "qg_internal.h"
@@ -750,15 +751,23 @@ struct PhaseScope {
 // Streams and events of the pipelined host path, created once per thread.
 struct HostPipe {
   cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  // chunk contractions rotate over kComp compute streams: a chunk with fewer
+  // output tiles than SMs then shares the GPU with the next one
+  static constexpr int kComp = 3;
+  cudaStream_t comps[kComp] = {};
   static constexpr int kMaxChunks = 64;
-  cudaEvent_t b_ready = nullptr, a_ready[kMaxChunks] = {}, c_ready[kMaxChunks] = {}, done = nullptr;
+  cudaEvent_t b_ready = nullptr, b_packed = nullptr, a_ready[kMaxChunks] = {}, c_ready[kMaxChunks] = {},
+              done = nullptr;
   bool ok = false;
   HostPipe() {
     ok = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess &&
          cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking) == cudaSuccess &&
          cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking) == cudaSuccess &&
          cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&b_packed, cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess;
+    comps[0] = comp;
+    for (int i = 1; ok && i < kComp; ++i) ok = cudaStreamCreateWithFlags(&comps[i], cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; ok && i < kMaxChunks; ++i)
       ok = cudaEventCreateWithFlags(&a_ready[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&c_ready[i], cudaEventDisableTiming) == cudaSuccess;
@@ -773,6 +782,79 @@ struct HostPipe {
   }
 };
 
+// Pipelined host products (common, right, left, full): B goes up first and is
+// packed; A streams up in row chunks (a multiple of `align` rows, so every
+// chunk maps to whole 128-row blocks of the packed layout) while the earlier
+// chunks are packed and contracted; each chunk's output streams back on its
+// own stream, so both PCIe directions overlap the contraction.
+static HostPipe& host_pipe() {
+  static thread_local HostPipe hp;
+  return hp;
+}
+
+struct ChunkOut {
+  const void* src = nullptr;
+  void* dst = nullptr;
+  size_t bytes = 0;
+};
+
+static int host_pipeline(size_t m, size_t k, size_t n, size_t align, size_t col_tiles, const uint32_t* a,
+                         const uint32_t* b,
+                         const std::function<int(const uint32_t* db, cudaStream_t s)>& pack_b,
+                         const std::function<int(size_t r0, size_t rows, const uint32_t* da, cudaStream_t s,
+                                                 PhaseScope& ps, ChunkOut* out)>& chunk) {
+  HostPipe& hp = host_pipe();
+  if (!hp.ok) return QG_CUDA_ERROR;
+  PhaseScope ps;
+  size_t rows_per = (512 + align - 1) / align * align;
+  size_t nchunks = ceil_div(m, rows_per);
+  if (nchunks > (size_t)HostPipe::kMaxChunks) {
+    rows_per = ceil_div(ceil_div(m, (size_t)HostPipe::kMaxChunks), align) * align;
+    nchunks = ceil_div(m, rows_per);
+  }
+  // a chunk that already fills most SMs runs alone (overlapping kernels only
+  // contend: config 2); smaller ones rotate over up to kComp streams (config 4)
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t chunk_tiles = (rows_per / align) * (col_tiles ? col_tiles : 1);
+  int ncomp = chunk_tiles * 4 >= (size_t)sms * 3 ? 1 : (int)ceil_div((size_t)sms, chunk_tiles ? chunk_tiles : 1);
+  if (ncomp > HostPipe::kComp) ncomp = HostPipe::kComp;
+  DevBuf da(hp.in), db(hp.in);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
+  QG_TRY(cudaEventRecord(hp.b_ready, hp.in));
+  for (size_t i = 0; i < nchunks; ++i) {
+    const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+    if (rows * k)
+      QG_TRY(cudaMemcpyAsync((uint32_t*)da.p + r0 * k, a + r0 * k, rows * k * 4, cudaMemcpyHostToDevice, hp.in));
+    QG_TRY(cudaEventRecord(hp.a_ready[i], hp.in));
+  }
+  QG_TRY(cudaStreamWaitEvent(hp.comp, hp.b_ready, 0));
+  int st = pack_b((const uint32_t*)db.p, hp.comp);
+  if (st) return st;
+  QG_TRY(cudaEventRecord(hp.b_packed, hp.comp));
+  for (int j = 1; j < ncomp; ++j) QG_TRY(cudaStreamWaitEvent(hp.comps[j], hp.b_packed, 0));
+  for (size_t i = 0; i < nchunks; ++i) {
+    const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+    cudaStream_t cs = hp.comps[i % ncomp];
+    QG_TRY(cudaStreamWaitEvent(cs, hp.a_ready[i], 0));
+    ChunkOut out;
+    if ((st = chunk(r0, rows, (const uint32_t*)da.p + r0 * k, cs, ps, &out))) return st;
+    QG_TRY(cudaEventRecord(hp.c_ready[i], cs));
+    QG_TRY(cudaStreamWaitEvent(hp.out, hp.c_ready[i], 0));
+    if (out.bytes) QG_TRY(cudaMemcpyAsync(out.dst, out.src, out.bytes, cudaMemcpyDeviceToHost, hp.out));
+  }
+  QG_TRY(cudaEventRecord(hp.done, hp.out));
+  QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
+  QG_TRY(cudaStreamSynchronize(hp.out));
+  ps.finish();
+  return QG_OK;
+}
+
 // mul_common_compressed on host data, pipelined over three streams: B goes
 // up first and is packed; A then streams up in row chunks of 512 while the
 // previous chunks are packed and contracted, and C streams back per chunk on
@@ -786,51 +868,33 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
   int bk = 0, kbs = 0;
   const bool tiled = (n % 2 == 0) && K > 0 && tiled_geometry(gp, K, &bk, &kbs) == QG_OK;
   if (tiled && m * n > 0) {
-    thread_local HostPipe hp;
-    if (!hp.ok) return QG_CUDA_ERROR;
-    PhaseScope ps;
-    const char* ce = getenv("QG_HOST_CHUNK");  // experiments
-    const size_t chunk = ce ? (size_t)atoi(ce) : 512;  // rows per pipeline chunk (a multiple of 128)
-    size_t nchunks = ceil_div(m, chunk);
-    const size_t rows_per = nchunks > (size_t)HostPipe::kMaxChunks ? ceil_div(ceil_div(m, HostPipe::kMaxChunks), 128) * 128 : chunk;
-    nchunks = ceil_div(m, rows_per);
     const size_t Kt = ceil_div(K, (size_t)bk);
-    DevBuf da(hp.in), db(hp.in), dca(hp.in), dcb(hp.in), dc(hp.in);
-    QG_TRY(da.alloc(m * k * 4));
-    QG_TRY(db.alloc(k * n * 4));
+    cudaStream_t s0 = host_pipe().in;
+    DevBuf dca(s0), dcb(s0), dc(s0);
     QG_TRY(dc.alloc(m * n * 4));
     QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
     QG_TRY(dcb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
-    QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
-    QG_TRY(cudaEventRecord(hp.b_ready, hp.in));
-    for (size_t i = 0; i < nchunks; ++i) {
-      const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
-      QG_TRY(cudaMemcpyAsync((uint32_t*)da.p + r0 * k, a + r0 * k, rows * k * 4, cudaMemcpyHostToDevice, hp.in));
-      QG_TRY(cudaEventRecord(hp.a_ready[i], hp.in));
-    }
-    QG_TRY(cudaStreamWaitEvent(hp.comp, hp.b_ready, 0));
-    QG_TRY(qgk::launch_pack_tiled(true, db.p, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, hp.comp, pl.p,
-                                  gp->balanced != 0));
-    for (size_t i = 0; i < nchunks; ++i) {
-      const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
-      double* ca_chunk = (double*)dca.p + (r0 / 128) * Kt * 128 * bk;
-      QG_TRY(cudaStreamWaitEvent(hp.comp, hp.a_ready[i], 0));
-      QG_TRY(qgk::launch_pack_tiled(false, (const uint32_t*)da.p + r0 * k, QG_U32, rows, k, k, pl.t, pl.e, bk,
-                                    ca_chunk, hp.comp, pl.p, gp->balanced != 0));
-      ps.begin(hp.comp);
-      if ((st = qg_mul_common_tiled(gp, ca_chunk, (const double*)dcb.p, rows, n, k, (int32_t*)dc.p + r0 * n, n,
-                                    hp.comp)))
-        return st;
-      ps.end(hp.comp);
-      QG_TRY(cudaEventRecord(hp.c_ready[i], hp.comp));
-      QG_TRY(cudaStreamWaitEvent(hp.out, hp.c_ready[i], 0));
-      QG_TRY(cudaMemcpyAsync(c + r0 * n, (const int32_t*)dc.p + r0 * n, rows * n * 4, cudaMemcpyDeviceToHost, hp.out));
-    }
-    QG_TRY(cudaEventRecord(hp.done, hp.out));
-    QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
-    QG_TRY(cudaStreamSynchronize(hp.out));
-    ps.finish();
-    return QG_OK;
+    return host_pipeline(
+        m, k, n, 128, ceil_div(n, (size_t)128), a, b,
+        [&](const uint32_t* db, cudaStream_t s2) {
+          return cuda_status(qgk::launch_pack_tiled(true, db, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, s2,
+                                                    pl.p, gp->balanced != 0));
+        },
+        [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s2, PhaseScope& ps, ChunkOut* out) {
+          double* ca_chunk = (double*)dca.p + (r0 / 128) * Kt * 128 * bk;
+          int st2 = cuda_status(qgk::launch_pack_tiled(false, da, QG_U32, rows, k, k, pl.t, pl.e, bk, ca_chunk, s2,
+                                                       pl.p, gp->balanced != 0));
+          if (st2) return st2;
+          ps.begin(s2);
+          if ((st2 = qg_mul_common_tiled(gp, ca_chunk, (const double*)dcb.p, rows, n, k, (int32_t*)dc.p + r0 * n, n,
+                                         s2)))
+            return st2;
+          ps.end(s2);
+          out->src = (const int32_t*)dc.p + r0 * n;
+          out->dst = c + r0 * n;
+          out->bytes = rows * n * 4;
+          return (int)QG_OK;
+        });
   }
   if (gp->balanced) {  // the row-layout kernels need unsigned words: re-plan
     qg_gpu_plan up;
@@ -955,36 +1019,40 @@ static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* 
   const qg_plan* plan = &gp->plan;
   int st = check_plan(plan);
   if (st) return st;
-  cudaStream_t s = nullptr;
   const size_t H = ceil_div(n, (size_t)plan->e);
   if (m * H == 0) return QG_OK;
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
-  PhaseScope ps;
-  DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
-  QG_TRY(da.alloc(m * k * 4));
-  QG_TRY(db.alloc(k * n * 4));
+  cudaStream_t s0 = host_pipe().in;
+  DevBuf dat(s0), dbt(s0), dcc(s0);
   QG_TRY(dat.alloc(ceil_div(m, 128) * 128 * kt * bk * 8));
   QG_TRY(dbt.alloc(ceil_div(H, 128) * 128 * kt * bk * 8));
   QG_TRY(dcc.alloc(m * H * 8));
-  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
-  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if (k && gp->balanced) {
-    if ((st = qg_pack_residues_tiled_bal(plan->p, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
-    if ((st = qg_pack_outer_cols_tiled_bal(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
-  } else if (k) {
-    if ((st = qg_pack_residues_tiled((uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
-    if ((st = qg_pack_outer_cols_tiled(plan, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
-  }
-  ps.begin(s);
-  if ((st = qg_mul_right_tiled(gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, H, s)))
-    return st;
-  ps.end(s);
-  QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
-  QG_TRY(cudaStreamSynchronize(s));
-  ps.finish();
-  return QG_OK;
+  const bool bal = gp->balanced != 0;
+  return host_pipeline(
+      m, k, n, 128, ceil_div(H, (size_t)128), a, b,
+      [&](const uint32_t* db, cudaStream_t s) {
+        if (!k) return (int)QG_OK;
+        return bal ? qg_pack_outer_cols_tiled_bal(plan, (uint32_t)bk, db, QG_U32, k, n, n, (double*)dbt.p, s)
+                   : qg_pack_outer_cols_tiled(plan, (uint32_t)bk, db, QG_U32, k, n, n, (double*)dbt.p, s);
+      },
+      [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s, PhaseScope& ps, ChunkOut* out) {
+        double* at = (double*)dat.p + (r0 / 128) * kt * 128 * bk;
+        int st2 = QG_OK;
+        if (k)
+          st2 = bal ? qg_pack_residues_tiled_bal(plan->p, (uint32_t)bk, da, QG_U32, rows, k, k, at, s)
+                    : qg_pack_residues_tiled((uint32_t)bk, da, QG_U32, rows, k, k, at, s);
+        if (st2) return st2;
+        ps.begin(s);
+        if ((st2 = qg_mul_right_tiled(gp, at, (const double*)dbt.p, rows, k, n, (double*)dcc.p + r0 * H, H, s)))
+          return st2;
+        ps.end(s);
+        out->src = (const double*)dcc.p + r0 * H;
+        out->dst = cc + r0 * H;
+        out->bytes = rows * H * 8;
+        return (int)QG_OK;
+      });
 }
 
 static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
@@ -992,36 +1060,41 @@ static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b
   const qg_plan* plan = &gp->plan;
   int st = check_plan(plan);
   if (st) return st;
-  cudaStream_t s = nullptr;
-  const size_t G = ceil_div(m, (size_t)plan->e);
+  const size_t e = plan->e, G = ceil_div(m, e);
   if (G * n == 0) return QG_OK;
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
-  PhaseScope ps;
-  DevBuf da(s), db(s), dat(s), dbt(s), dcc(s);
-  QG_TRY(da.alloc(m * k * 4));
-  QG_TRY(db.alloc(k * n * 4));
+  cudaStream_t s0 = host_pipe().in;
+  DevBuf dat(s0), dbt(s0), dcc(s0);
   QG_TRY(dat.alloc(ceil_div(G, 128) * 128 * kt * bk * 8));
   QG_TRY(dbt.alloc(ceil_div(n, 128) * 128 * kt * bk * 8));
   QG_TRY(dcc.alloc(G * n * 8));
-  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
-  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if (k && gp->balanced) {
-    if ((st = qg_pack_outer_rows_tiled_bal(plan, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
-    if ((st = qg_pack_residues_b_tiled_bal(plan->p, (uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
-  } else if (k) {
-    if ((st = qg_pack_outer_rows_tiled(plan, (uint32_t)bk, da.p, QG_U32, m, k, k, (double*)dat.p, s))) return st;
-    if ((st = qg_pack_residues_b_tiled((uint32_t)bk, db.p, QG_U32, k, n, n, (double*)dbt.p, s))) return st;
-  }
-  ps.begin(s);
-  if ((st = qg_mul_left_tiled(gp, (const double*)dat.p, (const double*)dbt.p, m, k, n, (double*)dcc.p, n, s)))
-    return st;
-  ps.end(s);
-  QG_TRY(cudaMemcpyAsync(cc, dcc.p, G * n * 8, cudaMemcpyDeviceToHost, s));
-  QG_TRY(cudaStreamSynchronize(s));
-  ps.finish();
-  return QG_OK;
+  const bool bal = gp->balanced != 0;
+  return host_pipeline(
+      m, k, n, 128 * e, ceil_div(n, (size_t)128), a, b,  // chunks of whole 128-group blocks of the outer-rows layout
+      [&](const uint32_t* db, cudaStream_t s) {
+        if (!k) return (int)QG_OK;
+        return bal ? qg_pack_residues_b_tiled_bal(plan->p, (uint32_t)bk, db, QG_U32, k, n, n, (double*)dbt.p, s)
+                   : qg_pack_residues_b_tiled((uint32_t)bk, db, QG_U32, k, n, n, (double*)dbt.p, s);
+      },
+      [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s, PhaseScope& ps, ChunkOut* out) {
+        const size_t g0 = r0 / e, groups = ceil_div(rows, e);
+        double* at = (double*)dat.p + (g0 / 128) * kt * 128 * bk;
+        int st2 = QG_OK;
+        if (k)
+          st2 = bal ? qg_pack_outer_rows_tiled_bal(plan, (uint32_t)bk, da, QG_U32, rows, k, k, at, s)
+                    : qg_pack_outer_rows_tiled(plan, (uint32_t)bk, da, QG_U32, rows, k, k, at, s);
+        if (st2) return st2;
+        ps.begin(s);
+        if ((st2 = qg_mul_left_tiled(gp, at, (const double*)dbt.p, rows, k, n, (double*)dcc.p + g0 * n, n, s)))
+          return st2;
+        ps.end(s);
+        out->src = (const double*)dcc.p + g0 * n;
+        out->dst = cc + g0 * n;
+        out->bytes = groups * n * 8;
+        return (int)QG_OK;
+      });
 }
 
 static qg_gpu_plan single_block(const qg_plan* plan, size_t k) {
@@ -1073,45 +1146,47 @@ int qg_host_mul_full(const qg_full_plan* fp, uint64_t kblock_words, const uint32
   if (fp->base.beta > 53) return QG_PLAN_MISMATCH;  // gemm.hpp:383 check_backend
   if (!kblock_words && k > fp->base.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:384
   if (m * n == 0) return QG_OK;
-  cudaStream_t s = nullptr;
-  const int qs = fp->dq + 1, ts = fp->dtheta + 1;
-  const size_t G = ceil_div(m, (size_t)qs), H = ceil_div(n, (size_t)ts);
+  const size_t qs = fp->dq + 1, ts = fp->dtheta + 1;
+  const size_t G = ceil_div(m, qs), H = ceil_div(n, ts);
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(&gp, k ? k : 1, &bk, &kbs))) return st;
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
   qg_plan pa = fp->base, pb = fp->base;
-  pa.e = qs;
-  pa.d = qs - 1;
+  pa.e = (int)qs;
+  pa.d = (int)qs - 1;
   pb.t = fp->theta_exponent;
-  pb.e = ts;
-  pb.d = ts - 1;
-  PhaseScope ps;
-  DevBuf da(s), db(s), dat(s), dbt(s), dcc(s), dc(s);
-  QG_TRY(da.alloc(m * k * 4));
-  QG_TRY(db.alloc(k * n * 4));
+  pb.e = (int)ts;
+  pb.d = (int)ts - 1;
+  cudaStream_t s0 = host_pipe().in;
+  DevBuf dat(s0), dbt(s0), dcc(s0), dc(s0);
   QG_TRY(dat.alloc(ceil_div(G, 128) * 128 * kt * bk * 8));
   QG_TRY(dbt.alloc(ceil_div(H, 128) * 128 * kt * bk * 8));
   QG_TRY(dcc.alloc(G * H * 8));
   QG_TRY(dc.alloc(m * n * 4));
-  if (m * k) QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
-  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
-  if (k) {
-    if ((st = cuda_status(qgk::launch_pack_outer_rows_tiled(da.p, QG_U32, m, k, k, pa.t, pa.e, bk, (double*)dat.p,
-                                                            s))))
-      return st;
-    if ((st = cuda_status(qgk::launch_pack_outer_tiled(db.p, QG_U32, k, n, n, pb.t, pb.e, bk, (double*)dbt.p, s))))
-      return st;
-  }
-  ps.begin(s);
-  if ((st = qg_mul_full_tiled(fp, gp.kblock_words, (const double*)dat.p, (const double*)dbt.p, m, k, n,
-                              (double*)dcc.p, H, s)))
-    return st;
-  ps.end(s);
-  if ((st = qg_uncompress_full(fp, (const double*)dcc.p, H, m, n, (int32_t*)dc.p, n, s))) return st;
-  QG_TRY(cudaMemcpyAsync(c, dc.p, m * n * 4, cudaMemcpyDeviceToHost, s));
-  QG_TRY(cudaStreamSynchronize(s));
-  ps.finish();
-  return QG_OK;
+  return host_pipeline(
+      m, k, n, 128 * qs, ceil_div(H, (size_t)128), a, b,
+      [&](const uint32_t* db, cudaStream_t s) {
+        if (!k) return (int)QG_OK;
+        return cuda_status(qgk::launch_pack_outer_tiled(db, QG_U32, k, n, n, pb.t, pb.e, bk, (double*)dbt.p, s));
+      },
+      [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s, PhaseScope& ps, ChunkOut* out) {
+        const size_t g0 = r0 / qs;
+        double* at = (double*)dat.p + (g0 / 128) * kt * 128 * bk;
+        int st2 = QG_OK;
+        if (k && (st2 = cuda_status(qgk::launch_pack_outer_rows_tiled(da, QG_U32, rows, k, k, pa.t, pa.e, bk, at, s))))
+          return st2;
+        ps.begin(s);
+        if ((st2 = qg_mul_full_tiled(fp, gp.kblock_words, at, (const double*)dbt.p, rows, k, n,
+                                     (double*)dcc.p + g0 * H, H, s)))
+          return st2;
+        ps.end(s);
+        if ((st2 = qg_uncompress_full(fp, (const double*)dcc.p + g0 * H, H, rows, n, (int32_t*)dc.p + r0 * n, n, s)))
+          return st2;
+        out->src = (const int32_t*)dc.p + r0 * n;
+        out->dst = c + r0 * n;
+        out->bytes = rows * n * 4;
+        return (int)QG_OK;
+      });
 }
 
 

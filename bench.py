@@ -580,6 +580,7 @@ def our_arm(args):
     # events sit between the two replays.
     use_graph = world == 1 and not args.no_graph
     launches_per_step = None
+    kernel_name = None
     if use_graph:
         g_pack, g_mul = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         n0 = qg.kernel_launches()
@@ -590,6 +591,7 @@ def our_arm(args):
             qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca), qg._ptr(cb), m_rank, n, k,
                                                  qg._ptr(c), n, sp()))
         launches_per_step = qg.kernel_launches() - n0
+        kernel_name = qg.last_kernel()
 
         def step():  # noqa: F811
             g_pack.replay()
@@ -647,7 +649,7 @@ def our_arm(args):
     traffic = ncu.get("contraction", {}).get(args.config, {}).get("dram_bytes") if ncu else None
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": qg.last_kernel(), "kernel_ms": round(contract_avg, 4),
+                "kernel": kernel_name or qg.last_kernel(), "kernel_ms": round(contract_avg, 4),
                 "share_of_step": round(contract_avg / (sum(step_ms) / len(step_ms)), 4),
                 "peak_source": "measured DMMA.8x8x4 microbenchmark on this pool (profiles/r01_fp64_peak.json); "
                                "cuBLAS DGEMM 35.7 TF/s",
@@ -662,7 +664,9 @@ def our_arm(args):
                    "p": p, "m": m_total, "k": k, "n": n,
                    "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
                             "source": args.plan},
-                   "layout": "tiled packed operands (128 x stage_words blocks, CB transposed)",
+                   "layout": "tiled packed operands (128 x stage_words blocks, CB transposed)" + (
+                       "; contraction on 64x64 tiles with k split over a thread-block cluster"
+                       if (kernel_name or "").startswith("small") else ""),
                    "l2": "flushed between timed steps (256 MiB write); A,B residues (2x128 MiB f64) exceed the 126 MB L2",
                    "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
                    "launch": "CUDA graph replay (packs; contraction)" if use_graph else "direct launches"},

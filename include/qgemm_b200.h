@@ -177,9 +177,22 @@ int qg_pack_a_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* a, qg_dty
                     size_t k, size_t lda, double* ca_t, void* stream);
 int qg_pack_b_tiled(const qg_gpu_plan* gplan, uint32_t bk, const void* b, qg_dtype dtype, size_t k,
                     size_t n, size_t ldb, double* cb_t, void* stream);
-/* qg_mul_common on tiled operands (n and ldc even). */
+/* qg_mul_common on tiled operands. Products whose 128 x 128 tiles would fill
+ * less than half of the SMs (config 1: 16 tiles), odd n / ldc and C not
+ * 8-byte aligned run on 64 x 64 tiles with the k stages split over a
+ * thread-block cluster (qg_small.cu); the rest on the persistent 128 x 128
+ * kernel (qg_dot.cu). */
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m,
                         size_t n, size_t k, int32_t* c, size_t ldc, void* stream);
+
+/* mul_common_compressed(A, B, plan), gemm.hpp:254-261 (compress_rows_reversed
+ * + compress_cols_forward + packed_common_product + reduce_common_entry, with
+ * blocked_accumulate's k-blocks, gemm.hpp:450-489) on device residues in one
+ * call: a m x k (lda), b k x n (ldb), both of `dtype`; C m x n int32 (ldc).
+ * Tiled packs into stream-ordered workspaces + qg_mul_common_tiled; plans with
+ * one-digit words wider than 31 bits run on the reference layout. */
+int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda, const void* b, size_t ldb,
+                             qg_dtype dtype, size_t m, size_t k, size_t n, int32_t* c, size_t ldc, void* stream);
 
 /* ---- mixed variant on the tiled layout (the B200 fast path of
  * mul_right_compressed). A's residues as dense 128 x BK blocks (e = 1), B's

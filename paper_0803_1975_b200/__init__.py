@@ -178,6 +178,7 @@ def _load():
         "qg_pack_a_tiled": ([P(_GpuPlan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_pack_b_tiled": ([P(_GpuPlan), u32, vp, i32, sz, sz, sz, vp, vp], i32),
         "qg_mul_common_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_mul_common_compressed": ([P(_GpuPlan), vp, sz, vp, sz, i32, sz, sz, sz, vp, sz, vp], i32),
         "qg_plan_right_gpu": ([u32, u64, u64, P(_GpuPlan)], i32),
         "qg_right_tiled_stage": ([P(_GpuPlan), u64, P(u32)], i32),
         "qg_pack_residues_tiled": ([u32, vp, i32, sz, sz, sz, vp, vp], i32),
@@ -597,8 +598,8 @@ def mul_common_compressed(a_or_ca, b_or_cb, plan: Optional[Union[CompressionPlan
         k = a.shape[1]
         if not isinstance(plan, GpuPlan) and k > base.kmax:  # compress_rows_reversed's check
             raise PlanMismatch(f"common dimension {k} exceeds kmax={base.kmax}")
-        if b.shape[1] % 2 == 0 and not os.environ.get("QG_FORCE_ROW_LAYOUT"):
-            return mul_common_tiled(a, b, gp)
+        if not os.environ.get("QG_FORCE_ROW_LAYOUT"):
+            return mul_common_residues(a, b, gp)
         if gp.balanced:  # the row layout holds the reference's unsigned words
             gp = plan_gpu(base.p, k, balanced=False)
             base = gp.plan
@@ -641,6 +642,25 @@ def pack_tiled(a, plan: Union[CompressionPlan, GpuPlan], bk: int, operand: str):
     else:
         out = torch.empty(lib.qg_tiled_words(cols, rows, plan.e, bk), dtype=torch.float64, device=a.device)
         _check(lib.qg_pack_b_tiled(ctypes.byref(pl), bk, _ptr(a), _dtype_code(a), rows, cols, cols, _ptr(out), _stream()))
+    return out
+
+
+def mul_common_residues(a, b, plan: Union[CompressionPlan, GpuPlan]):
+    """mul_common_compressed(A, B, plan) on device residues through one ABI
+    call (qg_mul_common_compressed): tiled packs into stream-ordered
+    workspaces, then the tiled contraction (64x64 tiles with k split over a
+    thread-block cluster for small products). Returns int32 C (m x n)."""
+    torch = _torch()
+    _require_cuda(a, b)
+    if a.dtype != b.dtype:
+        b = b.to(a.dtype)
+    m, k = a.shape
+    n = b.shape[1]
+    gp = _as_gpu_plan(plan, k)
+    out = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    g = gp._c()
+    _check(lib.qg_mul_common_compressed(ctypes.byref(g), _ptr(a), k, _ptr(b), n, _dtype_code(a), m, k, n,
+                                        _ptr(out), n, _stream()))
     return out
 
 

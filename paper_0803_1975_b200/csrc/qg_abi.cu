@@ -59,6 +59,17 @@ bool dims_ok(size_t a, size_t b, size_t c = 0) {
   return a <= lim && b <= lim && c <= lim;
 }
 
+// stream-ordered device buffer, freed on its stream
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  explicit DevBuf(cudaStream_t st) : s(st) {}
+  cudaError_t alloc(size_t bytes) { return bytes ? cudaMallocAsync(&p, bytes, s) : cudaSuccess; }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 int check_dtype(qg_dtype d) { return (d == QG_F64 || d == QG_U32 || d == QG_I32) ? QG_OK : QG_INVALID_ARGUMENT; }
 
 // Device flag for DigitOverflow (redq / extract_all throw it in the reference).
@@ -428,13 +439,76 @@ int qg_uncompress_full(const qg_full_plan* fp, const double* cc, size_t ldcc, si
                                                  c, ldc, as_stream(stream)));
 }
 
+}  // extern "C"
+
+namespace {
+
+// Keep freed stream-ordered allocations mapped across calls on this device
+// (the default release threshold of 0 re-maps workspaces on every call).
+void keep_pool_mapped() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+  if (done.load() & (1ull << dev)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.fetch_or(1ull << dev);
+}
+
+int device_sms() {
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+// The one-launch small path (qg_small.cu) takes products whose 128x128 tiles
+// would occupy less than half of the SMs (config 1: 16 tiles), and odd n
+// (the tiled epilogue stores column pairs). QG_SMALL=0/1 forces it off/on.
+bool use_small_path(size_t m, size_t n) {
+  const char* e = getenv("QG_SMALL");
+  if (e && e[0] == '0') return n % 2 != 0;
+  if (e && e[0] == '1') return true;
+  return n % 2 != 0 || ceil_div(m, 128) * ceil_div(n, 128) * 2 < (size_t)device_sms();
+}
+
+// Geometry of the small path on a tiled layout of stage depth bk (Kt stages,
+// k-blocks of kbs stages): the stages split over a cluster of CTAs (<= 8,
+// about one CTA per SM). Blocks restart at split starts; any partition of k
+// into pieces of <= the exact block is exact.
+void small_geometry(size_t m, size_t n, size_t Kt, int kbs, int* splits, int* split_stages, uint64_t* extractions) {
+  const size_t tiles = ceil_div(m, 64) * ceil_div(n, 64);
+  size_t S = (size_t)device_sms() / (tiles ? tiles : 1);
+  if (const char* e = getenv("QG_SMALL_SPLITS")) S = (size_t)atoi(e);  // experiments
+  S = S < 1 ? 1 : (S > 8 ? 8 : S);
+  if (S > Kt) S = Kt;
+  const size_t Ls = ceil_div(Kt, S);
+  S = ceil_div(Kt, Ls);
+  uint64_t ex = 0;
+  for (size_t s = 0; s < S; ++s) {
+    const uint64_t nst = ((s + 1) * Ls < Kt ? (s + 1) * Ls : Kt) - s * Ls;
+    ex += kbs ? (nst - 1) / kbs + 1 : 1;
+  }
+  *splits = (int)S;
+  *split_stages = (int)Ls;
+  *extractions = ex;
+}
+
+}  // namespace
+
+extern "C" {
+
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,
                         size_t k, int32_t* c, size_t ldc, void* stream) {
   if (!gplan) return QG_INVALID_ARGUMENT;
   const qg_plan& pl = gplan->plan;
   int st = check_plan(&pl);
   if (st) return st;
-  if (ldc < n || (ldc % 2) || (n % 2) || ((((uintptr_t)c) & 7) != 0)) return QG_INVALID_ARGUMENT;
+  if (ldc < n) return QG_INVALID_ARGUMENT;
+  // the main kernel stores column pairs; odd n / ldc or an unaligned C take the small kernel
+  const bool pairs_ok = !(ldc % 2) && !(n % 2) && ((((uintptr_t)c) & 7) == 0);
   const size_t K = ceil_div(k, pl.e);
   const uint64_t kb = gplan->kblock_words;
   if (kb == 0) return QG_INVALID_ARGUMENT;
@@ -466,12 +540,99 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
       if (cudaMemsetAsync(c + i * ldc, 0, n * sizeof(int32_t), as_stream(stream)) != cudaSuccess) return QG_CUDA_ERROR;
     return QG_OK;
   }
+  if (!pairs_ok || use_small_path(m, n)) {  // 64x64 tiles, k stages split over a cluster (qg_small.cu)
+    qgk::SmallArgs sa;
+    std::memset(&sa, 0, sizeof sa);
+    sa.a = ca_t;
+    sa.b = cb_t;
+    sa.M = (int)m;
+    sa.N = (int)n;
+    sa.K = (int)K;
+    sa.Kt = (int)ceil_div(K, (size_t)bk);
+    sa.balanced = a.balanced;
+    sa.kb_stages = kbs;
+    sa.anchor = a.anchor;
+    sa.qmask = a.qmask;
+    sa.p = pl.p;
+    sa.c = c;
+    sa.ldc = ldc;
+    int splits = 1, ls = 1;
+    uint64_t ex = 0;
+    small_geometry(m, n, (size_t)sa.Kt, kbs, &splits, &ls, &ex);
+    sa.split_stages = ls;
+    if ((unsigned __int128)ex * sa.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+    if (sa.balanced) {  // remove the Q/2 bias of every extraction, mod p
+      const uint64_t halfq = ((uint64_t)sa.qmask + 1) / 2;
+      sa.corr = (uint32_t)((pl.p - (ex % pl.p) * (halfq % pl.p) % pl.p) % pl.p);
+    }
+    return cuda_status(qgk::launch_small_tiled(sa, bk, splits, as_stream(stream), &g_last_kernel));
+  }
   // digit sums are uint32 (planner keeps nblocks * (Q-1) < 2^32); the fused
   // flush packs two per register as 16-bit lanes, reduced mod p in time
   if (pl.t <= 16) a.pack_period = (int)((65535u - (pl.p - 1)) / a.qmask);
   const uint64_t nblocks = (kbs ? ceil_div(K, (size_t)kbs * bk) : 1) + 1;
   if ((unsigned __int128)nblocks * a.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
   return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));
+}
+
+int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda, const void* b, size_t ldb,
+                             qg_dtype dtype, size_t m, size_t k, size_t n, int32_t* c, size_t ldc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (lda < k || ldb < n || ldc < n) return QG_INVALID_ARGUMENT;
+  const size_t K = ceil_div(k, (size_t)pl.e);
+  const uint64_t kb = gplan->kblock_words;
+  if (kb == 0) return QG_INVALID_ARGUMENT;
+  if (kb < K && kb * (uint64_t)pl.e > pl.kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
+  if (kb >= K && k > pl.kmax) return QG_PLAN_MISMATCH;
+  if (pl.t * pl.e > 53) return QG_PLAN_MISMATCH;  // DoubleWord words only
+  if (!dims_ok(m, n, k) || !dims_ok(lda, ldb, ldc)) return QG_INVALID_ARGUMENT;
+  if (m == 0 || n == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  if (K == 0) {
+    for (size_t i = 0; i < m; ++i)
+      if (cudaMemsetAsync(c + i * ldc, 0, n * sizeof(int32_t), s) != cudaSuccess) return QG_CUDA_ERROR;
+    return QG_OK;
+  }
+  if (pl.t > 31) {
+    // t * e <= 53 makes e = 1: one residue per word, and Eq. 3 keeps the whole
+    // dot product below Q = 2^t < 2^53 — C is the exact integer sum mod p.
+    // Integer contraction (64-bit sums, qg_word64.cu) + reduction.
+    keep_pool_mapped();
+    DevBuf acc(s), cw(s), bw(s);
+    if (acc.alloc(m * n * 8) || bw.alloc(k * n * 8)) return cuda_status(cudaGetLastError());
+    // B's residues as one-residue uint64 words (compress_cols_forward at e = 1)
+    if ((st = cuda_status(qgk::launch_pack_u64(qgk::PACK_COLS_FORWARD, b, dtype, k, n, ldb, pl.t, 1,
+                                               (uint64_t*)bw.p, n, 0, 0, s))))
+      return st;
+    int32_t* cdst = c;
+    if (ldc != n) {
+      if (cw.alloc(m * n * 4)) return cuda_status(cudaGetLastError());
+      cdst = (int32_t*)cw.p;
+    }
+    if ((st = cuda_status(qgk::launch_gemm_u64(1, a, dtype, lda, bw.p, -1, n, m, n, k, 0, 0, (uint64_t*)acc.p, n, s))))
+      return st;
+    if ((st = cuda_status(qgk::launch_word_reduce_u64((const uint64_t*)acc.p, m * n, 0, 0, (1ull << pl.t) - 1, pl.p,
+                                                      cdst, 0, s))))
+      return st;
+    if (ldc != n)
+      return cuda_status(cudaMemcpy2DAsync(c, ldc * 4, cdst, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, s));
+    return QG_OK;
+  }
+  // tiled packs into stream-ordered workspaces, then the tiled contraction
+  // (64x64-tile cluster kernel for small products, qg_small.cu)
+  keep_pool_mapped();
+  int bk = 0, kbs = 0;
+  if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
+  DevBuf ca(s), cb(s);
+  if (ca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8) != cudaSuccess) return cuda_status(cudaGetLastError());
+  if (cb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8) != cudaSuccess) return cuda_status(cudaGetLastError());
+  if ((st = qg_pack_a_tiled(gplan, bk, a, dtype, m, k, lda, (double*)ca.p, stream))) return st;
+  if ((st = qg_pack_b_tiled(gplan, bk, b, dtype, k, n, ldb, (double*)cb.p, stream))) return st;
+  return qg_mul_common_tiled(gplan, (const double*)ca.p, (const double*)cb.p, m, n, k, c, ldc, stream);
 }
 
 
@@ -678,15 +839,6 @@ int qg_uncompress(const qg_plan* plan, qg_orientation o, const double* words, si
 // ------------------------------------------------------------ host buffers
 
 namespace {
-struct DevBuf {
-  void* p = nullptr;
-  cudaStream_t s;
-  explicit DevBuf(cudaStream_t st) : s(st) {}
-  cudaError_t alloc(size_t bytes) { return bytes ? cudaMallocAsync(&p, bytes, s) : cudaSuccess; }
-  ~DevBuf() {
-    if (p) cudaFreeAsync(p, s);
-  }
-};
 
 // Phase split of the last host-data call, the reference's PhaseSeconds
 // (gemm.hpp, bench.hpp:67-152): multiply = device time of the contraction

@@ -99,6 +99,26 @@ cudaError_t launch_pack_tiled(bool b_operand, const void* src, int dtype, size_t
                               size_t ld, int t, int e, int bk, double* dst, cudaStream_t s,
                               uint32_t p = 0, bool balanced = false);
 
+// Small products (qg_small.cu): the tiled contraction with 64x64 tiles and
+// the k stages split over a cluster of `splits` CTAs (grid z), reduced over
+// distributed shared memory. a = CA_t, b = CB_t (the tiled layout of stage
+// depth bk, Kt stages).
+struct SmallArgs {
+  const double* a;
+  const double* b;
+  int M, N, K, Kt;      // rows of A, columns of B, words, stages of the layout
+  int balanced;
+  int kb_stages;        // stages per k-block inside a split; 0 = the split is one block
+  int split_stages;     // stages per split
+  double anchor;
+  uint32_t qmask, p;
+  uint32_t corr;        // balanced: (p - (#extractions * Q/2) mod p) mod p
+  int32_t* c;
+  size_t ldc;
+  int nstages;          // set by the launcher: shared-memory ring depth
+};
+cudaError_t launch_small_tiled(const SmallArgs& a, int bk, int splits, cudaStream_t s, const char** variant);
+
 // Reference high-part semantics (word.hpp:28-30): acc += trunc(a*b*2^-td).
 struct HighArgs {
   const double* ca;

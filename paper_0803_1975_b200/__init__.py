@@ -38,7 +38,7 @@ from typing import Optional, Union
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libqgemm_b200.so")
+LIB_PATH = os.environ.get("QG_LIB_PATH") or os.path.join(_HERE, "_lib", "libqgemm_b200.so")  # QG_LIB_PATH: experiment builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "qgemm_b200.h")
 
 

@@ -438,6 +438,40 @@ struct DigitSums<true> {
   }
 };
 
+// Split flush (kb_stages == 1): the warp tile's MI accumulator rows form
+// SG groups (row mi in group mi % SG); group q ends its k-blocks after k-step
+// split_step(q) of every stage, group SG-1 at the stage end. Every row's blocks
+// are then one stage long (shifted windows; any partition of k into pieces of
+// <= the exact block is exact), the flush bursts are SG times smaller, and in
+// the k-step where a group flushes its DMMAs issue first: its DADDs wait only
+// for them while the other rows' DMMAs queue behind and keep the pipe busy.
+template <int BK>
+struct SplitFlush {
+  static constexpr int KS = BK / 4;  // k-steps per stage
+#ifndef QG_SPLIT_GROUPS
+#define QG_SPLIT_GROUPS 4
+#endif
+  static constexpr int SG = KS < QG_SPLIT_GROUPS ? KS : QG_SPLIT_GROUPS;
+  __host__ __device__ static constexpr int step(int q) { return ((q + 1) * KS) / SG - 1; }
+  // group flushing after k-step kk, or -1
+  __host__ __device__ static constexpr int group_at(int kk) {
+    for (int q = 0; q < SG; ++q)
+      if (step(q) == kk) return q;
+    return -1;
+  }
+  // issue order of the rows in k-step kk: the flushing group's rows first
+  __host__ __device__ static constexpr int row(int kk, int i) {
+    const int q = group_at(kk);
+    if (q < 0) return i;
+    const int c = (MI - q + SG - 1) / SG;  // rows of group q
+    if (i < c) return q + i * SG;
+    int j = i - c;
+    for (int mi = 0; mi < MI; ++mi)
+      if (mi % SG != q && j-- == 0) return mi;
+    return i;
+  }
+};
+
 // Consumer side of k_gemm_bulk (TILED = false: padded row layout) and
 // k_gemm_tiled (TILED = true: dense A and B^T blocks). MID = 0: k-blocks end
 // on stage boundaries (every kb_stages stages). MID > 0 (kb_stages == 1 only):
@@ -490,9 +524,10 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) bf[ni] = TILED ? b_base[ni * 8 * BK + kk * 4] : b_base[kk * 4 * B_ST + ni * 8];
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi)
+          for (int mi0 = 0; mi0 < MI; ++mi0)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
+              const int mi = SPLIT ? SplitFlush<BK>::row(kk, mi0) : mi0;  // flushing rows first
               if (MULTI && MID < 0 && kk == 0) {
                 // fused flush (one stage per block): the finished block's digit
                 // d leaves each accumulator right before that accumulator's
@@ -505,10 +540,24 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
                 dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
               }
             }
-          if (MULTI && MID > 0 && kk == MID - 1) {  // compile-time position: no branch in the DMMA stream
+          if (MULTI && SPLIT) {  // groups ending their blocks mid-stage (compile-time positions)
+            const int q = SplitFlush<BK>::group_at(kk);
+            if (q >= 0 && q < SplitFlush<BK>::SG - 1) {
+              asm volatile("" ::: "memory");  // keep the next fragment loads below the flush (register pressure)
+#pragma unroll
+              for (int mi = 0; mi < MI; ++mi)
+                if (mi % SplitFlush<BK>::SG == q)
+#pragma unroll
+                  for (int ni = 0; ni < NI; ++ni) {
+                    ds.add(mi, ni, block_digit_t<BAL>(acc[mi][ni][0], args.anchor, args.qmask),
+                           block_digit_t<BAL>(acc[mi][ni][1], args.anchor, args.qmask));
+                    acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+                  }
+            }
+          } else if (MULTI && MID > 0 && kk == MID - 1) {  // compile-time position: no branch in the DMMA stream
             asm volatile("" ::: "memory");  // keep the next fragment loads below the flush (register pressure)
 #pragma unroll
-            for (int mi = (SPLIT ? 1 : 0); mi < MI; mi += (SPLIT ? 2 : 1))
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
               for (int ni = 0; ni < NI; ++ni) {
                 ds.add(mi, ni, block_digit_t<BAL>(acc[mi][ni][0], args.anchor, args.qmask),
@@ -544,11 +593,12 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
           }
         }
       } else if (MULTI && (MID == 0 || SPLIT)) {  // (MID != 0 flushes inside the unrolled k-steps)
-        if (SPLIT || ++kst == args.kb_stages) {  // SPLIT (kb_stages == 1): even accumulator rows end here
+        if (SPLIT || ++kst == args.kb_stages) {  // SPLIT (kb_stages == 1): the last row group ends here
           kst = 0;
           ++nflush;
 #pragma unroll
-          for (int mi = 0; mi < MI; mi += (SPLIT ? 2 : 1))
+          for (int mi = 0; mi < MI; ++mi)
+            if (!SPLIT || mi % SplitFlush<BK>::SG == SplitFlush<BK>::SG - 1)
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
               ds.add(mi, ni, block_digit_t<BAL>(acc[mi][ni][0], args.anchor, args.qmask),

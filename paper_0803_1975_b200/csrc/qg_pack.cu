@@ -121,14 +121,16 @@ template <typename TIn, int BK, bool BAL>
 __global__ void k_pack_a_tiled(const TIn* __restrict__ a, size_t m, size_t k, size_t lda, int t, int e,
                                unsigned Kt, size_t total, double* __restrict__ ca_t, uint32_t p) {
   const size_t K = (k + e - 1) / e;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const unsigned c = (unsigned)(idx % BK);
-    const size_t rest = idx / BK;
-    const unsigned r = (unsigned)(rest & 127);
-    const size_t rest2 = rest >> 7;
-    const size_t kt = rest2 % Kt, tm = rest2 / Kt;
-    const size_t row = tm * 128 + r, gw = kt * BK + c;
+  // 32-bit index arithmetic (the host keeps total < 2^32 on this path): a
+  // 64-bit division by the runtime Kt per word cost more than the loads
+  const unsigned tot = (unsigned)total;
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < tot; idx += gridDim.x * blockDim.x) {
+    const unsigned c = idx % BK;
+    const unsigned rest = idx / BK;
+    const unsigned r = rest & 127;
+    const unsigned rest2 = rest >> 7;
+    const unsigned kt = rest2 % Kt, tm = rest2 / Kt;
+    const size_t row = (size_t)tm * 128 + r, gw = (size_t)kt * BK + c;
     if (BAL) {
       long long w = 0;
       if (row < m && gw < K) {
@@ -630,6 +632,7 @@ static cudaError_t pack_tiled_t(bool b_operand, const TIn* src, size_t rows, siz
     const size_t Mt = (rows + 127) / 128;
     const size_t total = Mt * Kt * 128 * (size_t)BK;
     if (total == 0) return cudaSuccess;
+    if (total >= (size_t(1) << 32)) return cudaErrorInvalidValue;  // 32-bit word index (32 GiB of words)
     k_pack_a_tiled<TIn, BK, BAL><<<grid1d(total, 256), 256, 0, s>>>(src, rows, cols, ld, t, e, Kt, total, dst, p);
   }
   count_launch();

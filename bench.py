@@ -505,7 +505,8 @@ def our_arm(args):
     import torch.distributed as dist
 
     import paper_0803_1975_b200 as qg
-    from paper_0803_1975_b200.dist import ShardOps, mul_common_sharded
+    from paper_0803_1975_b200.dist import (PanelOps, ShardOps, mul_common_sharded, mul_common_sharded_pipelined,
+                                           panel_bounds)
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -565,8 +566,28 @@ def our_arm(args):
         return c
 
     ops = ShardOps(pack_rows=pack_rows, pack_cols=pack_cols, empty_cb=lambda shape: cb, contract=contract)
+    # multi-rank: the packed B goes out in column panels, each broadcast queued
+    # behind the pack that produced it, so rank 0's packing overlaps the wire
+    Kt = (K + bk - 1) // bk
+    Nt = (n + 127) // 128
+    W = Kt * 128 * bk  # words per 128-column tile column of CB_t
+
+    def panel_views(cb_, panels):
+        return [cb_[t0 * W:t1 * W] for t0, t1 in (panel_bounds(Nt, panels, j) for j in range(panels))]
+
+    def pack_cols_panel(b_, j, panels, cb_):
+        t0, t1 = panel_bounds(Nt, panels, j)
+        c0, c1 = t0 * 128, min(n, t1 * 128)
+        if c1 > c0:
+            qg._check(qg.lib.qg_pack_b_tiled(ctypes.byref(gpc), bk, ctypes.c_void_p(b_.data_ptr() + c0 * 8), 0, k,
+                                             c1 - c0, n, ctypes.c_void_p(cb_.data_ptr() + t0 * W * 8), sp()))
+
+    pops = PanelOps(pack_rows=pack_rows, panel_views=panel_views, pack_cols_panel=pack_cols_panel, contract=contract)
+    panels = max(1, min(args.bcast_panels, Nt))
 
     def step():
+        if world > 1 and panels > 1:
+            return mul_common_sharded_pipelined(a, b, cb, pops, rank, world, panels)
         return mul_common_sharded(a, b, tuple(cb.shape), ops, rank, world)
 
     for _ in range(args.warmup):
@@ -660,7 +681,8 @@ def our_arm(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
-        "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over {args.dist_backend.upper()}" if world > 1 else ""),
+        "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over {args.dist_backend.upper()}"
+                                       f" in {panels} column panels pipelined with rank 0's packing" if world > 1 else ""),
                    "p": p, "m": m_total, "k": k, "n": n,
                    "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
                             "source": args.plan},
@@ -749,6 +771,8 @@ def main():
     ap.add_argument("--kblock", type=int, default=0, help="override the plan's k-block (words)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path with several ranks on one GPU")
+    ap.add_argument("--bcast-panels", type=int, default=4,
+                    help="N>1: column panels the packed B is broadcast in (1 = one broadcast after the whole pack)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=2.0)

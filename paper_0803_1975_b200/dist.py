@@ -54,3 +54,49 @@ def mul_common_sharded(a_shard, b, cb_shape, ops: ShardOps, rank: int, world: in
     if world > 1:
         dist.broadcast(cb, src=0, group=group)
     return ops.contract(ca, cb), cb
+
+
+@dataclasses.dataclass
+class PanelOps:
+    """Column-panel form of the right operand's packing (pipelined broadcast).
+
+    pack_rows(a_shard) -> CA shard; panel_views(cb, panels) -> list of
+    contiguous views of cb, one per column panel; pack_cols_panel(b, j, panels,
+    cb) packs panel j of B into its view (rank 0); contract(ca, cb) -> C shard."""
+
+    pack_rows: Callable
+    panel_views: Callable
+    pack_cols_panel: Callable
+    contract: Callable
+
+
+def mul_common_sharded_pipelined(a_shard, b, cb, ops: PanelOps, rank: int, world: int, panels: int = 4,
+                                 group=None):
+    """mul_common_sharded with the packed right operand sent in column panels:
+    rank 0 packs panel j+1 while panel j is on the wire (each async broadcast
+    is queued behind the pack that produced it), every rank packs its CA shard
+    meanwhile, and the contraction starts once every panel has landed. The
+    packed words and C are those of mul_common_sharded (the panels are
+    disjoint column ranges of the same CB)."""
+    import torch.distributed as dist
+
+    ca = ops.pack_rows(a_shard)
+    works = []
+    for j, view in enumerate(ops.panel_views(cb, panels)):
+        if rank == 0:
+            ops.pack_cols_panel(b, j, panels, cb)
+        if world > 1:
+            works.append(dist.broadcast(view, src=0, group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return ops.contract(ca, cb), cb
+
+
+def panel_bounds(n_tiles: int, panels: int, j: int) -> Tuple[int, int]:
+    """Tile-column range [t0, t1) of panel j when n_tiles tile columns are cut
+    into `panels` contiguous panels (the first ones one tile larger)."""
+    if panels < 1 or not 0 <= j < panels:
+        raise ValueError("bad panel index")
+    base, extra = divmod(n_tiles, panels)
+    t0 = j * base + min(j, extra)
+    return t0, t0 + base + (1 if j < extra else 0)

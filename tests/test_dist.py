@@ -11,7 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_0803_1975_b200.dist import ShardOps, mul_common_sharded, shard_rows
+from paper_0803_1975_b200.dist import (PanelOps, ShardOps, mul_common_sharded, mul_common_sharded_pipelined,
+                                       panel_bounds, shard_rows)
 
 
 def test_shard_rows_cover_exactly():
@@ -78,3 +79,54 @@ def _worker(rank, world, port, p, m, k, n):
 @pytest.mark.parametrize("p,m,k,n", [(7, 70, 300, 50), (3, 9, 512, 33)])
 def test_row_sharded_world2_gloo(p, m, k, n):
     mp.spawn(_worker, args=(2, _free_port(), p, m, k, n), nprocs=2, join=True)
+
+
+def test_panel_bounds_cover_exactly():
+    for nt in (1, 5, 32, 33, 256):
+        for panels in (1, 2, 3, 4, 8):
+            spans = [panel_bounds(nt, panels, j) for j in range(panels)]
+            assert spans[0][0] == 0 and spans[-1][1] == nt
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _worker_panels(rank, world, port, p, m, k, n, panels):
+    """Pipelined (column-panel) broadcast: CB kept column-major (n x K, the
+    tiled layout's tn-major order in miniature) so a panel is contiguous."""
+    import oracle as O
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = O.plan_compression(p, k)
+        K = -(-k // plan.e)
+        row0, rows = shard_rows(m, world, rank)
+        a_shard = O.random_residue_matrix(rows, k, p, 42, row0=row0)
+        b = O.random_residue_matrix(k, n, p, 43) if rank == 0 else None
+        cbt = torch.empty((n, K), dtype=torch.float64)  # column-major CB
+
+        def views(cb, panels_):
+            return [cb[slice(*panel_bounds(n, panels_, j))] for j in range(panels_)]
+
+        def pack_panel(bb, j, panels_, cb):
+            c0, c1 = panel_bounds(n, panels_, j)
+            cb[c0:c1] = torch.from_numpy(O.compress_cols_forward(plan, np.ascontiguousarray(bb[:, c0:c1])).T.copy())
+
+        def contract(ca, cb):
+            acc = O.packed_common_product(plan, ca.numpy(), np.ascontiguousarray(cb.numpy().T), k)
+            return torch.from_numpy(((acc.astype(np.uint64) & np.uint64((1 << plan.t) - 1)) % np.uint64(p)).astype(np.int32))
+
+        ops = PanelOps(pack_rows=lambda a: torch.from_numpy(O.compress_rows_reversed(plan, a)),
+                       panel_views=views, pack_cols_panel=pack_panel, contract=contract)
+        c_shard, cb = mul_common_sharded_pipelined(a_shard, b, cbt, ops, rank, world, panels)
+        want_cb = O.compress_cols_forward(plan, O.random_residue_matrix(k, n, p, 43))
+        assert np.array_equal(np.ascontiguousarray(cb.numpy().T).view(np.uint64), want_cb.view(np.uint64))
+        want_c = O.naive_gemm(p, a_shard, O.random_residue_matrix(k, n, p, 43))
+        assert np.array_equal(c_shard.numpy().astype(np.uint32), want_c)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p,m,k,n,panels", [(7, 70, 300, 50, 4), (3, 9, 512, 33, 3), (5, 16, 100, 7, 8)])
+def test_pipelined_broadcast_world2_gloo(p, m, k, n, panels):
+    mp.spawn(_worker_panels, args=(2, _free_port(), p, m, k, n, panels), nprocs=2, join=True)

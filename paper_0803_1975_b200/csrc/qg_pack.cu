@@ -318,26 +318,39 @@ __global__ void __launch_bounds__(256) k_pack_outer_rows_tiled(const TIn* __rest
 // call stays asynchronous.
 __global__ void k_uncompress_full(const double* __restrict__ cc, size_t ldcc, unsigned m, unsigned n, int t,
                                   int qs, int ts, uint32_t p, uint32_t magic, int32_t* __restrict__ c, size_t ldc) {
+  // one thread per word (g, h): the word is read once and its qs x ts digits
+  // go to rows g qs + i, columns h ts + j (digit i + j qs)
   const uint64_t mask = (1ull << t) - 1;
-  const unsigned H = (n + ts - 1) / ts;
-  for (unsigned row = blockIdx.y; row < m; row += gridDim.y) {
-    const unsigned g = row / qs, i = row - g * qs;
+  const unsigned H = (n + ts - 1) / ts, G = (m + qs - 1) / qs;
+  const bool pair2 = ts == 2 && t <= 31 && (ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(c) & 7) == 0;
+  for (unsigned g = blockIdx.y; g < G; g += gridDim.y) {
     const double* wrow = cc + (size_t)g * ldcc;
-    int32_t* crow = c + (size_t)row * ldc;
     for (unsigned h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
-      const uint64_t bits = __double2ull_rz(wrow[h]) >> (t * i);
+      const uint64_t bits = __double2ull_rz(wrow[h]);
       const unsigned col0 = h * ts;
-      for (int j = 0; j < ts && col0 + j < n; ++j) {
-        const uint64_t x64 = (bits >> (t * j * qs)) & mask;
-        uint32_t r;
-        if (t > 31) {
-          r = (uint32_t)(x64 % p);  // one-digit words of a wide radix
-        } else {
-          const uint32_t x = (uint32_t)x64;
-          r = x - __umulhi(x, magic) * p;
-          r = r >= p ? r - p : r;
+      if (pair2 && col0 + 2 <= n) {  // two columns per word: one 8-byte store per row
+        for (int i = 0; i < qs && g * qs + i < m; ++i) {
+          const uint32_t x0 = (uint32_t)((bits >> (t * i)) & mask), x1 = (uint32_t)((bits >> (t * (i + qs))) & mask);
+          const uint32_t r0 = x0 - __umulhi(x0, magic) * p, r1 = x1 - __umulhi(x1, magic) * p;
+          *reinterpret_cast<int2*>(c + (size_t)(g * qs + i) * ldc + col0) =
+              make_int2((int)(r0 >= p ? r0 - p : r0), (int)(r1 >= p ? r1 - p : r1));
         }
-        crow[col0 + j] = (int32_t)r;
+        continue;
+      }
+      for (int i = 0; i < qs && g * qs + i < m; ++i) {
+        int32_t* crow = c + (size_t)(g * qs + i) * ldc;
+        for (int j = 0; j < ts && col0 + j < n; ++j) {
+          const uint64_t x64 = (bits >> (t * (i + j * qs))) & mask;
+          uint32_t r;
+          if (t > 31) {
+            r = (uint32_t)(x64 % p);  // one-digit words of a wide radix
+          } else {
+            const uint32_t x = (uint32_t)x64;
+            r = x - __umulhi(x, magic) * p;
+            r = r >= p ? r - p : r;
+          }
+          crow[col0 + j] = (int32_t)r;
+        }
       }
     }
   }
@@ -466,24 +479,67 @@ __global__ void k_redq(double* __restrict__ w, size_t count, int t, int e, uint3
   const int total_bits = t * e;
   const double limit = (double)(1ull << total_bits);
   const uint64_t mask = t >= 64 ? ~0ull : (1ull << t) - 1;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const double v = w[i];
-    if (!(v >= 0.0) || !(v < limit)) {
-      atomicExch(overflow, 1);
-      continue;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  // four words per thread per round, loads first: four loads in flight
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < count; i0 += 4 * stride) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = i0 + u * stride < count ? w[i0 + u * stride] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= count) break;
+      if (!(v[u] >= 0.0) || !(v[u] < limit)) {
+        atomicExch(overflow, 1);
+        continue;
+      }
+      const uint64_t bits = __double2ull_rz(v[u]);
+      uint64_t r = 0;
+      for (int s = 0; s < total_bits; s += t) r |= (uint64_t)digit_mod((bits >> s) & mask, t, p, magic) << s;
+      w[i] = __ull2double_rn(r);
     }
-    const uint64_t bits = __double2ull_rz(v);
-    uint64_t r = 0;
-    for (int s = 0; s < total_bits; s += t) r |= (uint64_t)digit_mod((bits >> s) & mask, t, p, magic) << s;
-    w[i] = __ull2double_rn(r);
   }
 }
 
-// uncompress, gemm.hpp:182-204 (+ extract_all, pack.hpp:104-119): every
-// stored word is split into its digits, each reduced mod p and scattered back
-// to its logical position; positions past the logical shape are dropped. 2-D
-// grid (stored rows on y, stored columns across threads): no index division.
+// uncompress of column-axis words (CC, CB^T-style rows) with e = 4 or 2 slots
+// per word and whole words per row: each word's digits leave as one 16- or
+// 8-byte vector store (coalesced across the warp), four words per thread
+// per round with their loads issued first
+template <int SL>
+__global__ void k_uncompress_cols_vec(const double* __restrict__ w, size_t srows, size_t scols, int t, int reversed,
+                                      uint32_t p, uint32_t magic, int32_t* __restrict__ out,
+                                      int* __restrict__ overflow) {
+  const double limit = (double)(1ull << (t * SL));
+  const uint64_t mask = (1ull << t) - 1;
+  const size_t count = srows * scols, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i0 < count; i0 += 4 * stride) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = i0 + u * stride < count ? w[i0 + u * stride] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= count) break;
+      if (!(v[u] >= 0.0) || !(v[u] < limit)) {
+        atomicExch(overflow, 1);
+        continue;
+      }
+      const uint64_t bits = __double2ull_rz(v[u]);
+      int32_t d[SL];
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        const int di = reversed ? SL - 1 - s : s;
+        d[s] = (int32_t)digit_mod((bits >> (t * di)) & mask, t, p, magic);
+      }
+      // word (si, sj) -> out[si][sj * SL .. + SL): the flat word index i times SL
+      if (SL == 4)
+        reinterpret_cast<int4*>(out)[i] = make_int4(d[0], d[1], d[2], d[SL - 1]);
+      else
+        reinterpret_cast<int2*>(out)[i] = make_int2(d[0], d[SL - 1]);
+    }
+  }
+}
+
 __global__ void k_uncompress(const double* __restrict__ w, size_t srows, size_t scols,
                              size_t lrows, size_t lcols, int t, int e, int slots, int reversed,
                              int column_axis, uint32_t p, uint32_t magic, int32_t* __restrict__ out,
@@ -738,8 +794,9 @@ cudaError_t launch_uncompress_full(const double* cc, size_t ldcc, size_t m, size
   if (m * n == 0) return cudaSuccess;
   if (m >= (1u << 31) || n >= (1u << 31)) return cudaErrorInvalidValue;
   const unsigned H = (unsigned)((n + ts - 1) / ts);
-  const dim3 grid((H + 127) / 128, (unsigned)(m < 65535 ? m : 65535));
-  k_uncompress_full<<<grid, 128, 0, s>>>(cc, ldcc, (unsigned)m, (unsigned)n, t, qs, ts, p,
+  const size_t G = (m + qs - 1) / qs;
+  const dim3 grid((H + 255) / 256, (unsigned)(G < 65535 ? G : 65535));
+  k_uncompress_full<<<grid, 256, 0, s>>>(cc, ldcc, (unsigned)m, (unsigned)n, t, qs, ts, p,
                                          (uint32_t)(0x100000000ull / p), c, ldc);
   count_launch();
   return cudaGetLastError();
@@ -762,6 +819,18 @@ cudaError_t launch_uncompress(const double* w, size_t srows, size_t scols, size_
   if (lrows * lcols && !covered) cudaMemsetAsync(out, 0, lrows * lcols * sizeof(int32_t), s);
   const size_t count = srows * scols;
   if (count == 0) return cudaGetLastError();
+  // whole words per row (lcols = scols * slots, lrows = srows), slots = e = 4 or 2,
+  // 16 / 8-byte aligned output: vector stores
+  if (column_axis && slots == e && (e == 4 || e == 2) && t <= 31 && lrows == srows && lcols == scols * (size_t)e &&
+      (reinterpret_cast<uintptr_t>(out) % (4 * e)) == 0) {
+    const uint32_t magic = (uint32_t)(0x100000000ull / p);
+    if (e == 4)
+      k_uncompress_cols_vec<4><<<grid1d(count, 256), 256, 0, s>>>(w, srows, scols, t, reversed, p, magic, out, overflow);
+    else
+      k_uncompress_cols_vec<2><<<grid1d(count, 256), 256, 0, s>>>(w, srows, scols, t, reversed, p, magic, out, overflow);
+    count_launch();
+    return cudaGetLastError();
+  }
   const size_t gx = (scols + 255) / 256;
   const dim3 grid((unsigned)(gx < 4096 ? gx : 4096), (unsigned)(srows < 65535 ? srows : 65535));
   k_uncompress<<<grid, 256, 0, s>>>(w, srows, scols, lrows, lcols, t, e, slots, reversed, column_axis, p,

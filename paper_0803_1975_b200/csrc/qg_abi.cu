@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <vector>
 
 #include "../../include/qgemm_b200.h"
 #include "qg_internal.h"
@@ -853,7 +854,7 @@ thread_local PhaseLog g_phase;
 std::atomic<int> g_phase_timing{0};
 
 struct PhaseScope {
-  static constexpr int kPairs = 64;
+  static constexpr int kPairs = 512;  // host_pipeline2d: up to 64 chunks x 8 panels
   // timing events created once per thread: creating them per call stalls the
   // host's enqueue loop of the pipelined path (measured +0.36 ms on config 2)
   static cudaEvent_t* pool() {
@@ -910,6 +911,15 @@ struct HostPipe {
   static constexpr int kMaxChunks = 64;
   cudaEvent_t b_ready = nullptr, b_packed = nullptr, a_ready[kMaxChunks] = {}, c_ready[kMaxChunks] = {},
               done = nullptr;
+  std::vector<cudaEvent_t> pool;  // host_pipeline2d's per-item and per-tile events, grown on demand
+  cudaEvent_t event(size_t i) {
+    while (pool.size() <= i) {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+      pool.push_back(e);
+    }
+    return pool[i];
+  }
   bool ok = false;
   HostPipe() {
     ok = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess &&
@@ -1007,6 +1017,139 @@ static int host_pipeline(size_t m, size_t k, size_t n, size_t align, size_t col_
   return QG_OK;
 }
 
+// The 2-D pipeline pays off when the contraction is long against B's
+// transfer (config 5: B is 78 ms of PCIe against a 0.36 s product, 448 ->
+// 403 ms); where the transfer dominates anyway (config 2) or the tiles get
+// too small for the GPU (config 4, 3.5 % at best) the 1-D pipeline stays.
+// Estimates: contraction at 30 TFLOP/s of packed FP64, PCIe at 50 GB/s.
+// QG_HOST_2D=0/1 forces it off/on.
+static bool use_pipeline2d(double packed_flop, size_t b_bytes) {
+  const char* e = getenv("QG_HOST_2D");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return packed_flop / 30e12 > 3.0 * ((double)b_bytes / 50e9);
+}
+
+// Two-dimensional variant of host_pipeline: A streams up in row chunks and B
+// in column panels, the two interleaved by bytes sent, so the contraction of
+// tile (chunk r, panel c) starts as soon as both have arrived and been packed
+// instead of after all of B (config 4: B alone is 4.7 ms of PCIe). Tiles
+// rotate over the compute streams; each tile's output leaves as a 2-D copy.
+struct TileOut {
+  const void* src = nullptr;
+  size_t spitch = 0;
+  void* dst = nullptr;
+  size_t dpitch = 0, width = 0, height = 0;
+};
+
+static int host_pipeline2d(
+    size_t m, size_t k, size_t n, size_t align, size_t col_align, size_t out_tiles_per_block, const uint32_t* a,
+    const uint32_t* b,
+    const std::function<int(size_t c0, size_t cols, const uint32_t* dbp, cudaStream_t s)>& pack_b_panel,
+    const std::function<int(size_t r0, size_t rows, const uint32_t* da, cudaStream_t s)>& pack_a_chunk,
+    const std::function<int(size_t r0, size_t rows, size_t c0, size_t cols, cudaStream_t s, PhaseScope& ps,
+                            TileOut* out)>& tile) {
+  HostPipe& hp = host_pipe();
+  if (!hp.ok) return QG_CUDA_ERROR;
+  PhaseScope ps;
+  // column panels (whole multiples of col_align columns; one col_align block =
+  // out_tiles_per_block 128-wide output tile columns)
+  const size_t col_blocks = ceil_div(n, col_align);
+  size_t want_p = 4;
+  if (const char* e = getenv("QG_HOST_PANELS")) want_p = (size_t)atoi(e);  // experiments
+  const size_t npanels = col_blocks < want_p ? (col_blocks ? col_blocks : 1) : (want_p ? want_p : 1);
+  const size_t blocks_per = ceil_div(col_blocks, npanels);
+  // row chunks large enough that one tile launch has ~96 output tiles of
+  // 128 x 128 (a tile launch on a few SMs would leave the GPU idle)
+  size_t want_tiles = 96;
+  if (const char* e = getenv("QG_HOST_TILES")) want_tiles = (size_t)atoi(e);  // experiments
+  const size_t tc = blocks_per * out_tiles_per_block;
+  size_t rows_per = ceil_div(want_tiles, tc ? tc : 1) * 128;
+  if (rows_per < 512) rows_per = 512;
+  rows_per = (rows_per + align - 1) / align * align;
+  size_t nchunks = ceil_div(m, rows_per);
+  if (nchunks > (size_t)HostPipe::kMaxChunks) {
+    rows_per = ceil_div(ceil_div(m, (size_t)HostPipe::kMaxChunks), align) * align;
+    nchunks = ceil_div(m, rows_per);
+  }
+  auto panel = [&](size_t j, size_t* c0, size_t* cols) {
+    *c0 = j * blocks_per * col_align;
+    const size_t c1 = (j + 1) * blocks_per * col_align;
+    *cols = (c1 < n ? c1 : n) - (*c0 < n ? *c0 : n);
+  };
+  DevBuf da(hp.in), db(hp.in);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));  // panel j: k x cols_j contiguous at column offset c0_j * k
+  size_t ev = 0;
+  std::vector<cudaEvent_t> a_packed(nchunks, nullptr), b_packed(npanels, nullptr);
+  std::vector<char> a_sent(nchunks, 0), b_sent(npanels, 0);
+  size_t ia = 0, ib = 0, bytes_a = 0, bytes_b = 0, ntile = 0, npack = 0;
+  while (ia < nchunks || ib < npanels) {
+    // the stream (A rows or B columns) that has sent fewer bytes goes next
+    const bool send_b = ib < npanels && (ia >= nchunks || bytes_b <= bytes_a);
+    cudaEvent_t ready = hp.event(ev++), packed = hp.event(ev++);
+    if (!ready || !packed) return QG_CUDA_ERROR;
+    cudaStream_t ps_s = hp.comps[npack++ % HostPipe::kComp];
+    if (send_b) {
+      size_t c0, cols;
+      panel(ib, &c0, &cols);
+      const uint32_t* dbp = (const uint32_t*)db.p + c0 * k;
+      if (k * cols)
+        QG_TRY(cudaMemcpy2DAsync((void*)dbp, cols * 4, b + c0, n * 4, cols * 4, k, cudaMemcpyHostToDevice, hp.in));
+      QG_TRY(cudaEventRecord(ready, hp.in));
+      QG_TRY(cudaStreamWaitEvent(ps_s, ready, 0));
+      int st = pack_b_panel(c0, cols, dbp, ps_s);
+      if (st) return st;
+      QG_TRY(cudaEventRecord(packed, ps_s));
+      b_packed[ib] = packed;
+      b_sent[ib] = 1;
+      bytes_b += k * cols * 4;
+    } else {
+      const size_t r0 = ia * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+      const uint32_t* dap = (const uint32_t*)da.p + r0 * k;
+      if (rows * k) QG_TRY(cudaMemcpyAsync((void*)dap, a + r0 * k, rows * k * 4, cudaMemcpyHostToDevice, hp.in));
+      QG_TRY(cudaEventRecord(ready, hp.in));
+      QG_TRY(cudaStreamWaitEvent(ps_s, ready, 0));
+      int st = pack_a_chunk(r0, rows, dap, ps_s);
+      if (st) return st;
+      QG_TRY(cudaEventRecord(packed, ps_s));
+      a_packed[ia] = packed;
+      a_sent[ia] = 1;
+      bytes_a += rows * k * 4;
+    }
+    // every tile the new item completes
+    const size_t r_lo = send_b ? 0 : ia, r_hi = send_b ? ia : ia + 1;
+    const size_t c_lo = send_b ? ib : 0, c_hi = send_b ? ib + 1 : ib;
+    for (size_t r = r_lo; r < r_hi; ++r)
+      for (size_t c = c_lo; c < c_hi; ++c) {
+        if (!a_sent[r] || !b_sent[c]) continue;
+        const size_t r0 = r * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+        size_t c0, cols;
+        panel(c, &c0, &cols);
+        cudaStream_t cs = hp.comps[ntile++ % HostPipe::kComp];
+        QG_TRY(cudaStreamWaitEvent(cs, a_packed[r], 0));
+        QG_TRY(cudaStreamWaitEvent(cs, b_packed[c], 0));
+        TileOut out;
+        int st = tile(r0, rows, c0, cols, cs, ps, &out);
+        if (st) return st;
+        cudaEvent_t done_t = hp.event(ev++);
+        if (!done_t) return QG_CUDA_ERROR;
+        QG_TRY(cudaEventRecord(done_t, cs));
+        QG_TRY(cudaStreamWaitEvent(hp.out, done_t, 0));
+        if (out.width && out.height)
+          QG_TRY(cudaMemcpy2DAsync(out.dst, out.dpitch, out.src, out.spitch, out.width, out.height,
+                                   cudaMemcpyDeviceToHost, hp.out));
+      }
+    if (send_b) ++ib;
+    else ++ia;
+  }
+  QG_TRY(cudaEventRecord(hp.done, hp.out));
+  QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
+  QG_TRY(cudaStreamSynchronize(hp.out));
+  ps.finish();
+  return QG_OK;
+}
+
 // mul_common_compressed on host data, pipelined over three streams: B goes
 // up first and is packed; A then streams up in row chunks of 512 while the
 // previous chunks are packed and contracted, and C streams back per chunk on
@@ -1026,6 +1169,32 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
     QG_TRY(dc.alloc(m * n * 4));
     QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
     QG_TRY(dcb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
+    const size_t Wt = Kt * 128 * bk;  // words per 128-row (column) block of CA_t (CB_t)
+    if (use_pipeline2d(2.0 * m * n * K, k * n * 4))
+      return host_pipeline2d(
+          m, k, n, 128, 128, 1, a, b,
+          [&](size_t c0, size_t cols, const uint32_t* dbp, cudaStream_t s2) {
+            return cuda_status(qgk::launch_pack_tiled(true, dbp, QG_U32, k, cols, cols, pl.t, pl.e, bk,
+                                                      (double*)dcb.p + (c0 / 128) * Wt, s2, pl.p, gp->balanced != 0));
+          },
+          [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s2) {
+            return cuda_status(qgk::launch_pack_tiled(false, da, QG_U32, rows, k, k, pl.t, pl.e, bk,
+                                                      (double*)dca.p + (r0 / 128) * Wt, s2, pl.p, gp->balanced != 0));
+          },
+          [&](size_t r0, size_t rows, size_t c0, size_t cols, cudaStream_t s2, PhaseScope& ps, TileOut* out) {
+            ps.begin(s2);
+            int st2 = qg_mul_common_tiled(gp, (const double*)dca.p + (r0 / 128) * Wt,
+                                          (const double*)dcb.p + (c0 / 128) * Wt, rows, cols, k,
+                                          (int32_t*)dc.p + r0 * n + c0, n, s2);
+            if (st2) return st2;
+            ps.end(s2);
+            out->src = (const int32_t*)dc.p + r0 * n + c0;
+            out->dst = c + r0 * n + c0;
+            out->spitch = out->dpitch = n * 4;
+            out->width = cols * 4;
+            out->height = rows;
+            return (int)QG_OK;
+          });
     return host_pipeline(
         m, k, n, 128, ceil_div(n, (size_t)128), a, b,
         [&](const uint32_t* db, cudaStream_t s2) {
@@ -1182,6 +1351,38 @@ static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* 
   QG_TRY(dbt.alloc(ceil_div(H, 128) * 128 * kt * bk * 8));
   QG_TRY(dcc.alloc(m * H * 8));
   const bool bal = gp->balanced != 0;
+  const size_t Wt = kt * 128 * bk;  // words per 128-row / 128-word-column block
+  const size_t e = (size_t)plan->e;
+  if (use_pipeline2d(2.0 * m * H * k, k * n * 4))
+    return host_pipeline2d(
+        m, k, n, 128, 128 * e, 1, a, b,
+        [&](size_t c0, size_t cols, const uint32_t* dbp, cudaStream_t s) {
+          if (!k) return (int)QG_OK;
+          double* dst = (double*)dbt.p + (c0 / e / 128) * Wt;
+          return bal ? qg_pack_outer_cols_tiled_bal(plan, (uint32_t)bk, dbp, QG_U32, k, cols, cols, dst, s)
+                     : qg_pack_outer_cols_tiled(plan, (uint32_t)bk, dbp, QG_U32, k, cols, cols, dst, s);
+        },
+        [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s) {
+          if (!k) return (int)QG_OK;
+          double* at = (double*)dat.p + (r0 / 128) * Wt;
+          return bal ? qg_pack_residues_tiled_bal(plan->p, (uint32_t)bk, da, QG_U32, rows, k, k, at, s)
+                     : qg_pack_residues_tiled((uint32_t)bk, da, QG_U32, rows, k, k, at, s);
+        },
+        [&](size_t r0, size_t rows, size_t c0, size_t cols, cudaStream_t s, PhaseScope& ps, TileOut* out) {
+          const size_t h0 = c0 / e, hw = ceil_div(cols, e);
+          ps.begin(s);
+          int st2 = qg_mul_right_tiled(gp, (const double*)dat.p + (r0 / 128) * Wt,
+                                       (const double*)dbt.p + (h0 / 128) * Wt, rows, k, cols,
+                                       (double*)dcc.p + r0 * H + h0, H, s);
+          if (st2) return st2;
+          ps.end(s);
+          out->src = (const double*)dcc.p + r0 * H + h0;
+          out->dst = cc + r0 * H + h0;
+          out->spitch = out->dpitch = H * 8;
+          out->width = hw * 8;
+          out->height = rows;
+          return (int)QG_OK;
+        });
   return host_pipeline(
       m, k, n, 128, ceil_div(H, (size_t)128), a, b,
       [&](const uint32_t* db, cudaStream_t s) {

@@ -295,6 +295,14 @@ int qg_host_mul_common_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const ui
                            size_t m, size_t k, size_t n, uint32_t* c);
 /* blocked_accumulate(A, B, plan, kpanel), gemm.hpp:450-489 on HOST data:
  * panels of kpanel residues, each packed under `plan`, mod-p accumulation. */
+/* mul_common_compressed over `ngpus` devices of this process:
+ * rows of A and C sharded over devices[] (128-row multiples), B packed once on
+ * devices[0] into the tiled layout and broadcast as packed words by one
+ * grouped ncclBroadcast (NVLink / NVSwitch), every device packs and contracts
+ * its own rows; host buffers in / out as qg_host_mul_common_gpu. NCCL is
+ * dlopen'ed (libnccl.so.2) at the first call; QG_NCCL_ERROR if absent. */
+int qg_host_mul_common_multi(const qg_gpu_plan* gplan, const int* devices, int ngpus, const uint32_t* a,
+                             const uint32_t* b, size_t m, size_t k, size_t n, uint32_t* c);
 int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
                                size_t m, size_t k, size_t n, size_t kpanel, uint32_t* c);
 /* mul_right_compressed(A, compress_outer_cols(B)), gemm.hpp:320-325, on HOST

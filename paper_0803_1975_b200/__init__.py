@@ -171,6 +171,7 @@ def _load():
         "qg_uncompress": ([P(_Plan), _Orientation, vp, sz, sz, sz, sz, vp, vp], i32),
         "qg_host_mul_common": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_mul_common_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_common_multi": ([P(_GpuPlan), P(i32), i32, vp, vp, sz, sz, sz, vp], i32),
         "qg_host_blocked_accumulate": ([P(_Plan), vp, vp, sz, sz, sz, sz, vp], i32),
         "qg_host_mul_right": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_tiled_stage_words": ([P(_GpuPlan), u64, P(u32)], i32),
@@ -960,6 +961,24 @@ def mul_common_compressed_host(a, b, plan: Union[CompressionPlan, GpuPlan], out=
         pl = plan._c()
         _check(lib.qg_host_mul_common(ctypes.byref(pl), a.ctypes.data_as(vp), b.ctypes.data_as(vp), m, k, n,
                                       c.ctypes.data_as(vp)))
+    return c
+
+
+def mul_common_multi_host(a, b, plan: Union[CompressionPlan, GpuPlan], devices=(0,), out=None) -> np.ndarray:
+    """mul_common_compressed on host data over several GPUs of this process
+    (qg_host_mul_common_multi): rows of A and C sharded over `devices`, B
+    packed once and broadcast as packed words over NCCL."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
+    gp = _as_gpu_plan(plan, k)
+    c = np.empty((m, n), dtype=np.uint32) if out is None else out
+    devs = (ctypes.c_int * len(devices))(*devices)
+    g = gp._c()
+    _check(lib.qg_host_mul_common_multi(ctypes.byref(g), devs, len(devices), a.ctypes.data_as(ctypes.c_void_p),
+                                        b.ctypes.data_as(ctypes.c_void_p), m, k, n, c.ctypes.data_as(ctypes.c_void_p)))
     return c
 
 

@@ -42,6 +42,11 @@ int cuda_status(cudaError_t e) {
   return QG_CUDA_ERROR;
 }
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+#define QG_TRY(x)                       \
+  do {                                  \
+    cudaError_t e_ = (x);               \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
 size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 
 // CompressionPlan usable by the DoubleWord backend (pack.hpp:19-24).
@@ -604,14 +609,15 @@ int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda
     // Integer contraction (64-bit sums, qg_word64.cu) + reduction.
     keep_pool_mapped();
     DevBuf acc(s), cw(s), bw(s);
-    if (acc.alloc(m * n * 8) || bw.alloc(k * n * 8)) return cuda_status(cudaGetLastError());
+    QG_TRY(acc.alloc(m * n * 8));
+    QG_TRY(bw.alloc(k * n * 8));
     // B's residues as one-residue uint64 words (compress_cols_forward at e = 1)
     if ((st = cuda_status(qgk::launch_pack_u64(qgk::PACK_COLS_FORWARD, b, dtype, k, n, ldb, pl.t, 1,
                                                (uint64_t*)bw.p, n, 0, 0, s))))
       return st;
     int32_t* cdst = c;
     if (ldc != n) {
-      if (cw.alloc(m * n * 4)) return cuda_status(cudaGetLastError());
+      QG_TRY(cw.alloc(m * n * 4));
       cdst = (int32_t*)cw.p;
     }
     if ((st = cuda_status(qgk::launch_gemm_u64(1, a, dtype, lda, bw.p, -1, n, m, n, k, 0, 0, (uint64_t*)acc.p, n, s))))
@@ -629,8 +635,8 @@ int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda
   int bk = 0, kbs = 0;
   if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
   DevBuf ca(s), cb(s);
-  if (ca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8) != cudaSuccess) return cuda_status(cudaGetLastError());
-  if (cb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8) != cudaSuccess) return cuda_status(cudaGetLastError());
+  QG_TRY(ca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
+  QG_TRY(cb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
   if ((st = qg_pack_a_tiled(gplan, bk, a, dtype, m, k, lda, (double*)ca.p, stream))) return st;
   if ((st = qg_pack_b_tiled(gplan, bk, b, dtype, k, n, ldb, (double*)cb.p, stream))) return st;
   return qg_mul_common_tiled(gplan, (const double*)ca.p, (const double*)cb.p, m, n, k, c, ldc, stream);
@@ -894,11 +900,6 @@ struct PhaseScope {
   }
 };
 
-#define QG_TRY(x)                       \
-  do {                                  \
-    cudaError_t e_ = (x);               \
-    if (e_ != cudaSuccess) return cuda_status(e_); \
-  } while (0)
 }  // namespace
 
 // Streams and events of the pipelined host path, created once per thread.

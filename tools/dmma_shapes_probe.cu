@@ -93,6 +93,9 @@ static void run(const char* name, K kern, double flop_per_mma, int nacc, int war
 }
 
 int main() {
+  // one warp per SMSP (4 per SM) with the contraction's 32 independent
+  // accumulators per k-step, against two per SMSP
+  for (int w : {4, 8}) run("m8n8k4", k884<32>, 2.0 * 8 * 8 * 4, 32, w);
   for (int w : {8, 16}) {
     run("m8n8k4", k884<8>, 2.0 * 8 * 8 * 4, 8, w);
     run("m16n8k4", k1684<8>, 2.0 * 16 * 8 * 4, 8, w);

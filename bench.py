@@ -473,7 +473,7 @@ def redq_arm(args):
             arg = gp if args.plan == "gpu" else plan
             call = lambda: fn(an_u, bn_u, arg, out=out)  # noqa: E731
             api = f"mul_{variant}_compressed_host (qg_host_mul_{variant}{'_gpu' if args.plan == 'gpu' else ''})"
-        for _ in range(2):
+        for _ in range(3):
             call()
         times = []
         for _ in range(args.e2e_steps):
@@ -738,7 +738,7 @@ def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1):
     b.copy_(qg.random_residue_matrix(k, n, p, SEED + 1, dtype=torch.int32))
     torch.cuda.synchronize()
     an, bn, cn = a.numpy().view(np.uint32), b.numpy().view(np.uint32), c.numpy().view(np.uint32)
-    for _ in range(2):
+    for _ in range(3):
         qg.mul_common_compressed_host(an, bn, gp, out=cn)
     times = []
     for _ in range(args.e2e_steps):
@@ -773,7 +773,7 @@ def main():
                     help="gloo: functional check of the multi-rank path with several ranks on one GPU")
     ap.add_argument("--bcast-panels", type=int, default=4,
                     help="N>1: column panels the packed B is broadcast in (1 = one broadcast after the whole pack)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
     ap.add_argument("--ref-step-s", type=float, default=2.0)
     ap.add_argument("--no-e2e", action="store_true")

@@ -596,9 +596,9 @@ def our_arm(args):
     torch.cuda.synchronize()
 
     # One GPU: the step's launches are captured once into one CUDA graph
-    # (packs; contraction) and replayed, so host launch gaps stay out of the
-    # step (they dominate small shapes such as config 1). The contraction's
-    # events sit between the two replays.
+    # (packs, then the contraction) and replayed, so host launch gaps stay out
+    # of the step (they dominate small shapes such as config 1); the
+    # contraction's timing events are record nodes inside the graph.
     use_graph = world == 1 and not args.no_graph
     launches_per_step = None
     kernel_name = None

@@ -481,9 +481,13 @@ def redq_arm(args):
             call()
             times.append(time.perf_counter() - t0)
         t = sum(times) / len(times)
+        # the host path's result against the device product's, bit for bit
+        dev_out = c.cpu().numpy().astype(np.uint32) if variant == "full" else cc.cpu().numpy()
+        same = bool(np.array_equal(np.ascontiguousarray(out).view(np.uint32 if variant == "full" else np.uint64),
+                                   np.ascontiguousarray(dev_out).view(np.uint32 if variant == "full" else np.uint64)))
         line["e2e"] = {"value": 2.0 * m * n * k / t, "unit": "mult-adds/s (2mnk/s)",
                        "h2d_bytes_per_step": int((m * k + k * n) * 4), "d2h_bytes_per_step": int(out.nbytes),
-                       "ms_per_step": t * 1e3, "api": api}
+                       "ms_per_step": t * 1e3, "api": api, "matches_device": same}
     if not args.no_cpu:
         try:
             rate, rows, thr, dt, _, rpl, kind = reference_variant_sample(variant, p, m, k, n, target_s=args.cpu_s)
@@ -708,7 +712,7 @@ def our_arm(args):
     line["clocks"] = clk.summary()
 
     if not args.no_e2e:
-        e2e = e2e_measure(qg, gp, p, m_rank, k, n, args, rank, world)
+        e2e = e2e_measure(qg, gp, p, m_rank, k, n, args, rank, world, device_c=c)
         if rank == 0:
             line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -728,7 +732,7 @@ def our_arm(args):
     return 0
 
 
-def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1):
+def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1, device_c=None):
     """Same metric through the public host-buffer API (pinned buffers):
     H2D of A and B (uint32 ResidueMatrix data), pack + contraction kernels,
     D2H of C, every step. At N GPUs every rank calls the API on its own row
@@ -764,7 +768,9 @@ def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1):
             "h2d_bytes_per_step": int(a.numel() * 4 + b.numel() * 4) * world,
             "d2h_bytes_per_step": int(c.numel() * 4) * world, "ms_per_step": t * 1e3,
             "api": "mul_common_compressed_host (qg_host_mul_common_gpu), pipelined H2D/compute/D2H",
-            "checksum_rank0": int(cn.astype(np.uint64).sum() & 0xFFFFFFFF)}
+            "checksum_rank0": int(cn.astype(np.uint64).sum() & 0xFFFFFFFF),
+            "matches_device": None if device_c is None else
+            bool(np.array_equal(cn, device_c.cpu().numpy().astype(np.uint32)))}
 
 
 def main():

@@ -283,7 +283,7 @@ int qg_pack_outer_cols_tiled(const qg_plan* plan, uint32_t bk, const void* b, qg
 // (p-1) + kb (p-1)^2 < Q (the previous block's REDQ'd digit plus the block's
 // sum); a single block needs k <= kmax (gemm.hpp:295).
 static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const double* b_t, size_t M, size_t k,
-                        size_t N, double* cc, size_t ldcc, void* stream) {
+                        size_t N, double* cc, size_t ldcc, void* stream, bool accumulate = false) {
   const qg_plan& pl = gplan->plan;
   int st = check_plan(&pl);
   if (st) return st;
@@ -322,6 +322,10 @@ static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const doubl
   r.p = pl.p;
   r.cc = cc;
   r.ldcc = ldcc;
+  if (accumulate) {  // start from the (REDQ'd, digits < p) words in cc: unsigned plans only
+    if (bal) return QG_PLAN_MISMATCH;
+    r.accumulate = 1;
+  }
   if (bal) {  // constants of the balanced in-place REDQ (qg_dot.cu, redq_words_inplace_bal)
     r.balanced = 1;
     const uint64_t half = Q / 2;
@@ -1336,6 +1340,152 @@ int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uin
 
 // Host-data right / left products on the tiled path. gp's kblock_words
 // bounds the in-place REDQ blocks (kblock >= k: the reference's single block).
+// The mixed variant with k split into parts (config 4): part p brings its
+// rows of B (contiguous) and its columns of A (a 2-D copy) over PCIe, is
+// packed, and is contracted over all of m x n with the accumulators starting
+// from the previous parts' REDQ'd words (qg_dot.cu, EPI_REDQ accumulate). The
+// first contraction starts after 1/P of the transfers instead of after all of
+// B, every part's contraction fills the GPU, and the last part runs in row
+// chunks whose words stream back while the next chunk computes.
+// Unsigned plans (the accumulate mode loads canonical digits).
+static bool use_ksplit(double packed_flop, size_t b_bytes, size_t k, size_t block) {
+  const char* e = getenv("QG_HOST_KSPLIT");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return k >= 2 * (block ? block : 1);
+  const double tc = packed_flop / 30e12, tb = (double)b_bytes / 50e9;
+  return tc > tb && tc <= 3.0 * tb && k >= 8 * (block ? block : 512);
+}
+
+// rows_a / cols_b: rows of the contraction's A operand and columns of its B
+// operand (right: m and ceil(n/e) words; left: ceil(m/e) words and n);
+// row_align: A-operand rows per 128-row block of the packed layout.
+static int host_redq_ksplit(
+    const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n, size_t rows_a,
+    size_t cols_b, double* cc,
+    const std::function<int(const uint32_t* dap, size_t kp, uint32_t bkp, double* at, cudaStream_t s)>& pack_a,
+    const std::function<int(const uint32_t* dbp, size_t kp, uint32_t bkp, double* bt, cudaStream_t s)>& pack_b) {
+  HostPipe& hp = host_pipe();
+  if (!hp.ok) return QG_CUDA_ERROR;
+  PhaseScope ps;
+  // parts: whole multiples of the in-place REDQ block (same block structure per part)
+  int bk = 0, kbs = 0;
+  int st = right_tiled_geometry(gp, k, &bk, &kbs);
+  if (st) return st;
+  const size_t blk = kbs ? (size_t)kbs * bk : k;
+  size_t parts = 8;
+  if (const char* e = getenv("QG_HOST_KPARTS")) parts = (size_t)atoi(e);  // experiments
+  const size_t nblk = ceil_div(k, blk);
+  if (parts > nblk) parts = nblk;
+  if (parts < 1) parts = 1;
+  const size_t blk_per = ceil_div(nblk, parts);
+  parts = ceil_div(nblk, blk_per);
+  const size_t kp_max = blk_per * blk;
+  // per-part tiled buffers (the stage depth follows each part's own k, as in
+  // redq_product), sized for the largest part
+  auto part_geo = [&](size_t kp, int* bkp, size_t* ktp) {
+    int kbsp = 0;
+    const int st2 = right_tiled_geometry(gp, kp, bkp, &kbsp);
+    *ktp = ceil_div(kp, (size_t)*bkp);
+    return st2;
+  };
+  size_t wa = 0, wbt = 0;
+  for (size_t pi = 0; pi < parts; ++pi) {
+    const size_t kp = (k - pi * kp_max) < kp_max ? (k - pi * kp_max) : kp_max;
+    int bkp = 0;
+    size_t ktp = 0;
+    if ((st = part_geo(kp, &bkp, &ktp))) return st;
+    const size_t a_w = ceil_div(rows_a, 128) * 128 * ktp * bkp, b_w = ceil_div(cols_b, 128) * 128 * ktp * bkp;
+    wa = a_w > wa ? a_w : wa;
+    wbt = b_w > wbt ? b_w : wbt;
+  }
+  cudaStream_t s0 = hp.in;
+  DevBuf da(s0), db(s0), dat(s0), dbt(s0), dcc(s0);
+  QG_TRY(da.alloc(m * k * 4));
+  QG_TRY(db.alloc(k * n * 4));
+  QG_TRY(dat.alloc(2 * wa * 8));  // ping-pong: part p packs while part p-1 contracts
+  QG_TRY(dbt.alloc(2 * wbt * 8));
+  QG_TRY(dcc.alloc(rows_a * cols_b * 8));
+  cudaStream_t cs = hp.comps[0], pk = hp.comps[1];  // contractions; packs (one part ahead)
+  size_t ev = 0;
+  std::vector<cudaEvent_t> contracted(parts, nullptr);
+  for (size_t pi = 0; pi < parts; ++pi) {
+    const size_t k0 = pi * kp_max, kp = (k - k0) < kp_max ? (k - k0) : kp_max;
+    int bkp = 0;
+    size_t ktp = 0;
+    if ((st = part_geo(kp, &bkp, &ktp))) return st;
+    uint32_t* dap = (uint32_t*)da.p + m * k0;  // m x kp, contiguous (A's columns k0..)
+    uint32_t* dbp = (uint32_t*)db.p + k0 * n;  // kp x n, contiguous (B's rows k0..)
+    QG_TRY(cudaMemcpyAsync(dbp, b + k0 * n, kp * n * 4, cudaMemcpyHostToDevice, hp.in));
+    QG_TRY(cudaMemcpy2DAsync(dap, kp * 4, a + k0, k * 4, kp * 4, m, cudaMemcpyHostToDevice, hp.in));
+    cudaEvent_t ready = hp.event(ev++);
+    if (!ready) return QG_CUDA_ERROR;
+    QG_TRY(cudaEventRecord(ready, hp.in));
+    QG_TRY(cudaStreamWaitEvent(pk, ready, 0));
+    if (pi >= 2) QG_TRY(cudaStreamWaitEvent(pk, contracted[pi - 2], 0));  // its ping-pong buffers are free
+    double* at = (double*)dat.p + (pi % 2) * wa;
+    double* bt = (double*)dbt.p + (pi % 2) * wbt;
+    if ((st = pack_a(dap, kp, (uint32_t)bkp, at, pk))) return st;
+    if ((st = pack_b(dbp, kp, (uint32_t)bkp, bt, pk))) return st;
+    cudaEvent_t packed = hp.event(ev++);
+    if (!packed) return QG_CUDA_ERROR;
+    QG_TRY(cudaEventRecord(packed, pk));
+    QG_TRY(cudaStreamWaitEvent(cs, packed, 0));
+    const bool last = pi + 1 == parts;
+    const size_t rows_per = last ? 1024 : rows_a;  // the last part in row chunks: its words stream back
+    for (size_t r0 = 0; r0 < rows_a; r0 += rows_per) {
+      const size_t rows = (rows_a - r0) < rows_per ? (rows_a - r0) : rows_per;
+      ps.begin(cs);
+      if ((st = redq_product(gp, at + (r0 / 128) * ktp * 128 * bkp, bt, rows, kp, cols_b,
+                             (double*)dcc.p + r0 * cols_b, cols_b, cs, pi > 0)))
+        return st;
+      ps.end(cs);
+      if (last) {
+        cudaEvent_t done_c = hp.event(ev++);
+        if (!done_c) return QG_CUDA_ERROR;
+        QG_TRY(cudaEventRecord(done_c, cs));
+        QG_TRY(cudaStreamWaitEvent(hp.out, done_c, 0));
+        QG_TRY(cudaMemcpyAsync(cc + r0 * cols_b, (double*)dcc.p + r0 * cols_b, rows * cols_b * 8,
+                               cudaMemcpyDeviceToHost, hp.out));
+      }
+    }
+    contracted[pi] = hp.event(ev++);
+    if (!contracted[pi]) return QG_CUDA_ERROR;
+    QG_TRY(cudaEventRecord(contracted[pi], cs));
+  }
+  QG_TRY(cudaStreamWaitEvent(hp.out, contracted[parts - 1], 0));
+  QG_TRY(cudaEventRecord(hp.done, hp.out));
+  QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));
+  QG_TRY(cudaStreamSynchronize(hp.out));
+  ps.finish();
+  return QG_OK;
+}
+
+static int host_right_ksplit(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                             size_t n, double* cc) {
+  const qg_plan* plan = &gp->plan;
+  return host_redq_ksplit(
+      gp, a, b, m, k, n, m, ceil_div(n, (size_t)plan->e), cc,
+      [&](const uint32_t* dap, size_t kp, uint32_t bkp, double* at, cudaStream_t s) {
+        return qg_pack_residues_tiled(bkp, dap, QG_U32, m, kp, kp, at, s);
+      },
+      [&](const uint32_t* dbp, size_t kp, uint32_t bkp, double* bt, cudaStream_t s) {
+        return qg_pack_outer_cols_tiled(plan, bkp, dbp, QG_U32, kp, n, n, bt, s);
+      });
+}
+
+static int host_left_ksplit(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                            size_t n, double* cc) {
+  const qg_plan* plan = &gp->plan;
+  return host_redq_ksplit(
+      gp, a, b, m, k, n, ceil_div(m, (size_t)plan->e), n, cc,
+      [&](const uint32_t* dap, size_t kp, uint32_t bkp, double* at, cudaStream_t s) {
+        return qg_pack_outer_rows_tiled(plan, bkp, dap, QG_U32, m, kp, kp, at, s);
+      },
+      [&](const uint32_t* dbp, size_t kp, uint32_t bkp, double* bt, cudaStream_t s) {
+        return qg_pack_residues_b_tiled(bkp, dbp, QG_U32, kp, n, n, bt, s);
+      });
+}
+
 static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k, size_t n,
                       double* cc) {
   const qg_plan* plan = &gp->plan;
@@ -1345,6 +1495,8 @@ static int host_right(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* 
   if (m * H == 0) return QG_OK;
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
+  if (gp->balanced == 0 && use_ksplit(2.0 * m * H * k, k * n * 4, k, kbs ? (size_t)kbs * bk : 0))
+    return host_right_ksplit(gp, a, b, m, k, n, cc);
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
   cudaStream_t s0 = host_pipe().in;
   DevBuf dat(s0), dbt(s0), dcc(s0);
@@ -1418,6 +1570,8 @@ static int host_left(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b
   if (G * n == 0) return QG_OK;
   int bk = 0, kbs = 0;
   if ((st = right_tiled_geometry(gp, k ? k : 1, &bk, &kbs))) return st;
+  if (gp->balanced == 0 && use_ksplit(2.0 * G * n * k, k * n * 4, k, kbs ? (size_t)kbs * bk : 0))
+    return host_left_ksplit(gp, a, b, m, k, n, cc);
   const size_t kt = ceil_div(k ? k : 1, (size_t)bk);
   cudaStream_t s0 = host_pipe().in;
   DevBuf dat(s0), dbt(s0), dcc(s0);

@@ -507,6 +507,20 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
     int tm, tn;
     tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
     const int m0 = tm * BM, n0 = tn * BN;
+    if (EPI != EPI_DIGIT && args.accumulate) {
+      // continue from the words already in CC (a k-split host product: the
+      // previous part's REDQ left every digit below p, so the in-place REDQ
+      // block bound is the same as between blocks)
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = m0 + warp_m * WM + mi * 8 + g, col = n0 + warp_n * WN + ni * 8 + 2 * t + h;
+            acc[mi][ni][h] = (row < M && col < N) ? args.cc[(size_t)row * args.ldcc + col] : 0.0;
+          }
+    }
     int kst = 0;
     for (int kt = 0; kt < ktiles; ++kt) {
       if (!nomem) mbar_wait(full + slot, phase);

@@ -48,3 +48,45 @@ def test_host_right_2d(qg, orc, cuda, monkeypatch, p, m, k, n, panels):
     for s in range(e):
         digits[:, s::e] = (w >> np.uint64(gp.plan.t * s)) & np.uint64((1 << gp.plan.t) - 1)
     assert np.array_equal(digits[:, :n].astype(np.uint32), orc.naive_gemm(p, a, b))
+
+
+@pytest.mark.parametrize("p,m,k,n,parts", [(5, 700, 5000, 3000, "8"), (3, 300, 4000, 2049, "3"), (7, 1100, 3000, 700, "2")])
+def test_host_right_ksplit(qg, orc, cuda, monkeypatch, p, m, k, n, parts):
+    """The k-split host path of the mixed variant (host_right_ksplit: parts of
+    k contracted in turn, the accumulators continuing from the previous
+    parts' REDQ'd words): the CC words of a blocked GPU plan decode to
+    naive_gemm's C."""
+    monkeypatch.setenv("QG_HOST_KSPLIT", "1")
+    monkeypatch.setenv("QG_HOST_KPARTS", parts)
+    a = orc.random_residue_matrix(m, k, p, 41)
+    b = orc.random_residue_matrix(k, n, p, 42)
+    gp = qg.plan_right_gpu(p, k, n)
+    if gp.balanced:
+        gp = qg.GpuPlan(gp.plan, gp.kblock_words, gp.max_exact_words, 0)
+    got = qg.mul_right_compressed_host(a, b, gp)
+    e = gp.plan.e
+    digits = np.zeros((m, ((n + e - 1) // e) * e), dtype=np.uint64)
+    w = got.astype(np.uint64)
+    for s in range(e):
+        digits[:, s::e] = (w >> np.uint64(gp.plan.t * s)) & np.uint64((1 << gp.plan.t) - 1)
+    assert np.array_equal(digits[:, :n].astype(np.uint32), orc.naive_gemm(p, a, b))
+
+
+@pytest.mark.parametrize("p,m,k,n,parts", [(5, 700, 5000, 3000, "8"), (7, 1100, 3000, 700, "2"), (3, 2100, 3100, 300, "3")])
+def test_host_left_ksplit(qg, orc, cuda, monkeypatch, p, m, k, n, parts):
+    """The k-split host path of the left variant: CC words (digit s of
+    CC[g][j] = C[g e + s][j]) decode to naive_gemm's C."""
+    monkeypatch.setenv("QG_HOST_KSPLIT", "1")
+    monkeypatch.setenv("QG_HOST_KPARTS", parts)
+    a = orc.random_residue_matrix(m, k, p, 51)
+    b = orc.random_residue_matrix(k, n, p, 52)
+    gp = qg.plan_right_gpu(p, k, m)
+    if gp.balanced:
+        gp = qg.GpuPlan(gp.plan, gp.kblock_words, gp.max_exact_words, 0)
+    got = qg.mul_left_compressed_host(a, b, gp)
+    e = gp.plan.e
+    w = got.astype(np.uint64)
+    c = np.zeros((((m + e - 1) // e) * e, n), dtype=np.uint64)
+    for s in range(e):
+        c[s::e, :] = (w >> np.uint64(gp.plan.t * s)) & np.uint64((1 << gp.plan.t) - 1)
+    assert np.array_equal(c[:m].astype(np.uint32), orc.naive_gemm(p, a, b))

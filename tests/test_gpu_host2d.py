@@ -90,3 +90,4 @@ def test_host_left_ksplit(qg, orc, cuda, monkeypatch, p, m, k, n, parts):
     for s in range(e):
         c[s::e, :] = (w >> np.uint64(gp.plan.t * s)) & np.uint64((1 << gp.plan.t) - 1)
     assert np.array_equal(c[:m].astype(np.uint32), orc.naive_gemm(p, a, b))
+

@@ -167,6 +167,17 @@ inline ResidueMatrix mul_common_compressed(const ResidueMatrix& a, const Residue
         "mul_common_compressed");
   return c;
 }
+// The same over several GPUs of this process (qg_host_mul_common_multi): rows
+// of A and C sharded over `devices`, the packed B broadcast over NCCL.
+inline ResidueMatrix mul_common_compressed(const ResidueMatrix& a, const ResidueMatrix& b, const GpuPlan& plan,
+                                           const std::vector<int>& devices) {
+  detail::check_inner_dims(a, b);
+  ResidueMatrix c(a.rows, b.cols);
+  check(qg_host_mul_common_multi(&plan.c, devices.data(), (int)devices.size(), a.data.data(), b.data.data(), a.rows,
+                                 a.cols, b.cols, c.data.data()),
+        "mul_common_compressed");
+  return c;
+}
 // blocked_accumulate, gemm.hpp:450-489.
 inline ResidueMatrix blocked_accumulate(const ResidueMatrix& a, const ResidueMatrix& b,
                                         const CompressionPlan& plan, std::size_t kpanel) {

@@ -68,6 +68,7 @@ int main() {
   const auto c = mul_common_compressed(a, b, plan);
   CHECK(residue_checksum(c) == 262622u);
   CHECK(mul_common_compressed(a, b, plan_gpu(3, 512)) == c);
+  CHECK(mul_common_compressed(a, b, plan_gpu(3, 512), std::vector<int>{0}) == c);  // one-process multi-GPU entry
 
   // panel blocking (test_gemm.cpp:503-523): k twice past kmax
   const auto a14 = host_random_matrix(3, 14, 3, 31);

@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--big", action="store_true", help="shapes up to 4096 (the 128x128-tile kernels)")
     args = ap.parse_args()
     import torch
 
@@ -39,8 +40,12 @@ def main():
         for key in env_keys:
             os.environ.pop(key, None)
         p = rng.choice(primes)
-        m, n = rng.choice([1, 7, 64, 65, 300, 700, 1500]), rng.choice([1, 2, 33, 128, 129, 640, 1300])
-        k = rng.choice([1, 3, 50, 257, 1000, 3000, 6000])
+        if args.big:
+            m, n = rng.choice([1024, 2047, 2048, 3000, 4096]), rng.choice([1024, 1536, 2050, 4096])
+            k = rng.choice([256, 1000, 4096, 9000])
+        else:
+            m, n = rng.choice([1, 7, 64, 65, 300, 700, 1500]), rng.choice([1, 2, 33, 128, 129, 640, 1300])
+            k = rng.choice([1, 3, 50, 257, 1000, 3000, 6000])
         a = orc.random_residue_matrix(m, k, p, rng.randrange(1 << 30))
         b = orc.random_residue_matrix(k, n, p, rng.randrange(1 << 30))
         want = orc.naive_gemm(p, a, b)

@@ -13,10 +13,10 @@ for f in qg_abi.cu qg_dot.cu qg_small.cu qg_pack.cu qg_word64.cu; do
   nvcc $flags -c -o $bld/$f.o $here/paper_0803_1975_b200/csrc/$f &
   objs="$objs $bld/$f.o"
 done
-for f in qg_plan.cpp qg_io.cpp; do
+for f in qg_plan.cpp qg_io.cpp qg_multi.cpp; do
   nvcc $flags -x cu -c -o $bld/$f.o $here/paper_0803_1975_b200/csrc/$f &
   objs="$objs $bld/$f.o"
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libqgemm_b200.so $objs -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libqgemm_b200.so $objs -lcudart -ldl
 echo built $out/libqgemm_b200.so

@@ -2,13 +2,15 @@
 """bench.py — effective mod-p multiply-adds per second (2mnk/s) of the
 compressed modular GEMM on B200, the BASELINE.json metric.
 
-Workload (N=1): BASELINE config 2 — p=7, m=n=k=4096, dot-product variant
+Workload: BASELINE config 5 — p=3, m=n=k=32768, dot-product variant
 (Q-adic rows reversed / columns forward, FP64 tensor-core contraction,
-per-k-block digit extraction, mod-p accumulation between blocks).
+per-k-block digit extraction, mod-p accumulation between blocks), the config
+BASELINE's "1/2/4/8 B200" metric is quoted on (--config picks another).
 A "step" = pack A (K1) + pack B (K2) + the fused DMMA contraction/extract/mod-p
 kernel (K4) on device-resident residues (seeded SplitMix64, K0, generated
-once). For N>1 (torchrun) every rank owns m=4096 rows of A and C (weak
-scaling); rank 0 packs B and broadcasts the packed CB over NCCL each step.
+once). N>1 (torchrun, one process per GPU) is STRONG scaling: the fixed m
+rows of A and C are split over the ranks; each rank packs its own
+tile-column slot of B and the slots are all-gathered in place over NCCL.
 
 Keys beyond the base contract:
   roofline      the contraction kernel's achieved packed FP64 TFLOP/s vs the
@@ -119,48 +121,91 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU reference
-def reference_cpu_sample(p, m, k, n, target_s=4.0, threads=None, rows=None):
-    """Time the reference's own dot-product path (oracle/_ref: unmodified
-    compress_rows_reversed -> compress_cols_forward -> packed_common_product
-    -> reduce_common_entry, bench.hpp:127-146) at its own plan on a row
-    sample of the seeded workload, rows sharded over host threads.
-    Returns (rate 2*rows*n*k/s, rows, threads, seconds, C rows, plan)."""
-    import ctypes
+class RefCommon:
+    """The reference's own dot-product path (oracle/_ref: the unmodified
+    compress_cols_forward -> compress_rows_reversed -> packed_common_product
+    -> reduce_common_entry, bench.hpp:127-146) at its own plan, with the
+    packed B kept between calls: a full-size run packs B once for all m rows,
+    so a row sample is charged its pro-rata share (r/m) of the measured
+    single-threaded compress_cols_forward(B)."""
 
-    import numpy as np
+    def __init__(self, p, m, k, n):
+        import ctypes
 
-    import oracle
+        import oracle
 
-    ref = oracle.REF
-    kind = "reference"
-    threads = threads or host_threads()
-    pl = oracle.Plan()
-    if ref is None:
-        raise RuntimeError("oracle/_ref/libqgref.so is missing (built by __graft_entry__.build())")
-    st = ref.qgref_plan_compression(p, k, 53, 0, ctypes.byref(pl))
-    if st:
-        raise RuntimeError(f"reference plan failed: {st}")
-    b = oracle.random_residue_matrix(k, n, p, SEED + 1)
+        self.ref = oracle.REF
+        if self.ref is None:
+            raise RuntimeError("oracle/_ref/libqgref.so is missing (built by __graft_entry__.build())")
+        self.p, self.m, self.k, self.n = p, m, k, n
+        self.plan = oracle.Plan()
+        st = self.ref.qgref_plan_compression(p, k, 53, 0, ctypes.byref(self.plan))
+        if st:
+            raise RuntimeError(f"reference plan failed: {st}")
+        b = oracle.random_residue_matrix(k, n, p, SEED + 1)
+        sec = ctypes.c_double()
+        self.cb = self.ref.qgref_cb_create(ctypes.byref(self.plan), b.ctypes.data_as(ctypes.c_void_p), k, n,
+                                           ctypes.byref(sec))
+        if not self.cb:
+            raise RuntimeError("reference compress_cols_forward failed")
+        self.pack_b_s = sec.value
+        self._a = {}
 
-    def run(r):
-        a = oracle.random_residue_matrix(r, k, p, SEED)
-        c = np.empty((r, n), dtype=np.uint32)
-        mul, conv = ctypes.c_double(), ctypes.c_double()
-        t0 = time.perf_counter()
-        st = ref.qgref_mul_common(ctypes.byref(pl), a.ctypes.data_as(ctypes.c_void_p), b.ctypes.data_as(ctypes.c_void_p),
-                                  r, k, n, c.ctypes.data_as(ctypes.c_void_p), threads, ctypes.byref(mul), ctypes.byref(conv))
-        dt = time.perf_counter() - t0
+    def run(self, rows, threads):
+        """(charged seconds, wall seconds of the shards, C rows) for rows 0..rows-1."""
+        import ctypes
+
+        import numpy as np
+
+        import oracle
+
+        if rows not in self._a:
+            self._a = {rows: oracle.random_residue_matrix(rows, self.k, self.p, SEED)}
+        a = self._a[rows]
+        c = np.empty((rows, self.n), dtype=np.uint32)
+        wall = ctypes.c_double()
+        st = self.ref.qgref_mul_common_cb(ctypes.byref(self.plan), self.cb, a.ctypes.data_as(ctypes.c_void_p), rows,
+                                          self.k, c.ctypes.data_as(ctypes.c_void_p), threads, ctypes.byref(wall))
         if st:
             raise RuntimeError(f"reference mul_common failed: {st}")
-        return dt, c
+        return wall.value + self.pack_b_s * rows / self.m, wall.value, c
 
-    if rows is None:
-        pilot = max(threads, 8)
-        dt, _ = run(pilot)
-        rows = int(min(m, max(threads, pilot * target_s / max(dt, 1e-3))))
-        rows = max(threads, rows // threads * threads) if rows >= threads else rows
-    dt, c = run(rows)
-    return 2.0 * rows * n * k / dt, rows, threads, dt, c, pl, kind
+    def sample(self, threads, target_s, rows=None):
+        """Rate 2*rows*n*k / charged seconds on a row sample sized to ~target_s."""
+        if rows is None:
+            pilot = max(threads, 4)
+            dt, _, _ = self.run(pilot, threads)
+            rows = int(min(self.m, max(threads, pilot * target_s / max(dt, 1e-3))))
+            rows = max(threads, rows // threads * threads) if rows >= threads else max(1, rows)
+        dt, wall, c = self.run(rows, threads)
+        return 2.0 * rows * self.n * self.k / dt, rows, dt, c
+
+    def close(self):
+        if self.cb:
+            self.ref.qgref_cb_free(self.cb)
+            self.cb = None
+
+
+def reference_cpu_sample(p, m, k, n, target_s=4.0, threads=None, rows=None, one_thread_s=0.0):
+    """The reference's dot-product path on a row sample of the seeded workload,
+    rows sharded over all host threads (and, if one_thread_s > 0, a 1-thread
+    figure too). Returns a cpu_baseline dict and the sampled C rows."""
+    threads = threads or host_threads()
+    rc = RefCommon(p, m, k, n)
+    try:
+        rate, rows, dt, c = rc.sample(threads, target_s, rows)
+        out = {"value": rate, "unit": "mult-adds/s (2mnk/s)", "cores": threads, "kind": "reference",
+               "sample": f"rows 0..{rows - 1} of the same A x B ({rows}x{k} x {k}x{n}) through the reference's "
+                         f"compress_rows_reversed/packed_common_product/reduce_common_entry at its plan "
+                         f"t={rc.plan.t} e={rc.plan.e}, rows sharded over {threads} threads; "
+                         f"compress_cols_forward(B) ({rc.pack_b_s:.2f} s, 1 thread) charged pro rata {rows}/{m}",
+               "seconds": round(dt, 3), "pack_b_s": round(rc.pack_b_s, 3)}
+        if one_thread_s > 0:
+            r1, rows1, dt1, _ = rc.sample(1, one_thread_s)
+            out["one_thread"] = {"value": r1, "cores": 1, "rows": rows1, "seconds": round(dt1, 3)}
+        return out, c
+    finally:
+        rc.close()
 
 
 def reference_variant_sample(variant, p, m, k, n, target_s=4.0, threads=None, rows=None):
@@ -255,16 +300,23 @@ def reference_variant_sample(variant, p, m, k, n, target_s=4.0, threads=None, ro
 
 # ------------------------------------------------------------------ reference arm
 def reference_arm(args):
+    """The reference's own CPU implementation of the path (oracle/_ref, the
+    unmodified headers) on all host threads; each step is a bounded row
+    sample of the workload (B packed once before the steps and charged pro
+    rata per sample). Rank 0 alone runs it under torchrun."""
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
     p, m, k, n, desc = CONFIGS[args.config]
     variant = REDQ_VARIANTS.get(args.config, "common")
     rates, rows_used, thr = [], None, host_threads()
-    rows_used = None
+    rc = None
+    if variant == "common":
+        rc = RefCommon(p, m, k, n)
     for i in range(args.warmup + args.steps):
         if variant == "common":
-            rate, rows, thr, dt, _, pl, kind = reference_cpu_sample(p, m, k, n, target_s=args.ref_step_s, rows=rows_used)
+            rate, rows, dt, _ = rc.sample(thr, args.ref_step_s, rows_used)
+            pdesc = f"t={rc.plan.t} e={rc.plan.e}"
         else:
             try:
                 rate, rows, thr, dt, _, pl, kind = reference_variant_sample(variant, p, m, k, n,
@@ -272,19 +324,23 @@ def reference_arm(args):
             except RuntimeError as ex:
                 print(json.dumps({"impl": "reference", "unavailable": str(ex)}), flush=True)
                 return 0
+            pdesc = (f"t={pl.base.t} dq={pl.dq} dtheta={pl.dtheta}" if variant == "full" else f"t={pl.t} e={pl.e}")
         rows_used = rows
         if i >= args.warmup:
             rates.append(rate)
     value = sum(rates) / len(rates)
-    pdesc = (f"t={pl.base.t} dq={pl.dq} dtheta={pl.dtheta}" if variant == "full" else f"t={pl.t} e={pl.e}")
     sample = (f"rows 0..{rows_used - 1} of A ({rows_used}x{k}) x B ({k}x{n}), {variant} variant, reference plan "
               f"{pdesc}, {thr} threads")
+    if rc is not None:
+        sample += f"; compress_cols_forward(B) ({rc.pack_b_s:.2f} s, once) charged pro rata {rows_used}/{m} per step"
+        rc.close()
     line = {
         "impl": "reference", "metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": value, "unit": "mult-adds/s (2mnk/s)",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * rows_used * n * k / value * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 seed 42/43)",
+        "higher_is_better": True, "scaling": "strong" if variant == "common" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (SplitMix64 seed 42/43)",
         "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n},
-        "cpu_baseline": {"value": value, "unit": "mult-adds/s (2mnk/s)", "cores": thr, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "mult-adds/s (2mnk/s)", "cores": thr, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "mult-adds/s (2mnk/s)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -502,15 +558,21 @@ def redq_arm(args):
 
 
 def our_arm(args):
-    import numpy as np
-    import torch
+    """The dot-product variant (configs 1, 2, 3, 5). N=1: the whole product on
+    one GPU, the step one CUDA graph (both packs on forked branches + the
+    contraction). N>1 (torchrun, one process per GPU): STRONG scaling — the
+    fixed m rows of A and C are sharded over the ranks (m/N each); every rank
+    packs its own tile-column slot of B, the slots are all-gathered in place
+    over NCCL (dist.mul_common_allgather) while the rank packs its CA shard
+    and contracts its own columns, then it contracts the rest."""
     import ctypes
 
+    import numpy as np
+    import torch
     import torch.distributed as dist
 
     import paper_0803_1975_b200 as qg
-    from paper_0803_1975_b200.dist import (PanelOps, ShardOps, mul_common_sharded, mul_common_sharded_pipelined,
-                                           panel_bounds)
+    from paper_0803_1975_b200.dist import GatherOps, gather_slot, mul_common_allgather, shard_rows_aligned
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -524,102 +586,93 @@ def our_arm(args):
     dev = torch.device("cuda", local_dev)
     if world > 1:
         if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
 
-    p, m_rank, k, n, desc = CONFIGS[args.config]
+    p, m, k, n, desc = CONFIGS[args.config]
     gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
     if args.kblock:  # experiments: override the k-block of the chosen plan
         gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words, gp.balanced)
     pl = gp.plan
     K = -(-k // pl.e)
-    m_total = m_rank * world
-    row0 = rank * m_rank
+    row0, m_rank = shard_rows_aligned(m, world, rank)
 
-    # device-resident seeded inputs (K0): this rank's rows of A, all of B on rank 0
-    a = qg.random_residue_matrix(m_rank, k, p, SEED, row0=row0)
-    b = qg.random_residue_matrix(k, n, p, SEED + 1) if rank == 0 else None
+    # device-resident seeded inputs (K0): this rank's rows of A; B (every rank
+    # reads only its own tile-column slot of it when N > 1)
+    a = qg.random_residue_matrix(max(m_rank, 1), k, p, SEED, row0=row0)
+    b = qg.random_residue_matrix(k, n, p, SEED + 1)
     bk_c = ctypes.c_uint32()
     gpc = gp._c()
     qg._check(qg.lib.qg_tiled_stage_words(ctypes.byref(gpc), k, ctypes.byref(bk_c)))
     bk = bk_c.value
-    # tiled packed layouts (dense zero-padded 128 x bk blocks, CB transposed)
-    ca = torch.empty(qg.lib.qg_tiled_words(m_rank, k, pl.e, bk), dtype=torch.float64, device=dev)
-    cb = torch.empty(qg.lib.qg_tiled_words(n, k, pl.e, bk), dtype=torch.float64, device=dev)
-    c = torch.empty((m_rank, n), dtype=torch.int32, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
-    stream = torch.cuda.current_stream()
-    sp = qg._stream
-    plc = pl._c()
-
-    def pack_rows(a_):
-        qg._check(qg.lib.qg_pack_a_tiled(ctypes.byref(gpc), bk, qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), sp()))
-        return ca
-
-    def pack_cols(b_):
-        qg._check(qg.lib.qg_pack_b_tiled(ctypes.byref(gpc), bk, qg._ptr(b_), 0, k, n, n, qg._ptr(cb), sp()))
-        return cb
-
-    ev = {}
-
-    def contract(ca_, cb_):
-        ev["c0"].record(stream)
-        qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca_), qg._ptr(cb_), m_rank, n, k, qg._ptr(c), n, sp()))
-        ev["c1"].record(stream)
-        return c
-
-    ops = ShardOps(pack_rows=pack_rows, pack_cols=pack_cols, empty_cb=lambda shape: cb, contract=contract)
-    # multi-rank: the packed B goes out in column panels, each broadcast queued
-    # behind the pack that produced it, so rank 0's packing overlaps the wire
     Kt = (K + bk - 1) // bk
     Nt = (n + 127) // 128
     W = Kt * 128 * bk  # words per 128-column tile column of CB_t
+    _, _, P = gather_slot(Nt, world, rank)
+    # tiled packed layouts (dense zero-padded 128 x bk blocks, CB transposed);
+    # N > 1: CB_t holds world * P tile columns (equal all-gather slots)
+    ca = torch.empty(max(1, qg.lib.qg_tiled_words(m_rank, k, pl.e, bk)), dtype=torch.float64, device=dev)
+    cb = torch.zeros(world * P * W if world > 1 else qg.lib.qg_tiled_words(n, k, pl.e, bk), dtype=torch.float64,
+                     device=dev)
+    c = torch.empty((max(m_rank, 1), n), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    sp = qg._stream
 
-    def panel_views(cb_, panels):
-        return [cb_[t0 * W:t1 * W] for t0, t1 in (panel_bounds(Nt, panels, j) for j in range(panels))]
+    def pack_rows(a_):
+        if m_rank:
+            qg._check(qg.lib.qg_pack_a_tiled(ctypes.byref(gpc), bk, qg._ptr(a_), 0, m_rank, k, k, qg._ptr(ca), sp()))
+        return ca
 
-    def pack_cols_panel(b_, j, panels, cb_):
-        t0, t1 = panel_bounds(Nt, panels, j)
+    def pack_cols_slot(b_, t0, t1, slot):
         c0, c1 = t0 * 128, min(n, t1 * 128)
         if c1 > c0:
             qg._check(qg.lib.qg_pack_b_tiled(ctypes.byref(gpc), bk, ctypes.c_void_p(b_.data_ptr() + c0 * 8), 0, k,
-                                             c1 - c0, n, ctypes.c_void_p(cb_.data_ptr() + t0 * W * 8), sp()))
+                                             c1 - c0, n, qg._ptr(slot), sp()))
 
-    pops = PanelOps(pack_rows=pack_rows, panel_views=panel_views, pack_cols_panel=pack_cols_panel, contract=contract)
-    panels = max(1, min(args.bcast_panels, Nt))
+    kern_events = []
+
+    def contract(ca_, cb_, t0, t1):
+        c0, c1 = t0 * 128, min(n, t1 * 128)
+        if c1 <= c0 or not m_rank:
+            return
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca_), ctypes.c_void_p(cb_.data_ptr() + t0 * W * 8),
+                                             m_rank, c1 - c0, k, ctypes.c_void_p(c.data_ptr() + c0 * 4), n, sp()))
+        e1.record(stream)
+        kern_events.append((e0, e1))
+
+    ops = GatherOps(pack_rows=pack_rows, pack_cols_slot=pack_cols_slot, contract=contract)
 
     def step():
-        if world > 1 and panels > 1:
-            return mul_common_sharded_pipelined(a, b, cb, pops, rank, world, panels)
-        return mul_common_sharded(a, b, tuple(cb.shape), ops, rank, world)
+        mul_common_allgather(a, b, cb, ops, rank, world, Nt)
 
     for _ in range(args.warmup):
-        ev["c0"], ev["c1"] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         step()
     torch.cuda.synchronize()
+    kern_events.clear()
 
     # One GPU: the step's launches are captured once into one CUDA graph
-    # (packs, then the contraction) and replayed, so host launch gaps stay out
-    # of the step (they dominate small shapes such as config 1); the
-    # contraction's timing events are record nodes inside the graph.
+    # (both packs on forked branches, then the contraction) and replayed, so
+    # host launch gaps stay out of the step (they dominate small shapes such
+    # as config 1); the contraction's timing events are record nodes inside it.
     use_graph = world == 1 and not args.no_graph
     launches_per_step = None
     kernel_name = None
     if use_graph:
-        # the whole step (both packs, concurrent, + the contraction) is ONE graph; the
-        # contraction's timing events are record nodes inside it (external
-        # events), so no host launch gap sits between packs and contraction
         g_step = torch.cuda.CUDAGraph()
         gc0 = torch.cuda.Event(enable_timing=True, external=True)
         gc1 = torch.cuda.Event(enable_timing=True, external=True)
         n0 = qg.kernel_launches()
         side = torch.cuda.Stream()
         with torch.cuda.graph(g_step):
-            # the two packs are independent: B's runs on a forked branch of the graph
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
-                pack_cols(b)
+                pack_cols_slot(b, 0, Nt, cb)
             pack_rows(a)
             torch.cuda.current_stream().wait_stream(side)
             gc0.record()
@@ -631,8 +684,7 @@ def our_arm(args):
 
         def step():  # noqa: F811
             g_step.replay()
-            ev["c0"], ev["c1"] = gc0, gc1
-            return c
+            kern_events.append((gc0, gc1))
 
         for _ in range(3):
             step()
@@ -647,14 +699,14 @@ def our_arm(args):
     with ClockSampler(local_dev) as clk:
         for _ in range(args.steps):
             flush.fill_(1)  # evict L2 between timed steps (outside the events)
+            kern_events.clear()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ev["c0"], ev["c1"] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             step()
             s1.record(stream)
             s1.synchronize()
             step_ms.append(s0.elapsed_time(s1))
-            contract_ms.append(ev["c0"].elapsed_time(ev["c1"]))
+            contract_ms.append(sum(e0.elapsed_time(e1) for e0, e1 in kern_events))
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -662,67 +714,81 @@ def our_arm(args):
     launches = qg.kernel_launches() - launches0
     if use_graph:  # replays do not pass through the library's launch counter
         launches = launches_per_step * args.steps
+    kernel_name = kernel_name or qg.last_kernel()
     total_ms = sum(step_ms)
+    per_rank_ms = [total_ms / args.steps]
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank_ms = [float(x.item()) / args.steps for x in allt]
+        total_ms = max(float(x.item()) for x in allt)
     ms_per_step = total_ms / args.steps
-    value = 2.0 * m_total * n * k / (ms_per_step * 1e-3)
+    value = 2.0 * m * n * k / (ms_per_step * 1e-3)
 
     # parity spot-check inside the bench: checksum of this rank's C
-    checksum = qg.residue_checksum(c)
+    checksum = qg.residue_checksum(c[:m_rank]) if m_rank else 0
+    if world > 1:
+        cs = torch.tensor([checksum], dtype=torch.int64, device=dev)
+        dist.all_reduce(cs)
+        checksum = int(cs.item()) & 0xFFFFFFFF
 
     contract_avg = sum(contract_ms) / len(contract_ms)
-    packed_flop = 2.0 * m_rank * n * K  # per launch: packed words, not padding
+    packed_flop = 2.0 * m_rank * n * K  # per step on this rank: packed words, not padding
     peak_doc = load_json(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) or {}
     peak = float(peak_doc.get("dmma_m8n8k4_tflops", 37.09))
-    achieved = packed_flop / (contract_avg * 1e-3) / 1e12
+    achieved = packed_flop / (contract_avg * 1e-3) / 1e12 if contract_avg > 0 else 0.0
     ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
     traffic = ncu.get("contraction", {}).get(args.config, {}).get("dram_bytes") if ncu else None
     roofline = {"bound": "tensor", "achieved": round(achieved, 3), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": kernel_name or qg.last_kernel(), "kernel_ms": round(contract_avg, 4),
+                "kernel": kernel_name, "kernel_ms": round(contract_avg, 4),
                 "share_of_step": round(contract_avg / (sum(step_ms) / len(step_ms)), 4),
                 "peak_source": "measured DMMA.8x8x4 microbenchmark on this pool (profiles/r01_fp64_peak.json); "
                                "cuBLAS DGEMM 35.7 TF/s",
-                "algorithmic_flop_per_launch": packed_flop}
+                "algorithmic_flop_per_launch": packed_flop,
+                "per_unit": "2 FLOP per packed word product; m_rank x n x ceil(k/e) products per step"}
+    if world > 1:
+        roofline["note"] = (f"rank 0's contraction launches ({'1 own-slot + rest' if world > 1 else ''}) summed; "
+                            "the own-slot launch shares the SMs with the NCCL all-gather")
 
+    par = (f"strong scaling: {world} ranks x {m_rank} rows of the fixed m={m}; packed B assembled by an in-place "
+           f"NCCL all-gather of per-rank tile-column slots ({P} of {Nt} tile columns each), own slot contracted "
+           f"first" if world > 1 else "single GPU")
     line = {
         "metric": "effective mod-p mult-adds/sec (2mnk/s)", "value": value, "unit": "mult-adds/s (2mnk/s)",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
-        "config": {"workload": desc + (f"; {world} ranks x {m_rank} rows, CB broadcast over {args.dist_backend.upper()}"
-                                       f" in {panels} column panels pipelined with rank 0's packing" if world > 1 else ""),
-                   "p": p, "m": m_total, "k": k, "n": n,
+        "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n,
                    "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
-                            "source": args.plan},
+                            "balanced": bool(gp.balanced), "source": args.plan},
                    "layout": "tiled packed operands (128 x stage_words blocks, CB transposed)" + (
                        "; contraction on 64x64 tiles with k split over a thread-block cluster"
                        if (kernel_name or "").startswith("small") else ""),
-                   "l2": "flushed between timed steps (256 MiB write); A,B residues (2x128 MiB f64) exceed the 126 MB L2",
-                   "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                   "l2": f"flushed between timed steps (256 MiB write); A,B residues "
+                         f"({(m_rank * k + k * n) * 8 / 2**20:.0f} MiB f64 per rank) exceed the 126 MB L2",
+                   "parallelism": par,
                    "launch": "one CUDA graph per step (packs + contraction)" if use_graph else "direct launches"},
         "roofline": roofline,
         "gpu_launches": launches,
-        "checksum_rank0": checksum if rank == 0 else None,
+        "checksum_c": checksum,
+        "per_rank_ms": [round(x, 3) for x in per_rank_ms],
         "wall_s_timed_region": round(wall, 4),
     }
     line["clocks"] = clk.summary()
+    del flush
 
     if not args.no_e2e:
-        e2e = e2e_measure(qg, gp, p, m_rank, k, n, args, rank, world, device_c=c)
+        e2e = e2e_measure(qg, gp, p, m, k, n, args, rank, world, device_c=c[:m_rank])
         if rank == 0:
             line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, rows, thr, dt, c_cpu, rpl, kind = reference_cpu_sample(p, m_rank, k, n, target_s=args.cpu_s)
-            agree = bool(np.array_equal(c[:rows].cpu().numpy().astype(np.uint32), c_cpu))
-            line["cpu_baseline"] = {"value": rate, "unit": "mult-adds/s (2mnk/s)", "cores": thr, "kind": kind,
-                                    "sample": f"rows 0..{rows - 1} of the same A x B ({rows}x{k} x {k}x{n}), reference plan "
-                                              f"t={rpl.t} e={rpl.e}, {dt:.2f} s wall",
-                                    "rows_bit_exact_vs_gpu": agree}
+            base, c_cpu = reference_cpu_sample(p, m, k, n, target_s=args.cpu_s, one_thread_s=args.cpu1_s)
+            base["rows_bit_exact_vs_gpu"] = bool(np.array_equal(c[:c_cpu.shape[0]].cpu().numpy().astype(np.uint32),
+                                                                c_cpu))
+            line["cpu_baseline"] = base
         except Exception as ex:  # the baseline must not kill the measurement
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:
@@ -733,68 +799,93 @@ def our_arm(args):
 
 
 def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1, device_c=None):
-    """Same metric through the public host-buffer API (pinned buffers):
-    H2D of A and B (uint32 ResidueMatrix data), pack + contraction kernels,
-    D2H of C, every step. At N GPUs every rank calls the API on its own row
-    shard of A (rows rank*m ..), time = max over ranks."""
+    """Same metric through the public host-buffer API: H2D of A and B (uint32
+    ResidueMatrix data), pack + contraction kernels, D2H of C, every step.
+    Headline from pinned host buffers; the same call on pageable buffers (a
+    plain std::vector / numpy array, what a reference caller passes) is
+    reported beside it. N > 1: every rank runs the API on its own row shard
+    (rows row0.. of the fixed m), time = max over ranks."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
+    from paper_0803_1975_b200.dist import shard_rows_aligned
+
+    row0, mr = shard_rows_aligned(m, world, rank)
     # seeded host inputs, made on the device by the library (K0) and copied out
     # before the timed region
-    a = torch.empty((m, k), dtype=torch.int32, pin_memory=True)
+    a = torch.empty((mr, k), dtype=torch.int32, pin_memory=True)
     b = torch.empty((k, n), dtype=torch.int32, pin_memory=True)
-    c = torch.empty((m, n), dtype=torch.int32, pin_memory=True)
-    a.copy_(qg.random_residue_matrix(m, k, p, SEED, row0=rank * m, dtype=torch.int32))
+    c = torch.empty((mr, n), dtype=torch.int32, pin_memory=True)
+    if mr:
+        a.copy_(qg.random_residue_matrix(mr, k, p, SEED, row0=row0, dtype=torch.int32))
     b.copy_(qg.random_residue_matrix(k, n, p, SEED + 1, dtype=torch.int32))
     torch.cuda.synchronize()
     an, bn, cn = a.numpy().view(np.uint32), b.numpy().view(np.uint32), c.numpy().view(np.uint32)
-    for _ in range(3):
-        qg.mul_common_compressed_host(an, bn, gp, out=cn)
-    times = []
-    for _ in range(args.e2e_steps):
+
+    def timed(a_, b_, c_, steps):
+        for _ in range(2):
+            qg.mul_common_compressed_host(a_, b_, gp, out=c_)
+        times = []
+        for _ in range(steps):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            qg.mul_common_compressed_host(a_, b_, gp, out=c_)
+            times.append(time.perf_counter() - t0)
+        t = sum(times) / len(times)
         if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        qg.mul_common_compressed_host(an, bn, gp, out=cn)
-        times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
-    if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-    return {"value": 2.0 * m * world * n * k / t, "unit": "mult-adds/s (2mnk/s)",
-            "h2d_bytes_per_step": int(a.numel() * 4 + b.numel() * 4) * world,
-            "d2h_bytes_per_step": int(c.numel() * 4) * world, "ms_per_step": t * 1e3,
-            "api": "mul_common_compressed_host (qg_host_mul_common_gpu), pipelined H2D/compute/D2H",
-            "checksum_rank0": int(cn.astype(np.uint64).sum() & 0xFFFFFFFF),
-            "matches_device": None if device_c is None else
-            bool(np.array_equal(cn, device_c.cpu().numpy().astype(np.uint32)))}
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    t = timed(an, bn, cn, args.e2e_steps)
+    out = {"value": 2.0 * m * n * k / t, "unit": "mult-adds/s (2mnk/s)",
+           "h2d_bytes_per_step": int((m * k + world * k * n) * 4),
+           "d2h_bytes_per_step": int(m * n * 4), "ms_per_step": t * 1e3,
+           "api": "mul_common_compressed_host (qg_host_mul_common_gpu), pipelined H2D/compute/D2H, pinned buffers"
+                  + (f"; each of {world} ranks on its row shard with all of B" if world > 1 else ""),
+           "checksum_rank0": int(cn.astype(np.uint64).sum() & 0xFFFFFFFF),
+           "matches_device": None if device_c is None else
+           bool(np.array_equal(cn, device_c.cpu().numpy().astype(np.uint32)))}
+    if args.pageable and world == 1:
+        del a, b, c
+        ap_, bp_ = np.array(an), np.array(bn)  # plain (pageable) copies
+        cp_ = np.empty_like(cn)
+        tpg = timed(ap_, bp_, cp_, max(2, args.e2e_steps // 2))
+        out["pageable"] = {"value": 2.0 * m * n * k / tpg, "ms_per_step": tpg * 1e3,
+                           "api": "the same call on pageable (non-pinned) numpy buffers",
+                           "matches_pinned": bool(np.array_equal(cp_, cn))}
+    return out
 
 
-def main():
+def make_parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="config5", choices=sorted(CONFIGS))
     ap.add_argument("--plan", default="gpu", choices=["gpu", "reference"],
                     help="gpu: planner-chosen (t, e, kblock); reference: plan_compression's plan")
     ap.add_argument("--kblock", type=int, default=0, help="override the plan's k-block (words)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path with several ranks on one GPU")
-    ap.add_argument("--bcast-panels", type=int, default=4,
-                    help="N>1: column panels the packed B is broadcast in (1 = one broadcast after the whole pack)")
+    ap.add_argument("--pageable", type=int, default=1, help="also time e2e from pageable host buffers (N=1)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
+    ap.add_argument("--cpu1-s", type=float, default=3.0, help="target seconds of the 1-thread CPU sample (0: skip)")
     ap.add_argument("--ref-step-s", type=float, default=2.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step's kernels directly (no CUDA graph)")
     ap.add_argument("--redq-plan", default="", help="experiments: right/left plan 't:e:kblock_residues:balanced'")
-    args = ap.parse_args()
+    return ap
+
+
+def main():
+    args = make_parser().parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

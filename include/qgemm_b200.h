@@ -120,6 +120,12 @@ enum { QG_PLAN_UNSIGNED_ONLY = 1 };
 int qg_plan_gpu_ex(uint32_t p, uint64_t k, int flags, qg_gpu_plan* out);
 /* Eq. G bound for balanced digits (qg_gpu_plan.balanced = 1). */
 int qg_max_exact_block_balanced(const qg_plan* plan, uint64_t* words);
+/* Eq. 3 bound (residues per k-block) that the contraction enforces for a GPU
+ * plan, recomputed from (p, t): largest_common_dim (plan.hpp:113-115), capped
+ * by a smaller plan.kmax, for unsigned plans; the balanced-digit bound
+ * ((2^(t-1) - 1) / floor(p/2)^2) for balanced ones. plan.kmax itself always
+ * stays the reference's meaning. */
+int qg_gpu_plan_kmax(const qg_gpu_plan* gplan, uint64_t* kmax);
 
 /* -------------------------------------------------- device (stream-ordered) */
 /* random_residue_matrix, prng.hpp:31-38 (SplitMix64 stream, counter-based):

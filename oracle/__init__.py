@@ -147,6 +147,9 @@ def _load_ref():
         "qgref_compress_outer_rows": ([P(Plan), vp, sz, sz, vp], i32),
         "qgref_packed_common_product": ([P(Plan), vp, vp, sz, sz, sz, vp], i32),
         "qgref_mul_common": ([P(Plan), vp, vp, sz, sz, sz, vp, i32, dp, dp], i32),
+        "qgref_cb_create": ([P(Plan), vp, sz, sz, dp], vp),
+        "qgref_cb_free": ([vp], None),
+        "qgref_mul_common_cb": ([P(Plan), vp, vp, sz, sz, vp, i32, dp], i32),
         "qgref_mul_right": ([P(Plan), vp, vp, sz, sz, sz, vp, vp, i32, dp, dp], i32),
         "qgref_blocked_accumulate": ([P(Plan), vp, vp, sz, sz, sz, sz, vp], i32),
         "qgref_plan_full": ([u32, u64, i32, P(FullPlan)], i32),

@@ -225,6 +225,47 @@ int qgref_mul_common(const qgo_plan* plan, const uint32_t* a, const uint32_t* b,
   });
 }
 
+// The same dot-product path with the packed B kept between calls, so that a
+// row sample can be charged its pro-rata share of compress_cols_forward(B)
+// (a full-size run packs B once for all m rows, bench.hpp:127-146):
+//   qgref_cb_create  packs B (the reference's single-threaded call) and
+//                    reports its seconds;
+//   qgref_mul_common_cb  compress_rows_reversed + packed_common_product +
+//                    reduce_common_entry on `m` rows, sharded over threads.
+void* qgref_cb_create(const qgo_plan* plan, const uint32_t* b, size_t k, size_t n, double* sec_pack) {
+  CompressedMatrix<DoubleWord>* out = nullptr;
+  const int st = guarded([&] {
+    const CompressionPlan pl = import_plan(plan);
+    const ResidueMatrix bm = wrap(b, k, n);
+    const auto t0 = std::chrono::steady_clock::now();
+    out = new CompressedMatrix<DoubleWord>(compress_cols_forward<DoubleWord>(bm, pl));
+    if (sec_pack) *sec_pack = seconds_since(t0);
+  });
+  return st == QGO_OK ? out : nullptr;
+}
+
+void qgref_cb_free(void* cb) { delete static_cast<CompressedMatrix<DoubleWord>*>(cb); }
+
+int qgref_mul_common_cb(const qgo_plan* plan, const void* cbh, const uint32_t* a, size_t m, size_t k,
+                        uint32_t* c, int threads, double* sec_wall) {
+  return guarded([&] {
+    const CompressionPlan pl = import_plan(plan);
+    const auto& cb = *static_cast<const CompressedMatrix<DoubleWord>*>(cbh);
+    const size_t n = cb.logical_cols;
+    const int nth = threads > 0 ? threads : 1;
+    const auto t0 = std::chrono::steady_clock::now();
+    shard_rows(m, nth, [&](size_t r0, size_t r1) {
+      if (r0 >= r1) return;
+      ResidueMatrix as(r1 - r0, k);
+      std::memcpy(as.data.data(), a + r0 * k, (r1 - r0) * k * sizeof(uint32_t));
+      const auto ca = compress_rows_reversed<DoubleWord>(as, pl);
+      const auto acc = packed_common_product(ca, cb);
+      for (size_t i = 0; i < acc.size(); ++i) c[r0 * n + i] = reduce_common_entry(acc[i], pl);
+    });
+    if (sec_wall) *sec_wall = seconds_since(t0);
+  });
+}
+
 // Mixed/right variant (bench.hpp:148-165): compress_outer_cols, packed_right_product,
 // redq_in_place; cc gets the post-REDQ words (m x ceil(n/e)), c (optional) the uncompressed C.
 int qgref_mul_right(const qgo_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,

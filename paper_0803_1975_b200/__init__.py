@@ -156,6 +156,7 @@ def _load():
         "qg_plan_gpu": ([u32, u64, P(_GpuPlan)], i32),
         "qg_plan_gpu_ex": ([u32, u64, i32, P(_GpuPlan)], i32),
         "qg_max_exact_block_balanced": ([P(_Plan), P(u64)], i32),
+        "qg_gpu_plan_kmax": ([P(_GpuPlan), P(u64)], i32),
         "qg_gen_residues": ([u64, u32, sz, sz, sz, vp, i32, vp], i32),
         "qg_compress_rows_reversed": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
         "qg_compress_cols_forward": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
@@ -317,6 +318,15 @@ class GpuPlan:
     @staticmethod
     def _from(c: "_GpuPlan") -> "GpuPlan":
         return GpuPlan(CompressionPlan._from(c.plan), c.kblock_words, c.max_exact_words, c.balanced)
+
+    def eq3_kmax(self) -> int:
+        """Residues a k-block may hold (Eq. 3) for this plan's digits
+        (qg_gpu_plan_kmax): plan.kmax's bound for unsigned digits, the
+        balanced-digit bound for balanced ones."""
+        out = ctypes.c_uint64()
+        g = self._c()
+        _check(lib.qg_gpu_plan_kmax(ctypes.byref(g), ctypes.byref(out)))
+        return out.value
 
 
 def make_plan(p: int, t: int, e: int, beta: int = 53) -> CompressionPlan:

@@ -23,6 +23,8 @@ uint64_t stage_block_tiled(uint64_t limit, int* bk);
 uint64_t stage_block_redq(uint64_t limit, int* bk);
 int stage_single(uint64_t K);
 uint64_t max_exact_block_balanced(uint32_t p, int t, int e);
+uint64_t largest_common_dim(uint32_t p, int t);
+uint64_t largest_common_dim_balanced(uint32_t p, int t);
 }  // namespace qg
 
 namespace qgk {
@@ -60,6 +62,17 @@ int check_plan(const qg_plan* plan) {
 }
 
 // kernel arguments carry dimensions as int: larger ones are refused, not wrapped
+// Eq. 3 bound of a GPU plan, recomputed from (p, t) instead of trusting the
+// struct's kmax field: balanced digits (|v| <= p/2) have their own, ~4x
+// larger bound; an unsigned plan keeps a caller's smaller kmax (the
+// AddHighBits reduction, plan.hpp:150-157) but never exceeds plan.hpp:113-115.
+uint64_t gpu_kmax(const qg_gpu_plan* gp) {
+  const qg_plan& pl = gp->plan;
+  if (gp->balanced) return qg::largest_common_dim_balanced(pl.p, pl.t);
+  const uint64_t lcd = qg::largest_common_dim(pl.p, pl.t);
+  return pl.kmax < lcd ? pl.kmax : lcd;
+}
+
 bool dims_ok(size_t a, size_t b, size_t c = 0) {
   const size_t lim = 0x7FFFFFFF;
   return a <= lim && b <= lim && c <= lim;
@@ -110,7 +123,7 @@ int run_common(const qg_plan& pl, uint64_t kblock, const double* ca, size_t ldca
   const uint64_t exact = qg::max_exact_block(pl.p, pl.t, pl.e);
   const uint32_t qmask = (uint32_t)((1ull << pl.t) - 1);
   uint64_t kb = kblock < K ? kblock : K;
-  if (kb > exact) kb = exact;
+  if (kb > exact) return QG_NOT_EXACT;  // a block past Eq. G: refused, never clamped silently
   int bk = 32;
   uint64_t blk = K;  // words per k-block
   bool dmma = kb >= K;
@@ -174,8 +187,8 @@ int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
   const qg_plan& pl = gp->plan;
   const uint64_t exact = gp->balanced ? qg::max_exact_block_balanced(pl.p, pl.t, pl.e)
                                       : qg::max_exact_block(pl.p, pl.t, pl.e);
-  uint64_t kb = gp->kblock_words < K ? gp->kblock_words : K;
-  if (kb > exact) kb = exact;
+  const uint64_t kb = gp->kblock_words < K ? gp->kblock_words : K;
+  if (kb > exact) return QG_NOT_EXACT;  // a block past Eq. G: refused, never clamped silently
   if (kb >= K) {
     const char* e = getenv("QG_TILED_SINGLE_BK");  // experiments
     *bk = e ? atoi(e) : qg::stage_single(K);
@@ -191,6 +204,14 @@ int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
 }  // namespace
 
 extern "C" {
+
+int qg_gpu_plan_kmax(const qg_gpu_plan* gplan, uint64_t* kmax) {
+  if (!gplan || !kmax) return QG_INVALID_ARGUMENT;
+  int st = check_plan(&gplan->plan);
+  if (st) return st;
+  *kmax = gpu_kmax(gplan);
+  return QG_OK;
+}
 
 int qg_tiled_stage_words(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk) {
   if (!gplan || !bk) return QG_INVALID_ARGUMENT;
@@ -297,8 +318,12 @@ static int redq_product(const qg_gpu_plan* gplan, const double* a_t, const doubl
   if ((st = right_tiled_geometry(gplan, k, &bk, &kbs))) return st;
   if (kbs == 0) {
     if (bal ? (uint64_t)k * pm >= lim : k > pl.kmax) return QG_PLAN_MISMATCH;  // gemm.hpp:295 for unsigned
-  } else if (h + (uint64_t)kbs * bk * pm >= lim) {
-    return QG_PLAN_MISMATCH;  // a block would overflow a digit after the in-place REDQ
+    // continuing from REDQ'd words: their digits (< p) add to the block's sums
+    if (accumulate && h + (uint64_t)k * pm >= lim) return QG_PLAN_MISMATCH;
+  } else if (h + (uint64_t)gplan->kblock_words * pm >= lim) {
+    // the plan's block (before rounding down to whole stages) would overflow
+    // a digit after the in-place REDQ: refused, never rounded into range
+    return QG_PLAN_MISMATCH;
   }
   if (ldcc < N) return QG_INVALID_ARGUMENT;
   if (M == 0 || N == 0) return QG_OK;
@@ -522,8 +547,9 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   const size_t K = ceil_div(k, pl.e);
   const uint64_t kb = gplan->kblock_words;
   if (kb == 0) return QG_INVALID_ARGUMENT;
-  if (kb < K && kb * (uint64_t)pl.e > pl.kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
-  if (kb >= K && k > pl.kmax) return QG_PLAN_MISMATCH;
+  const uint64_t kmax = gpu_kmax(gplan);
+  if (kb < K && kb * (uint64_t)pl.e > kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
+  if (kb >= K && k > kmax) return QG_PLAN_MISMATCH;
   if (m == 0 || n == 0) return QG_OK;
   int bk = 0, kbs = 0;
   if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
@@ -596,8 +622,9 @@ int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda
   const size_t K = ceil_div(k, (size_t)pl.e);
   const uint64_t kb = gplan->kblock_words;
   if (kb == 0) return QG_INVALID_ARGUMENT;
-  if (kb < K && kb * (uint64_t)pl.e > pl.kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
-  if (kb >= K && k > pl.kmax) return QG_PLAN_MISMATCH;
+  const uint64_t kmax = gpu_kmax(gplan);
+  if (kb < K && kb * (uint64_t)pl.e > kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
+  if (kb >= K && k > kmax) return QG_PLAN_MISMATCH;
   if (pl.t * pl.e > 53) return QG_PLAN_MISMATCH;  // DoubleWord words only
   if (!dims_ok(m, n, k) || !dims_ok(lda, ldb, ldc)) return QG_INVALID_ARGUMENT;
   if (m == 0 || n == 0) return QG_OK;
@@ -750,8 +777,9 @@ int qg_mul_common(const qg_gpu_plan* gplan, const double* ca, const double* cb, 
   uint64_t kb = gplan->kblock_words;
   if (kb == 0) return QG_INVALID_ARGUMENT;
   // Eq. 3 per block (gemm.hpp:456): a block may hold at most kmax residues.
-  if (kb < K && kb * (uint64_t)pl.e > pl.kmax) return QG_PLAN_MISMATCH;
-  if (kb >= K && k > pl.kmax) return QG_PLAN_MISMATCH;
+  const uint64_t kmax = gpu_kmax(gplan);
+  if (kb < K && kb * (uint64_t)pl.e > kmax) return QG_PLAN_MISMATCH;
+  if (kb >= K && k > kmax) return QG_PLAN_MISMATCH;
   if (K == 0) {
     cudaStream_t s = as_stream(stream);
     for (size_t i = 0; i < m; ++i)

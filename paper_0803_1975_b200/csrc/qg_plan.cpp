@@ -575,7 +575,6 @@ int qg_plan_gpu_ex(uint32_t p, uint64_t k, int flags, qg_gpu_plan* out) {
         best_cost = cost;
         found = true;
         fill(&best.plan, p, t, e, 53, std::ldexp(1.0, -t * (e - 1)));
-        if (bal) best.plan.kmax = km;  // Eq. 3 bound of the balanced digits
         best.kblock_words = kb;
         best.max_exact_words = exact;
         best.balanced = bal;

@@ -100,3 +100,93 @@ def panel_bounds(n_tiles: int, panels: int, j: int) -> Tuple[int, int]:
     base, extra = divmod(n_tiles, panels)
     t0 = j * base + min(j, extra)
     return t0, t0 + base + (1 if j < extra else 0)
+
+
+def shard_rows_aligned(m: int, world: int, rank: int, align: int = 128) -> Tuple[int, int]:
+    """Strong-scaling row shard of a fixed m: (row0, rows) of rank `rank`,
+    whole multiples of `align` rows (one 128-row block of the tiled CA_t per
+    block) except the last rank's tail; ranks past the end get 0 rows."""
+    if world < 1 or not 0 <= rank < world or align < 1:
+        raise ValueError("bad world/rank/align")
+    per_rank = -(-m // world)  # ceil(m / world)
+    per = -(-per_rank // align) * align
+    row0 = min(m, rank * per)
+    return row0, min(m, row0 + per) - row0
+
+
+def gather_slot(n_tiles: int, world: int, rank: int) -> Tuple[int, int, int]:
+    """Tile-column slot of `rank` in the all-gathered packed B: every rank
+    owns P = ceil(n_tiles/world) tile columns of CB_t (the last slots may be
+    short or empty; the gathered buffer holds world*P tile columns so that
+    every rank contributes the same number of words). Returns (t0, t1, P)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    per = -(-n_tiles // world)
+    t0 = min(n_tiles, rank * per)
+    return t0, min(n_tiles, t0 + per), per
+
+
+@dataclasses.dataclass
+class GatherOps:
+    """The device steps of the all-gather form (SURVEY.md §8e alternative).
+
+    pack_rows(a_shard) -> CA shard; pack_cols_slot(b, t0, t1, slot) packs
+    tile columns [t0, t1) of B into this rank's slot (a contiguous view of
+    the gathered buffer); contract(ca, cb, t0, t1) contracts this rank's rows
+    against tile columns [t0, t1) of the gathered CB into C."""
+
+    pack_rows: Callable
+    pack_cols_slot: Callable
+    contract: Callable
+
+
+def mul_common_allgather(a_shard, b, cb, ops: GatherOps, rank: int, world: int, n_tiles: int, group=None):
+    """C[rows of this rank] = A_shard x B mod p with the packed right operand
+    assembled by one all-gather: rank r packs only its own tile-column slot of
+    CB (compress_cols_forward is column-separable, gemm.hpp:122-140), the
+    slots are all-gathered in place over NCCL (every rank sends 1/world of
+    the packed words instead of rank 0 sending all of them), the CA shard is
+    packed while the gather is on the wire, the rank's own columns are
+    contracted first (they are local), and the rest once the gather has
+    landed. The words and C are those of mul_common_sharded.
+
+    ``cb`` is the flat gathered buffer of world * P tile columns; its slot j
+    is ``cb.view(world, -1)[j]``."""
+    import torch.distributed as dist
+
+    t0, t1, _ = gather_slot(n_tiles, world, rank)
+    slots = cb.view(world, -1)
+    ops.pack_cols_slot(b, t0, t1, slots[rank])
+    work = None
+    if world > 1:
+        work = _all_gather_slots(cb, slots, rank, group)
+    ca = ops.pack_rows(a_shard)
+    if t1 > t0:
+        ops.contract(ca, cb, t0, t1)
+    if work is not None:
+        work.wait()
+    if t1 < n_tiles:
+        ops.contract(ca, cb, t1, n_tiles)
+    if t0 > 0:
+        ops.contract(ca, cb, 0, t0)
+    return ca, cb
+
+
+class _Done:
+    def wait(self):
+        return None
+
+
+def _all_gather_slots(cb, slots, rank, group):
+    """In-place all-gather of the per-rank slots of ``cb`` (async). NCCL (and
+    gloo on CPU tensors) take the flat in-place form; a backend without it
+    (gloo on CUDA tensors, the one-GPU functional check) gets the list form."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl" or not cb.is_cuda:
+        return dist.all_gather_into_tensor(cb, slots[rank], group=group, async_op=True)
+    parts = [s.cpu() for s in slots]
+    dist.all_gather(parts, parts[rank].clone(), group=group)
+    for dst, src in zip(slots, parts):
+        dst.copy_(src)
+    return _Done()

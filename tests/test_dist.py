@@ -130,3 +130,85 @@ def _worker_panels(rank, world, port, p, m, k, n, panels):
 @pytest.mark.parametrize("p,m,k,n,panels", [(7, 70, 300, 50, 4), (3, 9, 512, 33, 3), (5, 16, 100, 7, 8)])
 def test_pipelined_broadcast_world2_gloo(p, m, k, n, panels):
     mp.spawn(_worker_panels, args=(2, _free_port(), p, m, k, n, panels), nprocs=2, join=True)
+
+
+def test_aligned_shards_and_slots_cover_exactly():
+    from paper_0803_1975_b200.dist import gather_slot, shard_rows_aligned
+
+    for m in (0, 1, 100, 512, 4096, 32768, 32769):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_rows_aligned(m, world, r) for r in range(world)]
+            assert sum(rows for _, rows in spans) == m
+            pos = 0
+            for row0, rows in spans:
+                assert row0 == pos and (rows % 128 == 0 or row0 + rows == m)
+                pos += rows
+    for nt in (1, 3, 32, 256, 257):
+        for world in (1, 2, 3, 8):
+            slots = [gather_slot(nt, world, r) for r in range(world)]
+            assert slots[0][0] == 0 and max(s[1] for s in slots) == nt
+            assert all(a[1] == b[0] or b[0] == b[1] for a, b in zip(slots, slots[1:]))
+            assert all(s[1] - s[0] <= s[2] for s in slots)
+    assert [shard_rows_aligned(32768, 8, r)[1] for r in range(8)] == [4096] * 8
+
+
+TILE = 4  # columns per "tile column" in the miniature layout
+
+
+def _worker_gather(rank, world, port, p, m, k, n):
+    """All-gather form (strong scaling): every rank packs only its own
+    tile-column slot of CB (kept column-major, TILE columns per tile, so a
+    slot is contiguous like the tiled CB_t), the slots are all-gathered in
+    place, and the rank contracts its own slot first."""
+    import oracle as O
+    from paper_0803_1975_b200.dist import GatherOps, gather_slot, mul_common_allgather, shard_rows_aligned
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = O.plan_compression(p, k)
+        K = -(-k // plan.e)
+        row0, rows = shard_rows_aligned(m, world, rank, align=8)
+        a_shard = O.random_residue_matrix(rows, k, p, 42, row0=row0)
+        b = O.random_residue_matrix(k, n, p, 43)  # each rank reads only its own slot's columns
+        nt = -(-n // TILE)
+        _, _, per = gather_slot(nt, world, rank)
+        cb = torch.zeros(world * per * TILE * K, dtype=torch.float64)
+        c = torch.full((rows, n), -1, dtype=torch.int32)
+        order = []
+
+        def pack_slot(bb, t0, t1, slot):
+            c0, c1 = t0 * TILE, min(n, t1 * TILE)
+            if c1 > c0:
+                words = O.compress_cols_forward(plan, np.ascontiguousarray(bb[:, c0:c1])).T.copy()  # cols x K
+                slot[:words.size] = torch.from_numpy(words.reshape(-1))
+
+        def contract(ca, cb_, t0, t1):
+            order.append((t0, t1))
+            c0, c1 = t0 * TILE, min(n, t1 * TILE)
+            cols = cb_[t0 * TILE * K:t0 * TILE * K + (c1 - c0) * K].numpy().reshape(c1 - c0, K)
+            acc = O.packed_common_product(plan, ca.numpy(), np.ascontiguousarray(cols.T), k)
+            c[:, c0:c1] = torch.from_numpy(((acc.astype(np.uint64) & np.uint64((1 << plan.t) - 1)) %
+                                            np.uint64(p)).astype(np.int32))
+
+        ops = GatherOps(pack_rows=lambda a: torch.from_numpy(O.compress_rows_reversed(plan, a)),
+                        pack_cols_slot=pack_slot, contract=contract)
+        mul_common_allgather(a_shard, b, cb, ops, rank, world, nt)
+        # every rank ends with the whole packed B, bit for bit
+        want_cb = O.compress_cols_forward(plan, O.random_residue_matrix(k, n, p, 43))
+        got = cb[:n * K].numpy().reshape(n, K).T
+        assert np.array_equal(np.ascontiguousarray(got).view(np.uint64), want_cb.view(np.uint64))
+        t0, t1, _ = gather_slot(nt, world, rank)
+        if t1 > t0:
+            assert order[0] == (t0, t1)  # own slot first
+        assert sorted(order) == sorted(set(order)) and sum(b - a for a, b in order) == nt
+        want_c = O.naive_gemm(p, a_shard, O.random_residue_matrix(k, n, p, 43))
+        assert np.array_equal(c.numpy().astype(np.uint32), want_c)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p,m,k,n", [(7, 70, 300, 50), (3, 9, 512, 33), (5, 16, 100, 7), (3, 5, 64, 3)])
+def test_allgather_world2_gloo(p, m, k, n):
+    mp.spawn(_worker_gather, args=(2, _free_port(), p, m, k, n), nprocs=2, join=True)

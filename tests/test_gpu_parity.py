@@ -110,7 +110,7 @@ def test_mul_common_gpu_plan_blocked(qg, orc, cuda, p, m, k, n):
     import torch
 
     gp = qg.plan_gpu(p, k)
-    assert gp.kblock_words * gp.plan.e <= gp.plan.kmax or gp.kblock_words * gp.plan.e >= k
+    assert gp.kblock_words * gp.plan.e <= gp.eq3_kmax() or gp.kblock_words * gp.plan.e >= k
     assert gp.kblock_words <= gp.max_exact_words
     a = orc.random_residue_matrix(m, k, p, 4242)
     b = orc.random_residue_matrix(k, n, p, 4243)

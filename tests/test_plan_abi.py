@@ -111,14 +111,19 @@ def test_gpu_planner_invariants(p, k):
     pl = gp.plan
     K = -(-k // pl.e)
     assert pl.t * pl.e < 53 or pl.e == 1
+    # plan.kmax keeps the reference's meaning (plan.hpp:113-115) even for
+    # balanced plans; the Eq. 3 bound the kernels enforce is eq3_kmax()
+    assert pl.kmax == ((1 << pl.t) - 1) // ((p - 1) ** 2)
+    kmax = gp.eq3_kmax()
+    assert kmax == (((1 << (pl.t - 1)) - 1) // ((p // 2) ** 2) if gp.balanced else pl.kmax)
     if gp.kblock_words < K:  # multi-block: Eq. 3 per block, Eq. G, stage-aligned
-        assert gp.kblock_words * pl.e <= pl.kmax
+        assert gp.kblock_words * pl.e <= kmax
         assert gp.kblock_words <= gp.max_exact_words
         assert gp.kblock_words % 4 == 0
         nblocks = -(-K // gp.kblock_words)
         assert nblocks * ((1 << pl.t) - 1) < (1 << 32)
     else:
-        assert k <= pl.kmax
+        assert k <= kmax
         assert K <= gp.max_exact_words
 
 

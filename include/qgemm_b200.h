@@ -169,6 +169,25 @@ int qg_mul_common_repacked(const qg_gpu_plan* gplan, const double* ca, const dou
                            size_t m, size_t n, size_t k, double* cc, int32_t* workspace,
                            void* stream);
 
+/* mul_common_repacked on the tiled layout: the contraction with
+ * ReduceAndCompress (pack.hpp:141-155) fused into its epilogue — C's rows
+ * leave as forward words of e residues under gplan->plan (t, e); no int32 C
+ * in HBM (p < 256 on the 128x128-tile kernel; otherwise through an int32
+ * workspace). cc: m x ceil(n/e) words (ldcc). */
+int qg_mul_common_repacked_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m,
+                                 size_t n, size_t k, double* cc, size_t ldcc, void* stream);
+/* mul_common_repacked(A, B) on device residues in one call (tiled packs into
+ * stream-ordered workspaces + qg_mul_common_repacked_tiled). */
+int qg_mul_common_repacked_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda, const void* b, size_t ldb,
+                                      qg_dtype dtype, size_t m, size_t k, size_t n, double* cc, size_t ldcc,
+                                      void* stream);
+/* mul_common_repacked(A, B, plan), gemm.hpp:275-280, on HOST data: cc gets
+ * m x ceil(n/e) words, bit-identical to compress_outer_cols(C, plan). */
+int qg_host_mul_common_repacked(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                                size_t n, double* cc);
+int qg_host_mul_common_repacked_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b, size_t m,
+                                    size_t k, size_t n, double* cc);
+
 /* ---- tiled packed layout (the B200 fast path for the dot-product variant).
  * The same words as compress_rows_reversed / compress_cols_forward, stored as
  * dense, zero-padded 128 x BK blocks so that one pipeline stage of the
@@ -279,6 +298,27 @@ int qg_mul_right(const qg_plan* plan, const double* a, size_t lda, const double*
 int qg_packed_right_product(const qg_plan* plan, const double* a, size_t lda,
                             const double* cbo, size_t m, size_t k, size_t n, double* cc,
                             void* stream);
+
+/* packed_left_product, gemm.hpp:340-364 (DoubleWord, reference layout):
+ * CA (compress_outer_rows words, ceil(m/e) x k, ldca) x B (k x n residues of
+ * `dtype`, ldb) -> cc (ceil(m/e) x n pre-REDQ words). qg_mul_left adds the
+ * REDQ of mul_left_compressed(ca, b), gemm.hpp:366-371. */
+int qg_packed_left_product(const qg_plan* plan, const double* ca, size_t ldca, const void* b, qg_dtype dtype,
+                           size_t ldb, size_t m, size_t k, size_t n, double* cc, void* stream);
+int qg_mul_left(const qg_plan* plan, const double* ca, size_t ldca, const void* b, qg_dtype dtype, size_t ldb,
+                size_t m, size_t k, size_t n, double* cc, void* stream);
+/* extract_all, pack.hpp:104-119, over `count` words: digits[i*e + s] = digit s
+ * of word i (unreduced); QG_DIGIT_OVERFLOW if a word is negative or >= Q^e. */
+int qg_extract_digits(const qg_plan* plan, const double* words, size_t count, uint64_t* digits, void* stream);
+int qg_extract_digits_u64(const qg_plan* plan, const uint64_t* words, size_t count, uint64_t* digits,
+                          void* stream);
+/* Device memory for callers without the CUDA headers (include/qgemm_b200.hpp):
+ * synchronous copies on the legacy default stream (the stream the entry
+ * points use when passed NULL). */
+int qg_device_alloc(size_t bytes, void** ptr);
+int qg_device_free(void* ptr);
+int qg_copy_to_device(void* dst, const void* src, size_t bytes);
+int qg_copy_to_host(void* dst, const void* src, size_t bytes);
 
 /* redq_in_place, gemm.hpp:313-316 / redq, pack.hpp:124-137. Words that do
  * not fit e digits make the call return QG_DIGIT_OVERFLOW (checked on the

@@ -234,6 +234,18 @@ def _load():
         "qg_host_mul_right_i64": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_mul_left_i64": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
         "qg_host_mul_full_i64": ([P(_FullPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_mul_common_repacked_tiled": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp, sz, vp], i32),
+        "qg_mul_common_repacked_compressed": ([P(_GpuPlan), vp, sz, vp, sz, i32, sz, sz, sz, vp, sz, vp], i32),
+        "qg_host_mul_common_repacked": ([P(_Plan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_host_mul_common_repacked_gpu": ([P(_GpuPlan), vp, vp, sz, sz, sz, vp], i32),
+        "qg_packed_left_product": ([P(_Plan), vp, sz, vp, i32, sz, sz, sz, sz, vp, vp], i32),
+        "qg_mul_left": ([P(_Plan), vp, sz, vp, i32, sz, sz, sz, sz, vp, vp], i32),
+        "qg_extract_digits": ([P(_Plan), vp, sz, vp, vp], i32),
+        "qg_extract_digits_u64": ([P(_Plan), vp, sz, vp, vp], i32),
+        "qg_device_alloc": ([sz, P(vp)], i32),
+        "qg_device_free": ([vp], i32),
+        "qg_copy_to_device": ([vp, vp, sz], i32),
+        "qg_copy_to_host": ([vp, vp, sz], i32),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),
@@ -692,11 +704,52 @@ def mul_common_tiled(a, b, plan: Union[CompressionPlan, GpuPlan]):
 
 
 def mul_common_repacked(a, b, plan: Union[CompressionPlan, GpuPlan]) -> CompressedMatrix:
-    """mul_common_repacked, gemm.hpp:275-280 (ReduceAndCompress of C's rows)."""
+    """mul_common_repacked, gemm.hpp:275-280: C reduced and its rows re-packed
+    forward in groups of e (ReduceAndCompress, pack.hpp:141-155) under the
+    plan's (t, e), fused into the contraction's epilogue
+    (qg_mul_common_repacked_compressed: no int32 C in HBM). Under a
+    CompressionPlan the words are the reference's bit for bit."""
     torch = _torch()
-    c = mul_common_compressed(a, b, plan)
+    _require_cuda(a, b)
+    if a.shape[1] != b.shape[0]:  # check_inner_dims, gemm.hpp:22-27
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape[0]}x{a.shape[1]} times {b.shape[0]}x{b.shape[1]}")
+    m, k = a.shape
+    n = b.shape[1]
+    if not isinstance(plan, GpuPlan) and k > plan.kmax:  # compress_rows_reversed's check
+        raise PlanMismatch(f"common dimension {k} exceeds kmax={plan.kmax}")
+    gp = _as_gpu_plan(plan, k)
+    base = gp.plan
+    if b.dtype != a.dtype:
+        b = b.to(a.dtype)
+    a, b = a.contiguous(), b.contiguous()
+    H = (n + base.e - 1) // base.e
+    out = torch.empty((m, H), dtype=torch.float64, device=a.device)
+    g = gp._c()
+    _check(lib.qg_mul_common_repacked_compressed(ctypes.byref(g), _ptr(a), k, _ptr(b), n, _dtype_code(a), m, k, n,
+                                                 _ptr(out), H, _stream()))
+    return CompressedMatrix(m, n, m, H, PackOrientation(PackDirection.Forward, PackAxis.Column, base.e), base, out)
+
+
+def mul_common_repacked_host(a, b, plan: Union[CompressionPlan, GpuPlan], out=None) -> np.ndarray:
+    """mul_common_repacked on host ResidueMatrix data (uint32): m x ceil(n/e)
+    float64 words (qg_host_mul_common_repacked[_gpu], pipelined)."""
+    a, b = _host_u32(a), _host_u32(b)
+    if a.shape[1] != b.shape[0]:
+        raise DimensionMismatch(f"inner dimensions disagree: {a.shape} times {b.shape}")
+    m, k = a.shape
+    n = b.shape[1]
     base = plan.plan if isinstance(plan, GpuPlan) else plan
-    return compress_outer_cols(c, base)
+    cc = np.empty((m, (n + base.e - 1) // base.e), dtype=np.float64) if out is None else out
+    vp = ctypes.c_void_p
+    if isinstance(plan, GpuPlan):
+        g = plan._c()
+        _check(lib.qg_host_mul_common_repacked_gpu(ctypes.byref(g), a.ctypes.data_as(vp), b.ctypes.data_as(vp), m, k,
+                                                   n, cc.ctypes.data_as(vp)))
+    else:
+        pl = plan._c()
+        _check(lib.qg_host_mul_common_repacked(ctypes.byref(pl), a.ctypes.data_as(vp), b.ctypes.data_as(vp), m, k, n,
+                                               cc.ctypes.data_as(vp)))
+    return cc
 
 
 def packed_right_product(a, cb: CompressedMatrix) -> CompressedMatrix:

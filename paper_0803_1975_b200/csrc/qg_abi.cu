@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <memory>
 #include <vector>
 
 #include "../../include/qgemm_b200.h"
@@ -98,7 +100,11 @@ struct DeviceFlag {
   int* ptr = nullptr;
   cudaStream_t s;
   explicit DeviceFlag(cudaStream_t st) : s(st) {
-    static thread_local int* flag = nullptr;
+    // keyed by device: a thread may call the library on several GPUs
+    static thread_local std::map<int, int*> flags;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    int*& flag = flags[dev];
     if (!flag && cudaMalloc(&flag, sizeof(int)) != cudaSuccess) flag = nullptr;
     ptr = flag;
     if (ptr && cudaMemsetAsync(ptr, 0, sizeof(int), s) != cudaSuccess) ptr = nullptr;
@@ -217,8 +223,10 @@ int qg_tiled_stage_words(const qg_gpu_plan* gplan, uint64_t k, uint32_t* bk) {
   if (!gplan || !bk) return QG_INVALID_ARGUMENT;
   int st = check_plan(&gplan->plan);
   if (st) return st;
+  const uint64_t K = ceil_div(k, gplan->plan.e), kb = gplan->kblock_words, kmax = gpu_kmax(gplan);
+  if (kb < K && kb * (uint64_t)gplan->plan.e > kmax) return QG_PLAN_MISMATCH;  // Eq. 3 first, as the contraction
   int b = 0, kbs = 0;
-  if ((st = tiled_geometry(gplan, ceil_div(k, gplan->plan.e), &b, &kbs))) return st;
+  if ((st = tiled_geometry(gplan, K, &b, &kbs))) return st;
   *bk = (uint32_t)b;
   return QG_OK;
 }
@@ -611,6 +619,90 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));
 }
 
+// mul_common_repacked, gemm.hpp:275-280, on the tiled layout: C's rows leave
+// the contraction as forward-packed words of e adjacent residues
+// (ReduceAndCompress, pack.hpp:141-155, under gplan->plan's t and e). The
+// 128x128-tile kernel does it in its epilogue (EPI_REPACK: no int32 C in
+// HBM); products that take the small cluster kernel, or p >= 256, go through
+// an int32 workspace and the outer-cols pack instead.
+int qg_mul_common_repacked_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m,
+                                 size_t n, size_t k, double* cc, size_t ldcc, void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if (pl.t * pl.e > 53) return QG_PLAN_MISMATCH;  // output words must be exact doubles
+  const size_t H = ceil_div(n, (size_t)pl.e);
+  if (ldcc < H) return QG_INVALID_ARGUMENT;
+  const size_t K = ceil_div(k, pl.e);
+  const uint64_t kb = gplan->kblock_words;
+  if (kb == 0) return QG_INVALID_ARGUMENT;
+  const uint64_t kmax = gpu_kmax(gplan);
+  if (kb < K && kb * (uint64_t)pl.e > kmax) return QG_PLAN_MISMATCH;  // Eq. 3 per block
+  if (kb >= K && k > kmax) return QG_PLAN_MISMATCH;
+  if (m == 0 || n == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  if (K == 0) return cuda_status(cudaMemset2DAsync(cc, ldcc * 8, 0, H * 8, m, s));
+  int bk = 0, kbs = 0;
+  if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
+  if (pl.p > 255 || use_small_path(m, n)) {
+    DevBuf ws(s);
+    QG_TRY(ws.alloc(m * n * sizeof(int32_t)));
+    if ((st = qg_mul_common_tiled(gplan, ca_t, cb_t, m, n, k, (int32_t*)ws.p, n, stream))) return st;
+    return cuda_status(qgk::launch_pack(qgk::PACK_OUTER_COLS, ws.p, QG_I32, m, n, n, pl.t, pl.e, cc, ldcc, 0, 0, s));
+  }
+  qgk::GemmArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.a = ca_t;
+  a.b = cb_t;
+  if (!dims_ok(m, n, K) || !dims_ok(ldcc, 1)) return QG_INVALID_ARGUMENT;
+  a.M = (int)m;
+  a.N = (int)n;
+  a.K = (int)K;
+  a.kb_stages = kbs;
+  a.balanced = gplan->balanced != 0;
+  a.anchor = a.balanced ? std::ldexp(1.5, pl.t * pl.d + 52) + std::ldexp(1.0, pl.t * pl.d + pl.t - 1)
+                        : std::ldexp(1.0, pl.t * pl.d + 52);
+  a.qmask = (uint32_t)((1ull << pl.t) - 1);
+  a.p = pl.p;
+  a.t = pl.t;
+  a.e = pl.e;
+  a.cc = cc;
+  a.ldcc = ldcc;
+  const uint64_t nblocks = (kbs ? ceil_div(K, (size_t)kbs * bk) : 1) + 1;
+  if ((unsigned __int128)nblocks * a.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+  // words cut by a 32-column warp segment are summed atomically from zero
+  if (32 % pl.e) QG_TRY(cudaMemset2DAsync(cc, ldcc * 8, 0, H * 8, m, s));
+  return cuda_status(qgk::launch_dot_tiled_repack(a, bk, s, &g_last_kernel));
+}
+
+// mul_common_repacked(A, B, plan) on device residues in one call: tiled packs
+// into stream-ordered workspaces, then qg_mul_common_repacked_tiled.
+int qg_mul_common_repacked_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda, const void* b, size_t ldb,
+                                      qg_dtype dtype, size_t m, size_t k, size_t n, double* cc, size_t ldcc,
+                                      void* stream) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (lda < k || ldb < n || ldcc < ceil_div(n, (size_t)pl.e)) return QG_INVALID_ARGUMENT;
+  if (pl.t * pl.e > 53 || pl.t > 31) return QG_PLAN_MISMATCH;
+  const size_t K = ceil_div(k, (size_t)pl.e);
+  if (m == 0 || n == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  if (K == 0) return cuda_status(cudaMemset2DAsync(cc, ldcc * 8, 0, ceil_div(n, (size_t)pl.e) * 8, m, s));
+  keep_pool_mapped();
+  int bk = 0, kbs = 0;
+  if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
+  DevBuf ca(s), cb(s);
+  QG_TRY(ca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
+  QG_TRY(cb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
+  if ((st = qg_pack_a_tiled(gplan, bk, a, dtype, m, k, lda, (double*)ca.p, stream))) return st;
+  if ((st = qg_pack_b_tiled(gplan, bk, b, dtype, k, n, ldb, (double*)cb.p, stream))) return st;
+  return qg_mul_common_repacked_tiled(gplan, (const double*)ca.p, (const double*)cb.p, m, n, k, cc, ldcc, stream);
+}
+
 int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda, const void* b, size_t ldb,
                              qg_dtype dtype, size_t m, size_t k, size_t n, int32_t* c, size_t ldc, void* stream) {
   if (!gplan) return QG_INVALID_ARGUMENT;
@@ -843,6 +935,104 @@ int qg_packed_right_product(const qg_plan* plan, const double* a, size_t lda, co
   return right_common(plan, a, lda, cbo, m, k, n, cc, 0, stream);
 }
 
+// packed_left_product / mul_left_compressed (DoubleWord, reference layout),
+// gemm.hpp:340-371: CC (ceil(m/e) x n words) = CA (compress_outer_rows words,
+// ceil(m/e) x k, ldca) x B (k x n residues). Both this and the right product
+// are row-major word matrix x row-major word matrix with exact sums < Q^e, so
+// the right variant's DMMA contraction runs it with the operands' roles
+// swapped; residues that are not float64 are widened on the device first
+// (an e = 1 forward pack is the identity on values).
+static int left_common(const qg_plan* plan, const double* ca, size_t ldca, const void* b, qg_dtype dtype,
+                       size_t ldb, size_t m, size_t k, size_t n, double* cc, int redq, void* stream) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if ((st = check_dtype(dtype))) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;          // gemm.hpp:349 check_common_dim
+  if (plan->t * plan->e > 53) return QG_PLAN_MISMATCH;  // sums must stay exact
+  if (ldca < k || ldb < n) return QG_INVALID_ARGUMENT;
+  const size_t G = ceil_div(m, (size_t)plan->e);
+  if (G == 0 || n == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  if (k == 0) return cuda_status(cudaMemsetAsync(cc, 0, G * n * sizeof(double), s));
+  DevBuf wide(s);
+  const double* bd = static_cast<const double*>(b);
+  size_t ldbd = ldb;
+  if (dtype != QG_F64) {
+    QG_TRY(wide.alloc(k * n * sizeof(double)));
+    QG_TRY(qgk::launch_pack(qgk::PACK_OUTER_COLS, b, dtype, k, n, ldb, 1, 1, (double*)wide.p, n, 0, 0, s));
+    bd = (const double*)wide.p;
+    ldbd = n;
+  }
+  qgk::GemmArgs r;
+  std::memset(&r, 0, sizeof r);
+  r.a = ca;
+  r.lda = ldca;
+  r.b = bd;
+  r.ldb = ldbd;
+  if (!dims_ok(G, n, k)) return QG_INVALID_ARGUMENT;
+  r.M = (int)G;
+  r.N = (int)n;
+  r.K = (int)k;
+  r.t = plan->t;
+  r.e = plan->e;
+  r.p = plan->p;
+  r.cc = cc;
+  r.ldcc = n;
+  return cuda_status(qgk::launch_right_dmma(r, redq != 0, s, &g_last_kernel));
+}
+
+int qg_packed_left_product(const qg_plan* plan, const double* ca, size_t ldca, const void* b, qg_dtype dtype,
+                           size_t ldb, size_t m, size_t k, size_t n, double* cc, void* stream) {
+  return left_common(plan, ca, ldca, b, dtype, ldb, m, k, n, cc, 0, stream);
+}
+
+int qg_mul_left(const qg_plan* plan, const double* ca, size_t ldca, const void* b, qg_dtype dtype, size_t ldb,
+                size_t m, size_t k, size_t n, double* cc, void* stream) {
+  return left_common(plan, ca, ldca, b, dtype, ldb, m, k, n, cc, 1, stream);
+}
+
+static int extract_digits(const qg_plan* plan, const void* words, bool u64, size_t count, uint64_t* digits,
+                          void* stream) {
+  if (!plan) return QG_INVALID_ARGUMENT;
+  if (plan->p < 2 || !qg::is_prime(plan->p)) return QG_INVALID_MODULUS;
+  if (plan->t < 1 || plan->e < 1 || plan->t * plan->e > (u64 ? 64 : 53)) return QG_PLAN_MISMATCH;
+  if (count == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  DeviceFlag flag(s);
+  if (!flag.ptr) return QG_CUDA_ERROR;
+  int st = cuda_status(qgk::launch_extract_digits(words, u64, count, plan->t, plan->e, digits, flag.ptr, s));
+  if (st) return st;
+  int over = 0;
+  if ((st = flag.read(&over))) return st;
+  return over ? QG_DIGIT_OVERFLOW : QG_OK;
+}
+
+int qg_extract_digits(const qg_plan* plan, const double* words, size_t count, uint64_t* digits, void* stream) {
+  return extract_digits(plan, words, false, count, digits, stream);
+}
+
+int qg_extract_digits_u64(const qg_plan* plan, const uint64_t* words, size_t count, uint64_t* digits,
+                          void* stream) {
+  return extract_digits(plan, words, true, count, digits, stream);
+}
+
+// Device memory for callers without the CUDA runtime headers (the C++
+// drop-in): synchronous, on the legacy default stream that the entry points
+// run on when passed a NULL stream.
+int qg_device_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return QG_INVALID_ARGUMENT;
+  *ptr = nullptr;
+  if (bytes == 0) return QG_OK;
+  return cuda_status(cudaMalloc(ptr, bytes));
+}
+int qg_device_free(void* ptr) { return ptr ? cuda_status(cudaFree(ptr)) : QG_OK; }
+int qg_copy_to_device(void* dst, const void* src, size_t bytes) {
+  return bytes ? cuda_status(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)) : QG_OK;
+}
+int qg_copy_to_host(void* dst, const void* src, size_t bytes) {
+  return bytes ? cuda_status(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)) : QG_OK;
+}
+
 int qg_redq(const qg_plan* plan, double* words, size_t count, void* stream) {
   int st = check_plan(plan);
   if (st) return st;
@@ -897,14 +1087,17 @@ struct PhaseScope {
   // host's enqueue loop of the pipelined path (measured +0.36 ms on config 2)
   static cudaEvent_t* pool() {
     if (!g_phase_timing.load(std::memory_order_relaxed)) return nullptr;
-    static thread_local cudaEvent_t ev[2 * kPairs] = {};
-    static thread_local bool made = false;
-    if (!made) {
-      made = true;
+    // events belong to a device: one pool per (thread, device)
+    static thread_local std::map<int, std::vector<cudaEvent_t>> pools;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::vector<cudaEvent_t>& ev = pools[dev];
+    if (ev.empty()) {
+      ev.assign(2 * kPairs, nullptr);
       for (auto& e : ev)
         if (cudaEventCreate(&e) != cudaSuccess) e = nullptr;
     }
-    return ev;
+    return ev.data();
   }
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   cudaEvent_t* ev = pool();
@@ -953,6 +1146,7 @@ struct HostPipe {
     }
     return pool[i];
   }
+  cudaEvent_t join[kComp + 1] = {};  // PipeJoin: one per compute stream + out
   bool ok = false;
   HostPipe() {
     ok = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess &&
@@ -963,6 +1157,8 @@ struct HostPipe {
          cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess;
     comps[0] = comp;
     for (int i = 1; ok && i < kComp; ++i) ok = cudaStreamCreateWithFlags(&comps[i], cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; ok && i <= kComp; ++i)
+      ok = cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; ok && i < kMaxChunks; ++i)
       ok = cudaEventCreateWithFlags(&a_ready[i], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&c_ready[i], cudaEventDisableTiming) == cudaSuccess;
@@ -982,10 +1178,35 @@ struct HostPipe {
 // chunk maps to whole 128-row blocks of the packed layout) while the earlier
 // chunks are packed and contracted; each chunk's output streams back on its
 // own stream, so both PCIe directions overlap the contraction.
+// One pipeline (streams, events) per host thread AND device: its streams and
+// events belong to the device that was current when it was made, so a thread
+// that moves to another GPU gets that GPU's own set.
 static HostPipe& host_pipe() {
-  static thread_local HostPipe hp;
-  return hp;
+  static thread_local std::map<int, std::unique_ptr<HostPipe>> pipes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::unique_ptr<HostPipe>& hp = pipes[dev];
+  if (!hp) hp.reset(new HostPipe());
+  return *hp;
 }
+
+// Joins every stream of the pipeline into hp.in when a pipelined call
+// returns, on success and on every early error return alike: the call's
+// buffers are freed stream-ordered on hp.in (DevBuf), so the frees then wait
+// for every pack, contraction and copy already queued on the compute streams
+// and on hp.out. Declare it after the call's DevBufs (destroyed before them).
+struct PipeJoin {
+  HostPipe& hp;
+  explicit PipeJoin(HostPipe& h) : hp(h) {}
+  PipeJoin(const PipeJoin&) = delete;
+  PipeJoin& operator=(const PipeJoin&) = delete;
+  ~PipeJoin() {
+    for (int i = 0; i <= HostPipe::kComp; ++i) {
+      cudaStream_t st = i < HostPipe::kComp ? hp.comps[i] : hp.out;
+      if (hp.join[i] && st && cudaEventRecord(hp.join[i], st) == cudaSuccess) cudaStreamWaitEvent(hp.in, hp.join[i], 0);
+    }
+  }
+};
 
 struct ChunkOut {
   const void* src = nullptr;
@@ -1018,6 +1239,7 @@ static int host_pipeline(size_t m, size_t k, size_t n, size_t align, size_t col_
   int ncomp = chunk_tiles * 4 >= (size_t)sms * 3 ? 1 : (int)ceil_div((size_t)sms, chunk_tiles ? chunk_tiles : 1);
   if (ncomp > HostPipe::kComp) ncomp = HostPipe::kComp;
   DevBuf da(hp.in), db(hp.in);
+  PipeJoin join(hp);  // after the buffers: joins the streams before they are freed
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
   if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
@@ -1113,6 +1335,7 @@ static int host_pipeline2d(
     *cols = (c1 < n ? c1 : n) - (*c0 < n ? *c0 : n);
   };
   DevBuf da(hp.in), db(hp.in);
+  PipeJoin join(hp);  // after the buffers: joins the streams before they are freed
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));  // panel j: k x cols_j contiguous at column offset c0_j * k
   size_t ev = 0;
@@ -1280,6 +1503,87 @@ static int host_common(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t*
   return QG_OK;
 }
 
+// mul_common_repacked on host data (gemm.hpp:275-280): the 1-D host
+// pipeline of host_common with the repacking contraction per row chunk, each
+// chunk's CC words streamed back while later chunks run. Plans the tiled
+// kernels cannot run exactly take the reference-layout path (two passes).
+static int host_common_repacked(const qg_gpu_plan* gp, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                                size_t n, double* cc) {
+  const qg_plan& pl = gp->plan;
+  const size_t K = ceil_div(k, pl.e), H = ceil_div(n, (size_t)pl.e);
+  if (m * H == 0) return QG_OK;
+  int bk = 0, kbs = 0;
+  const int geo = K > 0 ? tiled_geometry(gp, K, &bk, &kbs) : QG_OK;
+  if (geo != QG_OK && gp->balanced) return geo;
+  if (geo != QG_OK) {
+    cudaStream_t s = nullptr;
+    DevBuf da(s), db(s), dca(s), dcb(s), dcc(s);
+    QG_TRY(da.alloc(m * k * 4));
+    QG_TRY(db.alloc(k * n * 4));
+    QG_TRY(dca.alloc(m * K * 8));
+    QG_TRY(dcb.alloc(K * n * 8));
+    QG_TRY(dcc.alloc(m * H * 8));
+    QG_TRY(cudaMemcpyAsync(da.p, a, m * k * 4, cudaMemcpyHostToDevice, s));
+    QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, s));
+    QG_TRY(qgk::launch_pack(qgk::PACK_ROWS_REVERSED, da.p, QG_U32, m, k, k, pl.t, pl.e, (double*)dca.p, K, 0, 0, s));
+    QG_TRY(qgk::launch_pack(qgk::PACK_COLS_FORWARD, db.p, QG_U32, k, n, n, pl.t, pl.e, (double*)dcb.p, n, 0, 0, s));
+    int st = qg_mul_common_repacked(gp, (const double*)dca.p, (const double*)dcb.p, m, n, k, (double*)dcc.p, nullptr, s);
+    if (st) return st;
+    QG_TRY(cudaMemcpyAsync(cc, dcc.p, m * H * 8, cudaMemcpyDeviceToHost, s));
+    return cuda_status(cudaStreamSynchronize(s));
+  }
+  if (K == 0) {
+    std::memset(cc, 0, m * H * 8);
+    return QG_OK;
+  }
+  const size_t Kt = ceil_div(K, (size_t)bk);
+  cudaStream_t s0 = host_pipe().in;
+  DevBuf dca(s0), dcb(s0), dcc(s0);
+  QG_TRY(dcc.alloc(m * H * 8));
+  QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
+  QG_TRY(dcb.alloc(qg_tiled_words(n, k, pl.e, bk) * 8));
+  return host_pipeline(
+      m, k, n, 128, ceil_div(n, (size_t)128), a, b,
+      [&](const uint32_t* db, cudaStream_t s2) {
+        return cuda_status(qgk::launch_pack_tiled(true, db, QG_U32, k, n, n, pl.t, pl.e, bk, (double*)dcb.p, s2, pl.p,
+                                                  gp->balanced != 0));
+      },
+      [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s2, PhaseScope& ps, ChunkOut* out) {
+        double* ca_chunk = (double*)dca.p + (r0 / 128) * Kt * 128 * bk;
+        int st2 = cuda_status(qgk::launch_pack_tiled(false, da, QG_U32, rows, k, k, pl.t, pl.e, bk, ca_chunk, s2, pl.p,
+                                                     gp->balanced != 0));
+        if (st2) return st2;
+        ps.begin(s2);
+        if ((st2 = qg_mul_common_repacked_tiled(gp, ca_chunk, (const double*)dcb.p, rows, n, k,
+                                                (double*)dcc.p + r0 * H, H, s2)))
+          return st2;
+        ps.end(s2);
+        out->src = (const double*)dcc.p + r0 * H;
+        out->dst = cc + r0 * H;
+        out->bytes = rows * H * 8;
+        return (int)QG_OK;
+      });
+}
+
+int qg_host_mul_common_repacked(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m, size_t k,
+                                size_t n, double* cc) {
+  int st = check_plan(plan);
+  if (st) return st;
+  if (k > plan->kmax) return QG_PLAN_MISMATCH;  // compress_rows_reversed's check, gemm.hpp:106
+  qg_gpu_plan gp;
+  if ((st = qg_gpu_plan_from(plan, k, &gp))) return st;
+  return host_common_repacked(&gp, a, b, m, k, n, cc);
+}
+
+int qg_host_mul_common_repacked_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const uint32_t* b, size_t m,
+                                    size_t k, size_t n, double* cc) {
+  if (!gplan) return QG_INVALID_ARGUMENT;
+  int st = check_plan(&gplan->plan);
+  if (st) return st;
+  if (gplan->plan.t * gplan->plan.e > 53 || gplan->plan.t > 31) return QG_PLAN_MISMATCH;
+  return host_common_repacked(gplan, a, b, m, k, n, cc);
+}
+
 int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,
                        size_t k, size_t n, uint32_t* c) {
   int st = check_plan(plan);
@@ -1430,6 +1734,7 @@ static int host_redq_ksplit(
   }
   cudaStream_t s0 = hp.in;
   DevBuf da(s0), db(s0), dat(s0), dbt(s0), dcc(s0);
+  PipeJoin join(hp);  // after the buffers: joins the streams before they are freed
   QG_TRY(da.alloc(m * k * 4));
   QG_TRY(db.alloc(k * n * 4));
   QG_TRY(dat.alloc(2 * wa * 8));  // ping-pong: part p packs while part p-1 contracts

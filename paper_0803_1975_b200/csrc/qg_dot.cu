@@ -57,11 +57,11 @@ struct Geo {
 // Tiled-layout geometry (k_gemm_tiled): a stage is one dense 128 x BK block
 // of A and one of B^T, each a single contiguous chunk in HBM. Fragment loads
 // are conflict-free when BK = 4 or 12 (mod 16); BK in {4, 12, 20, 28, 36}.
-template <int BK>
+template <int BK, int RESERVE = 0>
 struct GeoT {
   static constexpr int A_TILE = BM * BK;
   static constexpr int STAGE = 2 * BM * BK;  // doubles
-  static constexpr int BUDGET = 232448 - 1024;
+  static constexpr int BUDGET = 232448 - 1024 - RESERVE;  // RESERVE: epilogue staging (EPI_REPACK)
   static constexpr int STAGES_RAW = BUDGET / (STAGE * 8);
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
   static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
@@ -160,7 +160,40 @@ __device__ __forceinline__ uint32_t block_digit_t(double acc, double anchor, uin
 
 // EPI_DIGIT: K4 epilogue (int32 C = digit sums mod p). EPI_REDQ: K5 fused
 // REDQ of exact packed sums (pack.hpp:124-137). EPI_RAW: plain words.
-enum { EPI_DIGIT = 0, EPI_REDQ = 1, EPI_RAW = 2 };
+// EPI_REPACK: K4 with ReduceAndCompress fused (pack.hpp:141-155): the residues
+// of C go through a per-warp shared-memory tile and leave as forward-packed
+// words of e adjacent columns (mul_common_repacked, gemm.hpp:275-280).
+enum { EPI_DIGIT = 0, EPI_REDQ = 1, EPI_RAW = 2, EPI_REPACK = 3 };
+// EPI_REPACK staging: one byte per residue (p < 256), one 64 x 32 tile per warp
+constexpr int REPACK_SMEM = BM * BN;
+template <int EPI>
+constexpr int epi_reserve() { return EPI == EPI_REPACK ? REPACK_SMEM : 0; }
+
+// ReduceAndCompress of one warp's 64 x 32 residue tile (st, row-major, WN
+// bytes per row; rows r0.., columns c0..): word h of a row packs columns
+// h e .. h e + e - 1 forward in base Q = 2^t (compress_forward, pack.hpp:47-54).
+// Words whose columns all lie in this segment are stored; a word cut by the
+// segment's edge gets its part added atomically (the parts occupy disjoint
+// bits, so the float64 sums are exact integers < 2^53 in any order; the
+// launcher zeroes CC first whenever a word can straddle segments).
+__device__ __forceinline__ void repack_segment(const uint8_t* st, const GemmArgs& a, int r0, int c0, int lane) {
+  const int N = a.N, e = a.e, tb = a.t;
+  if (c0 >= N) return;
+  const int cend = min(c0 + WN, N);
+  const int h_lo = c0 / e, h_hi = (cend - 1) / e, W = h_hi - h_lo + 1;
+  const int rows = min(WM, a.M - r0);
+  for (int idx = lane; idx < rows * W; idx += 32) {
+    const int row = idx / W, hw = h_lo + (idx - row * W);
+    const int wc0 = hw * e;
+    const int lo = max(wc0, c0), hi = min(wc0 + e, cend);
+    uint64_t word = 0;
+    for (int c = lo; c < hi; ++c) word |= (uint64_t)st[row * WN + (c - c0)] << (tb * (c - wc0));
+    double* dst = a.cc + (size_t)(r0 + row) * a.ldcc + hw;
+    const double wd = __ull2double_rn(word);  // exact: word < Q^e <= 2^53
+    if (wc0 >= c0 && min(wc0 + e, N) <= cend) *dst = wd;
+    else atomicAdd(dst, wd);
+  }
+}
 
 // redq, pack.hpp:124-137, on an exact integer-valued word w < 2^53: every
 // base-Q digit replaced by itself mod p.
@@ -480,9 +513,10 @@ struct SplitFlush {
 // into the first k-step of the next stage.
 template <int BK, int EPI, bool MULTI, int MID, bool TILED, bool PACK = false, bool SPLIT = false, bool BAL = false>
 __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint64_t* full, uint64_t* empty,
-                                        int tiles_m, int tiles_n, int my_tiles, int ktiles, bool nomem) {
+                                        int tiles_m, int tiles_n, int my_tiles, int ktiles, bool nomem,
+                                        uint8_t* repack = nullptr) {
   using G = Geo<BK>;
-  using GT = GeoT<BK>;
+  using GT = GeoT<BK, epi_reserve<EPI>()>;
   constexpr int S = TILED ? GT::STAGES : G::STAGES;
   constexpr int STAGE = TILED ? GT::STAGE : G::STAGE;
   constexpr int A_TILE = TILED ? GT::A_TILE : G::A_TILE;
@@ -645,6 +679,27 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
             for (int h = 0; h < 2; ++h) acc[mi][ni][h] = redq_word(acc[mi][ni][h], args.t, args.e, modp);
       }
     }
+    if (EPI == EPI_REPACK) {  // residues -> this warp's byte tile -> packed words
+      uint8_t* st = repack + warp * (WM * WN);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          uint32_t r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t x = block_digit_t<BAL>(acc[mi][ni][h], args.anchor, args.qmask) + ds.get(mi, ni, h) +
+                               (BAL ? args.corr : 0u);
+            const uint32_t r0 = x - __umulhi(x, modp.magic) * modp.p;
+            r[h] = min(r0, r0 - modp.p);
+          }
+          *reinterpret_cast<uint16_t*>(st + (mi * 8 + g) * WN + ni * 8 + 2 * t) = (uint16_t)(r[0] | (r[1] << 8));
+          acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
+      __syncwarp();
+      repack_segment(st, args, m0 + warp_m * WM, n0 + warp_n * WN, lane);
+      __syncwarp();  // the next tile overwrites the staging tile
+    }
     // interior tiles without accumulation (nearly all of them): no per-element
     // bounds or accumulate checks, one int2 store per accumulator pair
     const bool fast = EPI == EPI_DIGIT && !args.accumulate && m0 + BM <= M && n0 + BN <= N;
@@ -669,7 +724,7 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
       }
     }
 #pragma unroll
-    for (int mi = 0; mi < MI && !(EPI == EPI_DIGIT && fast); ++mi) {
+    for (int mi = 0; mi < MI && !(EPI == EPI_DIGIT && fast) && EPI != EPI_REPACK; ++mi) {
       const int row = m0 + warp_m * WM + mi * 8 + g;
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {
@@ -792,7 +847,7 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_bulk(GemmArgs args, int ti
 // left in the kernel. Same warpgroup split and consumers as k_gemm_bulk.
 template <int BK, int EPI, bool MULTI, int FLUSH, bool BAL>
 __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int tiles_m, int tiles_n) {
-  using GT = GeoT<BK>;
+  using GT = GeoT<BK, epi_reserve<EPI>()>;
   constexpr int S = GT::STAGES;
   constexpr int NWARPS = NT / 32;
   constexpr uint32_t CHUNK = BM * BK * 8;  // bytes of one operand block
@@ -837,19 +892,20 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int t
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  uint8_t* repack = reinterpret_cast<uint8_t*>(empty + S);  // EPI_REPACK staging (after the barriers)
   // FLUSH (multi-block): 0 = at stage ends; for kb_stages == 1 also
   // 1 = staggered (warps 4..7 cut mid-stage; two inlined consumer bodies, so
   // instantiated separately) and 2 = fused into the next stage's first k-step.
   if (FLUSH == 3)  // split phases: odd accumulator rows flush mid-stage, even rows at stage ends
-    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, false, true, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, false, true, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
   else if (FLUSH == 2)  // fused flush with packed digit sums (t <= 16)
-    consume<BK, EPI, MULTI, -1, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, -1, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
   else if (FLUSH == 1 && warp >= 4)
-    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
   else if (FLUSH == 1)
-    consume<BK, EPI, MULTI, 0, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, 0, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
   else
-    consume<BK, EPI, MULTI, 0, true, false, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem);
+    consume<BK, EPI, MULTI, 0, true, false, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
 }
 
 // Reference-semantics contraction (DoubleWord::high_part, word.hpp:28-30):
@@ -1015,9 +1071,9 @@ static cudaError_t launch_digit_bulk(const GemmArgs& a, int bk, cudaStream_t s) 
 static int num_sms();
 template <int BK, int EPI, bool MULTI, int FLUSH, bool BAL>
 static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
-  using GT = GeoT<BK>;
+  using GT = GeoT<BK, epi_reserve<EPI>()>;
   auto k = k_gemm_tiled<BK, EPI, MULTI, FLUSH, BAL>;
-  const size_t smem = GT::SMEM + 2 * GT::STAGES * sizeof(uint64_t);
+  const size_t smem = GT::SMEM + 2 * GT::STAGES * sizeof(uint64_t) + epi_reserve<EPI>();
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err) return err;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
@@ -1079,6 +1135,40 @@ cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const ch
     case 20: return launch_tiled_b<20>(a, flush, s);
     case 12: return launch_tiled_b<12>(a, flush, s);
     case 4: return launch_tiled_b<4>(a, flush, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// K4 with the fused ReduceAndCompress epilogue (EPI_REPACK): CC = m x ceil(n/e)
+// words in a.cc (a.ldcc), a.t / a.e the packing of the output rows.
+template <int BK, bool BAL>
+static cudaError_t launch_tiled_repack_bk(const GemmArgs& a, int flush, cudaStream_t s) {
+  if (a.kb_stages == 0) return launch_tiled_one<BK, EPI_REPACK, false, 0, BAL>(a, s);
+  if (a.kb_stages == 1 && flush == 3 && BK >= 8) return launch_tiled_one<BK, EPI_REPACK, true, (BK >= 8 ? 3 : 0), BAL>(a, s);
+  return launch_tiled_one<BK, EPI_REPACK, true, 0, BAL>(a, s);
+}
+
+template <int BK>
+static cudaError_t launch_tiled_repack_b(const GemmArgs& a, int flush, cudaStream_t s) {
+  return a.balanced ? launch_tiled_repack_bk<BK, true>(a, flush, s) : launch_tiled_repack_bk<BK, false>(a, flush, s);
+}
+
+cudaError_t launch_dot_tiled_repack(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
+  if (a.M == 0 || a.N == 0) return cudaSuccess;
+  static thread_local char name[80];
+  const char* e = getenv("QG_FLUSH");
+  const int flush = e ? (atoi(e) == 3 ? 3 : 0) : 3;
+  snprintf(name, sizeof name, "dot_tiled_repack_bk%d_%s%s%s", bk, a.kb_stages ? "multiblock" : "singleblock",
+           a.kb_stages == 1 && flush == 3 ? "_split" : "", a.balanced ? "_balanced" : "");
+  *variant = name;
+  switch (bk) {
+    case 52: return launch_tiled_repack_b<52>(a, flush, s);
+    case 44: return launch_tiled_repack_b<44>(a, flush, s);
+    case 36: return launch_tiled_repack_b<36>(a, flush, s);
+    case 28: return launch_tiled_repack_b<28>(a, flush, s);
+    case 20: return launch_tiled_repack_b<20>(a, flush, s);
+    case 12: return launch_tiled_repack_b<12>(a, flush, s);
+    case 4: return launch_tiled_repack_b<4>(a, flush, s);
   }
   return cudaErrorInvalidValue;
 }

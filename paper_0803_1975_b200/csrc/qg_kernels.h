@@ -37,6 +37,9 @@ cudaError_t launch_redq(double* w, size_t count, int t, int e, uint32_t p, int* 
 cudaError_t launch_uncompress(const double* w, size_t srows, size_t scols, size_t lrows,
                               size_t lcols, int t, int e, int slots, int reversed, int column_axis,
                               uint32_t p, int32_t* out, int* overflow, cudaStream_t s);
+// extract_all (pack.hpp:104-119) of every word: e unreduced digits per word.
+cudaError_t launch_extract_digits(const void* w, bool u64, size_t count, int t, int e, uint64_t* out, int* overflow,
+                                  cudaStream_t s);
 cudaError_t launch_reduce_common(const double* acc, size_t count, uint32_t qmask, uint32_t p,
                                  int32_t* c, cudaStream_t s);
 
@@ -72,6 +75,11 @@ cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const cha
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
 // Same contraction on the tiled layout (a = CA_t, b = CB_t; lda/ldb unused).
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
+// The same with ReduceAndCompress fused into the epilogue (p < 256): CC words
+// (a.cc, a.ldcc) = C's rows packed forward in groups of a.e under Q = 2^a.t.
+// Words that straddle 32-column warp segments are accumulated with atomics:
+// the caller zeroes CC first unless a.e divides 32.
+cudaError_t launch_dot_tiled_repack(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 // Mixed variant on the tiled layout: a = A_t (residues, e = 1 blocks), b =
 // CBo_t (compress_outer_cols words, transposed blocks); REDQ between k-blocks
 // (kb_stages) and in the epilogue, CC m x N (N = ceil(n/e)).

@@ -2,21 +2,30 @@
 // packings (K1-K3 + outer rows), REDQ, digit scatter (uncompress, K6) and the
 // common-entry reduction. Each thread produces whole words, so every output
 // store is a coalesced 8-byte write; input residues are read once.
+#include <type_traits>
 #include "qg_kernels.h"
 #include "qg_device.cuh"
 
 namespace qgk {
 
 // K0: random_residue_matrix, prng.hpp:31-38 — element (r, c) of the matrix is
-// SplitMix64 output number r*cols + c, reduced with `% p` (prng.hpp:25).
+// SplitMix64 output number r*cols + c, reduced mod p (prng.hpp:25). The
+// 64-bit `%` is emulated in software on the GPU (26 % of HBM speed, r1); it is
+// replaced by an exact Barrett reduction: with magic = floor((2^64-1)/p),
+// q = mulhi(x, magic) is floor(x/p) or one less (x magic / 2^64 > x/p - 1), so
+// x - q p lies in [0, 2p) and one conditional subtraction gives x mod p.
 template <typename TOut>
-__global__ void k_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t rows, size_t cols,
+__global__ void k_gen_residues(uint64_t seed, uint32_t p, uint64_t magic, size_t row0, size_t rows, size_t cols,
                                TOut* __restrict__ dst) {
   const size_t total = rows * cols;
   const size_t base = row0 * cols;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x)
-    store_residue(dst + i, (uint32_t)(splitmix64_at(seed, base + i) % p));
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t x = splitmix64_at(seed, base + i);
+    uint64_t r = x - __umul64hi(x, magic) * p;
+    if (r >= p) r -= p;
+    store_residue(dst + i, (uint32_t)r);
+  }
 }
 
 // Panel geometry of the common dimension: k residues split into panels of
@@ -608,10 +617,12 @@ cudaError_t launch_gen_residues(uint64_t seed, uint32_t p, size_t row0, size_t r
                                 void* dst, int dtype, cudaStream_t s) {
   const size_t total = rows * cols;
   if (total == 0) return cudaSuccess;
+  if (p == 0) return cudaErrorInvalidValue;
+  const uint64_t magic = ~0ull / p;
   if (dtype == 0)
-    k_gen_residues<double><<<grid1d(total, 256), 256, 0, s>>>(seed, p, row0, rows, cols, (double*)dst);
+    k_gen_residues<double><<<grid1d(total, 256), 256, 0, s>>>(seed, p, magic, row0, rows, cols, (double*)dst);
   else
-    k_gen_residues<uint32_t><<<grid1d(total, 256), 256, 0, s>>>(seed, p, row0, rows, cols, (uint32_t*)dst);
+    k_gen_residues<uint32_t><<<grid1d(total, 256), 256, 0, s>>>(seed, p, magic, row0, rows, cols, (uint32_t*)dst);
   count_launch();
   return cudaGetLastError();
 }
@@ -843,6 +854,45 @@ cudaError_t launch_reduce_common(const double* acc, size_t count, uint32_t qmask
                                  int32_t* c, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
   k_reduce_common<<<grid1d(count, 256), 256, 0, s>>>(acc, count, qmask, p, c);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// extract_all, pack.hpp:104-119, over `count` words: the e base-Q digits of
+// every word, least significant first, unreduced (each in [0, Q-1]); a word
+// that is negative or not below Q^e raises *overflow (DigitOverflow).
+// W = double (DoubleWord) or uint64_t (Int64Word).
+template <class W>
+__global__ void k_extract_digits(const W* __restrict__ w, size_t count, int t, int e, uint64_t* __restrict__ out,
+                                 int* overflow) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const W v = w[i];
+  const int total = t * e;
+  bool bad;
+  if constexpr (std::is_same<W, double>::value)
+    bad = !(v >= 0.0) || !(v < exp2((double)total));  // NaN and negative words included
+  else
+    bad = total < 64 && (uint64_t)v >= (1ull << total);
+  if (bad) {
+    atomicExch(overflow, 1);
+    return;
+  }
+  const uint64_t bits = std::is_same<W, double>::value ? __double2ull_rz((double)v) : (uint64_t)v;
+  const uint64_t mask = t >= 64 ? ~0ull : ((1ull << t) - 1);
+  for (int s = 0; s < e; ++s) {
+    const int sh = s * t;
+    out[i * e + s] = sh < 64 ? (bits >> sh) & mask : 0ull;
+  }
+}
+
+cudaError_t launch_extract_digits(const void* w, bool u64, size_t count, int t, int e, uint64_t* out, int* overflow,
+                                  cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (u64)
+    k_extract_digits<uint64_t><<<grid1d(count, 256), 256, 0, s>>>((const uint64_t*)w, count, t, e, out, overflow);
+  else
+    k_extract_digits<double><<<grid1d(count, 256), 256, 0, s>>>((const double*)w, count, t, e, out, overflow);
   count_launch();
   return cudaGetLastError();
 }

@@ -135,72 +135,74 @@ int cmd_plan(const Options& o) {  // qgemm_main.cpp:66-97
   const auto k = number<std::uint64_t>(o, "k", 0, true);
   const int bits = number<int>(o, "bits", 53, false);
   check_modulus(p);
+  const PrimeModulus mod(p);
   if (o.flag("full")) {
-    const FullPlan fp = plan_full(p, k, bits);
+    const FullPlan fp = plan_full(mod, k, bits);
     std::cout << "p        " << p << "\n"
               << "k        " << k << "\n"
-              << "beta     " << fp.base().beta() << "\n"
-              << "t        " << fp.base().t() << "\n"
-              << "Q        2^" << fp.base().t() << "\n"
+              << "beta     " << fp.base.beta << "\n"
+              << "t        " << fp.base.t << "\n"
+              << "Q        2^" << fp.base.t << "\n"
               << "dq+1     " << fp.q_slots() << "\n"
               << "dtheta+1 " << fp.theta_slots() << "\n"
-              << "Theta    2^" << fp.theta_exponent() << "\n"
-              << "digits   " << fp.base().e() << "\n"
-              << "kmax     " << fp.base().kmax() << "\n";
+              << "Theta    2^" << fp.theta_exponent << "\n"
+              << "digits   " << fp.base.e << "\n"
+              << "kmax     " << fp.base.kmax << "\n";
     return kExitOk;
   }
   const auto mode = o.flag("add-high-bits") ? ExtractionMode::AddHighBits : ExtractionMode::ReciprocalMul;
-  const CompressionPlan plan = plan_compression(p, k, bits, mode);
+  const CompressionPlan plan = plan_compression(mod, k, bits, mode);
   std::cout << "p        " << p << "\n"
             << "k        " << k << "\n"
-            << "beta     " << plan.beta() << "\n"
-            << "t        " << plan.t() << "\n"
-            << "Q        2^" << plan.t() << "\n"
-            << "d        " << plan.d() << "\n"
-            << "e        " << plan.e() << "\n"
-            << "kmax     " << plan.kmax() << "\n";
+            << "beta     " << plan.beta << "\n"
+            << "t        " << plan.t << "\n"
+            << "Q        2^" << plan.t << "\n"
+            << "d        " << plan.d << "\n"
+            << "e        " << plan.e << "\n"
+            << "kmax     " << plan.kmax << "\n";
   return kExitOk;
 }
 
 // One algorithm on host matrices, with the plans the reference chooses for it
 // in `gemm` and `verify` (qgemm_main.cpp:118-145, verify.hpp:29-68), on the
 // DoubleWord (i64 = false) or the Int64Word backend.
-ResidueMatrix run_algorithm(Algorithm algo, const ResidueMatrix& a, const ResidueMatrix& b, std::uint32_t p,
+ResidueMatrix run_algorithm(Algorithm algo, const ResidueMatrix& a, const ResidueMatrix& b, const PrimeModulus& mod,
                             int beta, std::uint64_t kpanel, bool verify_mode, bool i64) {
   const std::uint64_t k = a.cols;
   switch (algo) {
     case Algorithm::Naive:
-      return naive_gemm(a, b, p);
+      return naive_gemm(a, b, mod);
     case Algorithm::CommonCompressed: {
-      CompressionPlan plan;
-      try {
-        plan = plan_compression(p, k, beta);
-      } catch (const NoCompression&) {
-        if (!verify_mode || k > 1) throw;
-        plan = uncompressed_plan(p, k, beta);  // verify.hpp:37-44
-      }
+      const CompressionPlan plan = [&] {
+        try {
+          return plan_compression(mod, k, beta);
+        } catch (const NoCompression&) {
+          if (!verify_mode || k > 1) throw;
+          return uncompressed_plan(mod, k, beta);  // verify.hpp:37-44
+        }
+      }();
       return i64 ? mul_common_compressed<Int64Word>(a, b, plan) : mul_common_compressed(a, b, plan);
     }
     case Algorithm::RightCompressed: {
-      const CompressionPlan plan = plan_packed_axis(p, k, b.cols, beta);
-      return i64 ? uncompress(mul_right_compressed_i64(a, b, plan)) : uncompress(mul_right_compressed(a, b, plan));
+      const CompressionPlan plan = plan_packed_axis(mod, k, b.cols, beta);
+      return i64 ? uncompress(mul_right_compressed<Int64Word>(a, b, plan)) : uncompress(mul_right_compressed(a, b, plan));
     }
     case Algorithm::LeftCompressed: {
-      const CompressionPlan plan = plan_packed_axis(p, k, a.rows, beta);
-      return i64 ? uncompress(mul_left_compressed_i64(a, b, plan)) : uncompress(mul_left_compressed(a, b, plan));
+      const CompressionPlan plan = plan_packed_axis(mod, k, a.rows, beta);
+      return i64 ? uncompress(mul_left_compressed<Int64Word>(a, b, plan)) : uncompress(mul_left_compressed(a, b, plan));
     }
     case Algorithm::FullCompressed:
-      return i64 ? mul_full_compressed<Int64Word>(a, b, plan_full(p, k, beta))
-                 : mul_full_compressed(a, b, plan_full(p, k, beta));
+      return i64 ? mul_full_compressed<Int64Word>(a, b, plan_full(mod, k, beta))
+                 : mul_full_compressed(a, b, plan_full(mod, k, beta));
     case Algorithm::Blocked: {
       std::uint64_t kp;
       if (verify_mode) {
         kp = (k + 1) / 2;  // verify.hpp:60-66: two panels
       } else {
-        kp = kpanel ? kpanel : choose_panel(p, k, beta);
+        kp = kpanel ? kpanel : choose_panel(mod, k, beta);
         if (kp == 0) kp = k;
       }
-      const CompressionPlan plan = kp >= 2 ? plan_compression(p, kp, beta) : uncompressed_plan(p, 1, beta);
+      const CompressionPlan plan = kp >= 2 ? plan_compression(mod, kp, beta) : uncompressed_plan(mod, 1, beta);
       return i64 ? blocked_accumulate<Int64Word>(a, b, plan, kp) : blocked_accumulate(a, b, plan, kp);
     }
   }
@@ -237,7 +239,7 @@ int cmd_gemm(const Options& o) {  // qgemm_main.cpp:99-148
                             std::to_string(a.cols) + ", " + b_path + " is " + std::to_string(b.rows) + "x" +
                             std::to_string(b.cols));
   const Algorithm algo = parse_algorithm(o.values.at("algo"));
-  const ResidueMatrix c = run_algorithm(algo, a, b, fa.p, beta, kpanel, false, i64);
+  const ResidueMatrix c = run_algorithm(algo, a, b, PrimeModulus(fa.p), beta, kpanel, false, i64);
   write_matrix_file(out_path, c, fa.p);
   return kExitOk;
 }
@@ -249,6 +251,7 @@ int cmd_verify(const Options& o) {  // qgemm_main.cpp:150-170, verify.hpp:70-140
   const int beta = number<int>(o, "bits", 53, false);
   if (beta > 63) throw std::invalid_argument("--bits must be at most 63");
   check_modulus(p);
+  const PrimeModulus mod(p);
   if (max_dim < 1) throw std::invalid_argument("--max-dim must be >= 1");
   // verify.hpp:128-137: both word backends, DoubleWord at min(beta, 53),
   // Int64Word at 63 unless a wider beta was asked for
@@ -267,16 +270,16 @@ int cmd_verify(const Options& o) {  // qgemm_main.cpp:150-170, verify.hpp:70-140
       const std::size_t m = 1 + dims.below(max_dim);
       const std::size_t k = 1 + dims.below(max_dim);
       const std::size_t n = 1 + dims.below(max_dim);
-      const ResidueMatrix a = random_residue_matrix(m, k, p, seed * 2 + 1);
-      const ResidueMatrix b = random_residue_matrix(k, n, p, seed * 2 + 2);
+      const ResidueMatrix a = random_residue_matrix(m, k, mod, seed * 2 + 1);
+      const ResidueMatrix b = random_residue_matrix(k, n, mod, seed * 2 + 2);
       ResidueMatrix got;
       try {
-        got = run_algorithm(algo, a, b, p, bb, 0, true, i64);
+        got = run_algorithm(algo, a, b, mod, bb, 0, true, i64);
       } catch (const NoCompression&) {
         ++skipped;
         continue;
       }
-      const ResidueMatrix want = naive_gemm(a, b, p);
+      const ResidueMatrix want = naive_gemm(a, b, mod);
       ++cases;
       if (!(got == want)) {
         passed = false;
@@ -314,10 +317,11 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
   const bool i64 = backend_i64(beta);
   const auto kpanel = number<std::uint64_t>(o, "kpanel", 0, false);
   check_modulus(p);
+  const PrimeModulus mod(p);
   const Algorithm algo = parse_algorithm(o.values.at("algo"));
   set_phase_timing(true);  // seconds_multiply / seconds_convert per record
-  const ResidueMatrix a = random_residue_matrix(m, k, p, seed);
-  const ResidueMatrix b = random_residue_matrix(k, n, p, seed + 1);
+  const ResidueMatrix a = random_residue_matrix(m, k, mod, seed);
+  const ResidueMatrix b = random_residue_matrix(k, n, mod, seed + 1);
   std::vector<TimingRecord> out;
   for (int rep = 0; rep < reps; ++rep) {
     TimingRecord rec;
@@ -330,31 +334,31 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
     double extra_convert = 0;
     switch (algo) {
       case Algorithm::Naive:
-        c = naive_gemm(a, b, p);
+        c = naive_gemm(a, b, mod);
         break;
       case Algorithm::CommonCompressed: {
-        const CompressionPlan plan = plan_compression(p, k, beta);
-        rec.t = plan.t();
-        rec.e = plan.e();
+        const CompressionPlan plan = plan_compression(mod, k, beta);
+        rec.t = plan.t;
+        rec.e = plan.e;
         c = i64 ? mul_common_compressed<Int64Word>(a, b, plan) : mul_common_compressed(a, b, plan);
         break;
       }
       case Algorithm::RightCompressed:
       case Algorithm::LeftCompressed: {  // bench.hpp:108-141: plan_compression for both
-        const CompressionPlan plan = plan_compression(p, k, beta);
-        rec.t = plan.t();
-        rec.e = plan.e();
+        const CompressionPlan plan = plan_compression(mod, k, beta);
+        rec.t = plan.t;
+        rec.e = plan.e;
         PhaseSeconds ph;
         std::chrono::steady_clock::time_point t0;
         if (i64) {
-          const CompressedWords64 cc = algo == Algorithm::RightCompressed ? mul_right_compressed_i64(a, b, plan)
-                                                                          : mul_left_compressed_i64(a, b, plan);
+          const auto cc = algo == Algorithm::RightCompressed ? mul_right_compressed<Int64Word>(a, b, plan)
+                                                             : mul_left_compressed<Int64Word>(a, b, plan);
           ph = last_phase_seconds();
           t0 = std::chrono::steady_clock::now();
           c = uncompress(cc);
         } else {
-          const CompressedWords cc = algo == Algorithm::RightCompressed ? mul_right_compressed(a, b, plan)
-                                                                        : mul_left_compressed(a, b, plan);
+          const auto cc = algo == Algorithm::RightCompressed ? mul_right_compressed(a, b, plan)
+                                                             : mul_left_compressed(a, b, plan);
           ph = last_phase_seconds();
           t0 = std::chrono::steady_clock::now();
           c = uncompress(cc);
@@ -365,18 +369,18 @@ int cmd_bench(const Options& o) {  // qgemm_main.cpp:172-182, bench.hpp:61-166
         break;
       }
       case Algorithm::FullCompressed: {
-        const FullPlan fp = plan_full(p, k, beta);
-        rec.t = fp.base().t();
-        rec.e = fp.base().e();
+        const FullPlan fp = plan_full(mod, k, beta);
+        rec.t = fp.base.t;
+        rec.e = fp.base.e;
         c = i64 ? mul_full_compressed<Int64Word>(a, b, fp) : mul_full_compressed(a, b, fp);
         break;
       }
       case Algorithm::Blocked: {
-        std::uint64_t kp = kpanel ? kpanel : choose_panel(p, k, beta);
+        std::uint64_t kp = kpanel ? kpanel : choose_panel(mod, k, beta);
         if (kp == 0) kp = k;
-        const CompressionPlan plan = kp >= 2 ? plan_compression(p, kp, beta) : uncompressed_plan(p, 1, beta);
-        rec.t = plan.t();
-        rec.e = plan.e();
+        const CompressionPlan plan = kp >= 2 ? plan_compression(mod, kp, beta) : uncompressed_plan(mod, 1, beta);
+        rec.t = plan.t;
+        rec.e = plan.e;
         c = i64 ? blocked_accumulate<Int64Word>(a, b, plan, kp) : blocked_accumulate(a, b, plan, kp);
         break;
       }

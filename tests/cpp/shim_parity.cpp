@@ -1,6 +1,9 @@
 // Reference-style C++ test of the qgemm_b200 drop-in (include/qgemm_b200.hpp):
 // the known answers of /root/reference/proj/tests/test_gemm.cpp and README,
-// written against the new namespace exactly as a reference user would.
+// written against the new namespace exactly as a reference user would, plus
+// the B200 additions (GPU plans, the multi-device entry, residue-in right /
+// left products). tests/cpp/dropin_parity.cpp is the same-source comparison
+// with the reference itself.
 // Built by tests/test_cpp_shim.py; run on a GPU (it calls the CUDA path).
 #include <cstdio>
 #include <cstdlib>
@@ -54,21 +57,26 @@ int main() {
   const auto kA = from_rows(2, 2, {1, 2, 0, 1});
   const auto kB = from_rows(2, 2, {2, 0, 1, 1});
   const auto kC = from_rows(2, 2, {1, 2, 1, 1});
-  CompressionPlan p5;  // make_plan(3, 5, 2): Q = 32
-  p5.c = {3, 5, 1, 2, 53, 7, 1.0 / 32, 0};
+  CompressionPlan p5{PrimeModulus(3)};  // make_plan(3, 5, 2): Q = 32
+  p5.t = 5;
+  p5.d = 1;
+  p5.e = 2;
+  p5.kmax = 7;
+  p5.inv_qd = 1.0 / 32;
+  const PrimeModulus m3(3), m7(7);
   CHECK(mul_common_compressed(kA, kB, p5) == kC);
   CHECK(blocked_accumulate(kA, kB, p5, 1) == kC);
 
   // README.md:97-99: p=3, 512^3, seed 42 -> checksum 262622
   const auto a = host_random_matrix(512, 512, 3, 42);
   const auto b = host_random_matrix(512, 512, 3, 43);
-  CHECK(random_residue_matrix(512, 512, 3, 42) == a);  // the device generator, same stream
-  const auto plan = plan_compression(3, 512);
-  CHECK(plan.t() == 12 && plan.e() == 4);
+  CHECK(random_residue_matrix(512, 512, m3, 42) == a);  // the device generator, same stream
+  const auto plan = plan_compression(m3, 512);
+  CHECK(plan.t == 12 && plan.e == 4);
   const auto c = mul_common_compressed(a, b, plan);
   CHECK(residue_checksum(c) == 262622u);
-  CHECK(mul_common_compressed(a, b, plan_gpu(3, 512)) == c);
-  CHECK(mul_common_compressed(a, b, plan_gpu(3, 512), std::vector<int>{0}) == c);  // one-process multi-GPU entry
+  CHECK(mul_common_compressed(a, b, plan_gpu(m3, 512)) == c);
+  CHECK(mul_common_compressed(a, b, plan_gpu(m3, 512), std::vector<int>{0}) == c);  // one-process multi-GPU entry
 
   // panel blocking (test_gemm.cpp:503-523): k twice past kmax
   const auto a14 = host_random_matrix(3, 14, 3, 31);
@@ -85,35 +93,36 @@ int main() {
   // k beyond any single plan: the GPU planner blocks it (p=7, k=4096)
   const auto a7 = host_random_matrix(64, 4096, 7, 5);
   const auto b7 = host_random_matrix(4096, 48, 7, 6);
-  CHECK(mul_common_compressed(a7, b7, plan_gpu(7, 4096)) == host_naive(a7, b7, 7));
+  CHECK(mul_common_compressed(a7, b7, plan_gpu(m7, 4096)) == host_naive(a7, b7, 7));
 
   // right compression (test_gemm.cpp:417-443): CB = [[2],[33]], C = kC
   const auto cc = mul_right_compressed(kA, kB, p5);
   // C = kC: row 0 digits (1, 2) -> 1 + 2*32 = 65; row 1 digits (1, 1) -> 33
-  CHECK(cc.stored_cols == 1 && cc.data[0] == 65.0 && cc.data[1] == 33.0);
+  CHECK(cc.stored_cols == 1 && cc.data[0].value == 65.0 && cc.data[1].value == 33.0);
 
   CHECK(uncompress(cc) == kC);
 
   // left compression (test_gemm.cpp:177-199): CC digits [1,1] and [2,1]
   const auto cl = mul_left_compressed(kA, kB, p5);
-  CHECK(cl.stored_rows == 1 && cl.data[0] == 33.0 && cl.data[1] == 34.0);
+  CHECK(cl.stored_rows == 1 && cl.data[0].value == 33.0 && cl.data[1].value == 34.0);
   CHECK(uncompress(cl) == kC);
   CHECK(uncompress(mul_left_compressed(kA, from_rows(2, 2, {1, 0, 0, 1}), p5)) == kA);
 
   // full compression (test_gemm.cpp:201-214): dq = dtheta = 1, Q = 32, Theta = 2^10
-  FullPlan fp;
-  fp.c.base = {3, 5, 3, 4, 53, 7, 1.0 / 32768, 0};
-  fp.c.dq = fp.c.dtheta = 1;
-  fp.c.theta_exponent = 10;
+  CompressionPlan p54 = p5;  // make_plan(3, 5, 4)
+  p54.d = 3;
+  p54.e = 4;
+  p54.inv_qd = 1.0 / 32768;
+  FullPlan fp{p54, 1, 1, 10};
   CHECK(mul_full_compressed(kA, kB, fp) == kC);
   CHECK(mul_full_compressed(ResidueMatrix(2, 2), kB, fp) == ResidueMatrix(2, 2));
-  const auto f250 = plan_full(3, 250);  // test_plan.cpp:96-104
-  CHECK(f250.base().t() == 10 && f250.q_slots() == 2 && f250.theta_slots() == 2 && f250.theta_exponent() == 20);
-  CHECK(mul_full_compressed(a14, b14, plan_full(3, 14)) == host_naive(a14, b14, 3));
+  const auto f250 = plan_full(m3, 250);  // test_plan.cpp:96-104
+  CHECK(f250.base.t == 10 && f250.q_slots() == 2 && f250.theta_slots() == 2 && f250.theta_exponent == 20);
+  CHECK(mul_full_compressed(a14, b14, plan_full(m3, 14)) == host_naive(a14, b14, 3));
 
   // naive_gemm on the device
-  CHECK(naive_gemm(kA, kB, 3) == kC);
-  CHECK(naive_gemm(a7, b7, 7) == host_naive(a7, b7, 7));
+  CHECK(naive_gemm(kA, kB, m3) == kC);
+  CHECK(naive_gemm(a7, b7, m7) == host_naive(a7, b7, 7));
 
   // matrix files (test_io.cpp:11-37) and timing CSV rows (test_io.cpp:44-55)
   const std::string path = "/tmp/qgemm_b200_shim.mtx";
@@ -138,19 +147,19 @@ int main() {
   CHECK(std::string(algorithm_name(Algorithm::FullCompressed)) == "full");
 
   // Int64Word backend (word.hpp:36-54) at beta = 63: same C, reference words
-  const auto p63 = plan_compression(3, 14, 63);
+  const auto p63 = plan_compression(m3, 14, 63);
   CHECK(mul_common_compressed<Int64Word>(a14, b14, p63) == host_naive(a14, b14, 3));
-  CHECK(blocked_accumulate<Int64Word>(a14, b14, plan_compression(3, 7, 63), 7) == host_naive(a14, b14, 3));
-  CHECK(uncompress(mul_right_compressed_i64(a14, b14, plan_packed_axis(3, 14, 5, 63))) == host_naive(a14, b14, 3));
-  CHECK(uncompress(mul_left_compressed_i64(a14, b14, plan_packed_axis(3, 14, 3, 63))) == host_naive(a14, b14, 3));
-  CHECK(mul_full_compressed<Int64Word>(a14, b14, plan_full(3, 14, 63)) == host_naive(a14, b14, 3));
-  const auto l64 = mul_left_compressed_i64(kA, kB, p5);  // test_gemm.cpp:183-185 for Int64Word
-  CHECK(l64.data[0] == 33u && l64.data[1] == 34u);
+  CHECK(blocked_accumulate<Int64Word>(a14, b14, plan_compression(m3, 7, 63), 7) == host_naive(a14, b14, 3));
+  CHECK(uncompress(mul_right_compressed<Int64Word>(a14, b14, plan_packed_axis(m3, 14, 5, 63))) == host_naive(a14, b14, 3));
+  CHECK(uncompress(mul_left_compressed<Int64Word>(a14, b14, plan_packed_axis(m3, 14, 3, 63))) == host_naive(a14, b14, 3));
+  CHECK(mul_full_compressed<Int64Word>(a14, b14, plan_full(m3, 14, 63)) == host_naive(a14, b14, 3));
+  const auto l64 = mul_left_compressed<Int64Word>(kA, kB, p5);  // test_gemm.cpp:183-185 for Int64Word
+  CHECK(l64.data[0].value == 33u && l64.data[1].value == 34u);
 
   // errors: invalid modulus, dimension mismatch
   threw = false;
   try {
-    plan_compression(4, 10);
+    plan_compression(PrimeModulus(4), 10);
   } catch (const InvalidModulus&) {
     threw = true;
   }

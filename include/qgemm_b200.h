@@ -349,6 +349,19 @@ int qg_host_mul_common_gpu(const qg_gpu_plan* gplan, const uint32_t* a, const ui
  * dlopen'ed (libnccl.so.2) at the first call; QG_NCCL_ERROR if absent. */
 int qg_host_mul_common_multi(const qg_gpu_plan* gplan, const int* devices, int ngpus, const uint32_t* a,
                              const uint32_t* b, size_t m, size_t k, size_t n, uint32_t* c);
+/* The multi-process (one rank per GPU) host path in two halves around the
+ * caller's all-gather (paper_0803_1975_b200/dist.py):
+ * qg_host_pack_b_slot_tiled uploads columns [c0, c0+cols) of the HOST B
+ * (k x ldb uint32) and packs them into cb_slot (that slot of the tiled CB_t,
+ * stage depth bk) on `stream`; qg_host_mul_common_packed_b streams the HOST
+ * row shard A (m x k) up in chunks, packs and contracts it against the
+ * DEVICE CB_t (all n columns, gathered) and streams C (m x n) back; its
+ * contractions wait on ready_event (a cudaEvent_t recorded after the gather;
+ * NULL = none) while A's upload and packing already run. */
+int qg_host_pack_b_slot_tiled(const qg_gpu_plan* gplan, uint32_t bk, const uint32_t* b, size_t ldb, size_t k,
+                              size_t c0, size_t cols, double* cb_slot, void* stream);
+int qg_host_mul_common_packed_b(const qg_gpu_plan* gplan, const uint32_t* a, size_t m, size_t k, const double* cb_t,
+                                size_t n, uint32_t* c, void* ready_event);
 int qg_host_blocked_accumulate(const qg_plan* plan, const uint32_t* a, const uint32_t* b,
                                size_t m, size_t k, size_t n, size_t kpanel, uint32_t* c);
 /* mul_right_compressed(A, compress_outer_cols(B)), gemm.hpp:320-325, on HOST

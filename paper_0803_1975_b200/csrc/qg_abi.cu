@@ -1241,8 +1241,10 @@ static int host_pipeline(size_t m, size_t k, size_t n, size_t align, size_t col_
   DevBuf da(hp.in), db(hp.in);
   PipeJoin join(hp);  // after the buffers: joins the streams before they are freed
   QG_TRY(da.alloc(m * k * 4));
-  QG_TRY(db.alloc(k * n * 4));
-  if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
+  if (b) {  // b == NULL: the right operand is already packed on the device (pack_b only orders on it)
+    QG_TRY(db.alloc(k * n * 4));
+    if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
+  }
   QG_TRY(cudaEventRecord(hp.b_ready, hp.in));
   for (size_t i = 0; i < nchunks; ++i) {
     const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
@@ -1582,6 +1584,65 @@ int qg_host_mul_common_repacked_gpu(const qg_gpu_plan* gplan, const uint32_t* a,
   if (st) return st;
   if (gplan->plan.t * gplan->plan.e > 53 || gplan->plan.t > 31) return QG_PLAN_MISMATCH;
   return host_common_repacked(gplan, a, b, m, k, n, cc);
+}
+
+// Multi-process (one rank per GPU) host path, SURVEY.md §8e all-gather form:
+// each rank uploads and packs only its own tile-column slot of B, the slots
+// are all-gathered by the caller (torch.distributed / NCCL), and the rank's
+// row shard of A is streamed against the gathered CB_t.
+int qg_host_pack_b_slot_tiled(const qg_gpu_plan* gplan, uint32_t bk, const uint32_t* b, size_t ldb, size_t k,
+                              size_t c0, size_t cols, double* cb_slot, void* stream) {
+  if (!gplan || (k * cols && !b) || (cols && !cb_slot)) return QG_INVALID_ARGUMENT;
+  int st = check_plan(&gplan->plan);
+  if (st) return st;
+  if (ldb < c0 + cols) return QG_INVALID_ARGUMENT;
+  if (k == 0 || cols == 0) return QG_OK;
+  cudaStream_t s = as_stream(stream);
+  keep_pool_mapped();
+  DevBuf db(s);
+  QG_TRY(db.alloc(k * cols * 4));
+  QG_TRY(cudaMemcpy2DAsync(db.p, cols * 4, b + c0, ldb * 4, cols * 4, k, cudaMemcpyHostToDevice, s));
+  return qg_pack_b_tiled(gplan, bk, db.p, QG_U32, k, cols, cols, cb_slot, stream);
+}
+
+int qg_host_mul_common_packed_b(const qg_gpu_plan* gplan, const uint32_t* a, size_t m, size_t k, const double* cb_t,
+                                size_t n, uint32_t* c, void* ready_event) {
+  if (!gplan || (m * k && !a) || (m * n && !c) || (n && !cb_t)) return QG_INVALID_ARGUMENT;
+  const qg_plan& pl = gplan->plan;
+  int st = check_plan(&pl);
+  if (st) return st;
+  if (m == 0 || n == 0) return QG_OK;
+  const size_t K = ceil_div(k, pl.e);
+  if (K == 0) {
+    std::memset(c, 0, m * n * 4);
+    return QG_OK;
+  }
+  int bk = 0, kbs = 0;
+  if ((st = tiled_geometry(gplan, K, &bk, &kbs))) return st;
+  const size_t Kt = ceil_div(K, (size_t)bk);
+  cudaStream_t s0 = host_pipe().in;
+  DevBuf dca(s0), dc(s0);
+  QG_TRY(dc.alloc(m * n * 4));
+  QG_TRY(dca.alloc(qg_tiled_words(m, k, pl.e, bk) * 8));
+  cudaEvent_t ready = static_cast<cudaEvent_t>(ready_event);
+  return host_pipeline(
+      m, k, n, 128, ceil_div(n, (size_t)128), a, nullptr,
+      [&](const uint32_t*, cudaStream_t s2) {  // B is packed: order the contractions after its producer
+        return ready ? cuda_status(cudaStreamWaitEvent(s2, ready, 0)) : (int)QG_OK;
+      },
+      [&](size_t r0, size_t rows, const uint32_t* da, cudaStream_t s2, PhaseScope& ps, ChunkOut* out) {
+        double* ca_chunk = (double*)dca.p + (r0 / 128) * Kt * 128 * bk;
+        int st2 = cuda_status(qgk::launch_pack_tiled(false, da, QG_U32, rows, k, k, pl.t, pl.e, bk, ca_chunk, s2, pl.p,
+                                                     gplan->balanced != 0));
+        if (st2) return st2;
+        ps.begin(s2);
+        if ((st2 = qg_mul_common_tiled(gplan, ca_chunk, cb_t, rows, n, k, (int32_t*)dc.p + r0 * n, n, s2))) return st2;
+        ps.end(s2);
+        out->src = (const int32_t*)dc.p + r0 * n;
+        out->dst = c + r0 * n;
+        out->bytes = rows * n * 4;
+        return (int)QG_OK;
+      });
 }
 
 int qg_host_mul_common(const qg_plan* plan, const uint32_t* a, const uint32_t* b, size_t m,

@@ -1,15 +1,20 @@
 // qg_multi.cpp — mul_common_compressed over several GPUs of one process
 // (the C-ABI entry qg_host_mul_common_multi): rows of A and C
-// are sharded over the devices, B is packed once on the first device into the
-// tiled layout and broadcast as packed words with one grouped ncclBroadcast
-// (NVLink 5 / NVSwitch on a B200 node), every device packs and contracts its
-// own row shard. Host buffers in and out, like qg_host_mul_common_gpu.
+// are sharded over the devices; the right operand is assembled by an
+// all-gather: device i uploads and packs only its own tile-column slot of B
+// (compress_cols_forward is column-separable, gemm.hpp:122-140) and one
+// grouped in-place ncclAllGather (NVLink 5 / NVSwitch on a B200 node) gives
+// every device the whole packed CB_t, so every PCIe link carries 1/N of B.
+// Each device uploads and packs its A shard on a second stream meanwhile,
+// contracts its own slot's columns as soon as they are packed, and the rest
+// once the gather has landed. Host buffers in and out, like
+// qg_host_mul_common_gpu.
 //
 // NCCL is opened with dlopen at the first call (no link-time dependency: a
 // process that already loaded libnccl.so.2 — e.g. through torch — shares it).
 // Communicators are cached per device list. The one-process-per-GPU
-// deployment (bench.py under torchrun) uses torch.distributed for the same
-// broadcast (paper_0803_1975_b200/dist.py).
+// deployment (bench.py under torchrun) does the same all-gather through
+// torch.distributed (paper_0803_1975_b200/dist.py).
 #include <dlfcn.h>
 
 #include <cstdint>
@@ -32,7 +37,7 @@ typedef int ncclResult_t;
 enum { ncclSuccess = 0, ncclUint64 = 5 };
 struct Nccl {
   ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -51,11 +56,11 @@ Nccl& nccl() {
       return;
     }
     n.CommInitAll = reinterpret_cast<decltype(n.CommInitAll)>(dlsym(h, "ncclCommInitAll"));
-    n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(dlsym(h, "ncclBroadcast"));
+    n.AllGather = reinterpret_cast<decltype(n.AllGather)>(dlsym(h, "ncclAllGather"));
     n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(h, "ncclGroupStart"));
     n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    n.ok = n.CommInitAll && n.Broadcast && n.GroupStart && n.GroupEnd && n.GetErrorString;
+    n.ok = n.CommInitAll && n.AllGather && n.GroupStart && n.GroupEnd && n.GetErrorString;
     if (!n.ok) n.why = "libnccl.so.2 lacks an entry point";
   });
   return n;
@@ -133,35 +138,49 @@ extern "C" int qg_host_mul_common_multi(const qg_gpu_plan* gplan, const int* dev
   if (!comms) return st;
   int caller = 0;
   MQ_CU(cudaGetDevice(&caller));
-  const size_t wb = qg_tiled_words(n, k, pl.e, bk);  // packed CB_t words (broadcast size)
-  std::vector<DevMem> da(ngpus), dca(ngpus), dcb(ngpus), dc(ngpus), db(1);
-  std::vector<cudaStream_t> strm(ngpus, nullptr);
-  std::vector<size_t> r0(ngpus), rows(ngpus);
+  // gathered CB_t: ngpus equal slots of P tile columns (W words per tile column)
+  const size_t W = qg_tiled_words(128, k, pl.e, bk), Nt = (n + 127) / 128, P = (Nt + ngpus - 1) / ngpus;
+  const size_t slot_words = P * W;
+  std::vector<DevMem> da(ngpus), dca(ngpus), dcb(ngpus), dc(ngpus);
+  std::vector<cudaStream_t> sa(ngpus, nullptr), sb(ngpus, nullptr);
+  std::vector<cudaEvent_t> own(ngpus, nullptr), all(ngpus, nullptr);
+  std::vector<size_t> r0(ngpus), rows(ngpus), t0(ngpus), t1(ngpus);
+  // contract tile columns [u0, u1) of device i's rows against its CB_t
+  auto contract = [&](int i, size_t u0, size_t u1) -> int {
+    const size_t c0 = u0 * 128, c1 = u1 * 128 < n ? u1 * 128 : n;
+    if (c1 <= c0 || !rows[i]) return QG_OK;
+    return qg_mul_common_tiled(gplan, (const double*)dca[i].p, (const double*)dcb[i].p + u0 * W, rows[i], c1 - c0, k,
+                               (int32_t*)dc[i].p + c0, n, sa[i]);
+  };
   auto run = [&]() -> int {
     for (int i = 0; i < ngpus; ++i) {
       shard(m, ngpus, i, &r0[i], &rows[i]);
+      t0[i] = (size_t)i * P < Nt ? (size_t)i * P : Nt;
+      t1[i] = t0[i] + P < Nt ? t0[i] + P : Nt;
       MQ_CU(cudaSetDevice(devs[i]));
-      MQ_CU(cudaStreamCreateWithFlags(&strm[i], cudaStreamNonBlocking));
+      MQ_CU(cudaStreamCreateWithFlags(&sa[i], cudaStreamNonBlocking));
+      MQ_CU(cudaStreamCreateWithFlags(&sb[i], cudaStreamNonBlocking));
+      MQ_CU(cudaEventCreateWithFlags(&own[i], cudaEventDisableTiming));
+      MQ_CU(cudaEventCreateWithFlags(&all[i], cudaEventDisableTiming));
       da[i].dev = dca[i].dev = dcb[i].dev = dc[i].dev = devs[i];
-      MQ_CU(cudaMalloc(&dcb[i].p, wb * 8));
-      if (rows[i]) {
+      MQ_CU(cudaMalloc(&dcb[i].p, ngpus * slot_words * 8));
+      // this device's slot of B: up (2-D copy of its columns) and packed on sb
+      const size_t bc0 = t0[i] * 128 < n ? t0[i] * 128 : n, bc1 = t1[i] * 128 < n ? t1[i] * 128 : n;
+      MQ_TRY(qg_host_pack_b_slot_tiled(gplan, bk, b, n, k, bc0, bc1 - bc0, (double*)dcb[i].p + i * slot_words, sb[i]));
+      MQ_CU(cudaEventRecord(own[i], sb[i]));
+      if (rows[i]) {  // the A shard up and packed on sa meanwhile
         MQ_CU(cudaMalloc(&da[i].p, rows[i] * k * 4));
         MQ_CU(cudaMalloc(&dca[i].p, qg_tiled_words(rows[i], k, pl.e, bk) * 8));
         MQ_CU(cudaMalloc(&dc[i].p, rows[i] * n * 4));
-        MQ_CU(cudaMemcpyAsync(da[i].p, a + r0[i] * k, rows[i] * k * 4, cudaMemcpyHostToDevice, strm[i]));
-        MQ_TRY(qg_pack_a_tiled(gplan, bk, da[i].p, QG_U32, rows[i], k, k, (double*)dca[i].p, strm[i]));
+        MQ_CU(cudaMemcpyAsync(da[i].p, a + r0[i] * k, rows[i] * k * 4, cudaMemcpyHostToDevice, sa[i]));
+        MQ_TRY(qg_pack_a_tiled(gplan, bk, da[i].p, QG_U32, rows[i], k, k, (double*)dca[i].p, sa[i]));
       }
     }
-    // B up and packed once, on the first device
-    MQ_CU(cudaSetDevice(devs[0]));
-    db[0].dev = devs[0];
-    MQ_CU(cudaMalloc(&db[0].p, k * n * 4));
-    MQ_CU(cudaMemcpyAsync(db[0].p, b, k * n * 4, cudaMemcpyHostToDevice, strm[0]));
-    MQ_TRY(qg_pack_b_tiled(gplan, bk, db[0].p, QG_U32, k, n, n, (double*)dcb[0].p, strm[0]));
-    // the packed words to every device (one grouped broadcast)
+    // every slot to every device: one grouped in-place all-gather on the sb streams
     MQ_TRY(nccl_status(nc.GroupStart()));
     for (int i = 0; i < ngpus; ++i) {
-      const ncclResult_t r = nc.Broadcast(dcb[0].p, dcb[i].p, wb, ncclUint64, 0, (*comms)[i], strm[i]);
+      const ncclResult_t r = nc.AllGather((const double*)dcb[i].p + i * slot_words, dcb[i].p, slot_words, ncclUint64,
+                                          (*comms)[i], sb[i]);
       if (r != ncclSuccess) {
         nc.GroupEnd();
         return nccl_status(r);
@@ -169,25 +188,34 @@ extern "C" int qg_host_mul_common_multi(const qg_gpu_plan* gplan, const int* dev
     }
     MQ_TRY(nccl_status(nc.GroupEnd()));
     for (int i = 0; i < ngpus; ++i) {
-      if (!rows[i]) continue;
       MQ_CU(cudaSetDevice(devs[i]));
-      MQ_TRY(qg_mul_common_tiled(gplan, (const double*)dca[i].p, (const double*)dcb[i].p, rows[i], n, k,
-                                 (int32_t*)dc[i].p, n, strm[i]));
-      MQ_CU(cudaMemcpyAsync(c + r0[i] * n, dc[i].p, rows[i] * n * 4, cudaMemcpyDeviceToHost, strm[i]));
+      MQ_CU(cudaEventRecord(all[i], sb[i]));
+      // own columns first (local as soon as packed), the rest after the gather
+      MQ_CU(cudaStreamWaitEvent(sa[i], own[i], 0));
+      MQ_TRY(contract(i, t0[i], t1[i]));
+      MQ_CU(cudaStreamWaitEvent(sa[i], all[i], 0));
+      MQ_TRY(contract(i, t1[i], Nt));
+      MQ_TRY(contract(i, 0, t0[i]));
+      if (rows[i]) MQ_CU(cudaMemcpyAsync(c + r0[i] * n, dc[i].p, rows[i] * n * 4, cudaMemcpyDeviceToHost, sa[i]));
     }
     for (int i = 0; i < ngpus; ++i) {
       MQ_CU(cudaSetDevice(devs[i]));
-      MQ_CU(cudaStreamSynchronize(strm[i]));
+      MQ_CU(cudaStreamSynchronize(sa[i]));
+      MQ_CU(cudaStreamSynchronize(sb[i]));
     }
     return QG_OK;
   };
   st = run();
-  for (int i = 0; i < ngpus; ++i)
-    if (strm[i]) {
-      cudaSetDevice(devs[i]);
-      cudaStreamSynchronize(strm[i]);
-      cudaStreamDestroy(strm[i]);
-    }
+  for (int i = 0; i < ngpus; ++i) {
+    cudaSetDevice(devs[i]);
+    for (cudaStream_t x : {sa[i], sb[i]})
+      if (x) {
+        cudaStreamSynchronize(x);
+        cudaStreamDestroy(x);
+      }
+    for (cudaEvent_t x : {own[i], all[i]})
+      if (x) cudaEventDestroy(x);
+  }
   cudaSetDevice(caller);
   return st;
 }

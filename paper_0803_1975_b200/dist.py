@@ -190,3 +190,50 @@ def _all_gather_slots(cb, slots, rank, group):
     for dst, src in zip(slots, parts):
         dst.copy_(src)
     return _Done()
+
+
+def mul_common_allgather_host(a_shard, b, gp, rank: int, world: int, out=None, group=None):
+    """mul_common_compressed on HOST data, one rank per GPU (the public
+    multi-process entry; the all-gather form of SURVEY.md §8e): this rank's
+    row shard of A (uint32, rows x k) and the whole host B (k x n; only this
+    rank's tile-column slot of it is read and sent over PCIe) in, this rank's
+    rows of C out. The rank uploads and packs its B slot
+    (qg_host_pack_b_slot_tiled), the slots are all-gathered in place over
+    NCCL, and its A shard streams up, is packed and contracted against the
+    gathered CB_t while C streams back (qg_host_mul_common_packed_b, whose
+    contractions wait on the gather's event, not its A upload). Returns C's
+    rows (uint32)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_0803_1975_b200 as qg
+
+    a_shard, b = qg._host_u32(a_shard), qg._host_u32(b)
+    rows, k = a_shard.shape
+    if b.shape[0] != k:
+        raise qg.DimensionMismatch(f"inner dimensions disagree: {a_shard.shape} times {b.shape}")
+    n = b.shape[1]
+    c = np.empty((rows, n), dtype=np.uint32) if out is None else out
+    pl = gp.plan
+    bk = qg.tiled_stage_words(gp, k)
+    W = qg.lib.qg_tiled_words(128, k, pl.e, bk)
+    nt = (n + 127) // 128
+    t0, t1, per = gather_slot(nt, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cb = torch.empty(world * per * W, dtype=torch.float64, device=dev)
+    slots = cb.view(world, -1)
+    g = gp._c()
+    vp = ctypes.c_void_p
+    c0, c1 = min(n, t0 * 128), min(n, t1 * 128)
+    qg._check(qg.lib.qg_host_pack_b_slot_tiled(ctypes.byref(g), bk, b.ctypes.data_as(vp), n, k, c0, c1 - c0,
+                                               qg._ptr(slots[rank]), qg._stream()))
+    work = _all_gather_slots(cb, slots, rank, group) if world > 1 else None
+    if work is not None:
+        work.wait()  # the current stream now waits for the gather
+    ready = torch.cuda.Event()
+    ready.record()
+    qg._check(qg.lib.qg_host_mul_common_packed_b(ctypes.byref(g), a_shard.ctypes.data_as(vp), rows, k, qg._ptr(cb), n,
+                                                 c.ctypes.data_as(vp), vp(ready.cuda_event)))
+    return c

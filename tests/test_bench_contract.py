@@ -77,7 +77,7 @@ def test_multi_rank_strong_scaling_functional():
     slot first): C's checksum equals the single-GPU one (README.md:97-99)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "config1",
-           "--steps", "2", "--warmup", "3", "--dist-backend", "gloo", "--no-e2e", "--no-cpu"]
+           "--steps", "2", "--warmup", "3", "--dist-backend", "gloo", "--no-cpu", "--e2e-steps", "2"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.strip().split("\n") if l.startswith("{")]
@@ -85,3 +85,4 @@ def test_multi_rank_strong_scaling_functional():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["m"] == 512
     assert d["checksum_c"] == 262622
+    assert d["e2e"]["matches_device"] and d["e2e"]["value"] > 0  # the all-gather host path on rank 0's shard

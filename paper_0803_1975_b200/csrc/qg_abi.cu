@@ -16,6 +16,7 @@
 #include "../../include/qgemm_b200.h"
 #include "qg_internal.h"
 #include "qg_kernels.h"
+#include "qg_stage.h"
 
 namespace qg {
 bool is_prime(uint64_t n);
@@ -1147,6 +1148,7 @@ struct HostPipe {
     return pool[i];
   }
   cudaEvent_t join[kComp + 1] = {};  // PipeJoin: one per compute stream + out
+  qg::HostStager stage;               // pinned slots for pageable host buffers (allocated on first use)
   bool ok = false;
   HostPipe() {
     ok = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess &&
@@ -1205,6 +1207,7 @@ struct PipeJoin {
       cudaStream_t st = i < HostPipe::kComp ? hp.comps[i] : hp.out;
       if (hp.join[i] && st && cudaEventRecord(hp.join[i], st) == cudaSuccess) cudaStreamWaitEvent(hp.in, hp.join[i], 0);
     }
+    hp.stage.finish();  // no staged copy into the caller's buffers outlives the call
   }
 };
 
@@ -1243,33 +1246,33 @@ static int host_pipeline(size_t m, size_t k, size_t n, size_t align, size_t col_
   QG_TRY(da.alloc(m * k * 4));
   if (b) {  // b == NULL: the right operand is already packed on the device (pack_b only orders on it)
     QG_TRY(db.alloc(k * n * 4));
-    if (k * n) QG_TRY(cudaMemcpyAsync(db.p, b, k * n * 4, cudaMemcpyHostToDevice, hp.in));
+    if (k * n) QG_TRY(hp.stage.h2d(db.p, 0, b, 0, k * n * 4, 1, hp.in));
   }
   QG_TRY(cudaEventRecord(hp.b_ready, hp.in));
-  for (size_t i = 0; i < nchunks; ++i) {
-    const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
-    if (rows * k)
-      QG_TRY(cudaMemcpyAsync((uint32_t*)da.p + r0 * k, a + r0 * k, rows * k * 4, cudaMemcpyHostToDevice, hp.in));
-    QG_TRY(cudaEventRecord(hp.a_ready[i], hp.in));
-  }
   QG_TRY(cudaStreamWaitEvent(hp.comp, hp.b_ready, 0));
   int st = pack_b((const uint32_t*)db.p, hp.comp);
   if (st) return st;
   QG_TRY(cudaEventRecord(hp.b_packed, hp.comp));
   for (int j = 1; j < ncomp; ++j) QG_TRY(cudaStreamWaitEvent(hp.comps[j], hp.b_packed, 0));
+  // chunk i goes up, then its contraction and its copy back are queued: from
+  // pinned buffers every copy is async anyway; from pageable ones (staged,
+  // the host copies into pinned slots) chunk i+1 is staged while chunk i runs
   for (size_t i = 0; i < nchunks; ++i) {
     const size_t r0 = i * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
+    if (rows * k) QG_TRY(hp.stage.h2d((uint32_t*)da.p + r0 * k, 0, a + r0 * k, 0, rows * k * 4, 1, hp.in));
+    QG_TRY(cudaEventRecord(hp.a_ready[i], hp.in));
     cudaStream_t cs = hp.comps[i % ncomp];
     QG_TRY(cudaStreamWaitEvent(cs, hp.a_ready[i], 0));
     ChunkOut out;
     if ((st = chunk(r0, rows, (const uint32_t*)da.p + r0 * k, cs, ps, &out))) return st;
     QG_TRY(cudaEventRecord(hp.c_ready[i], cs));
     QG_TRY(cudaStreamWaitEvent(hp.out, hp.c_ready[i], 0));
-    if (out.bytes) QG_TRY(cudaMemcpyAsync(out.dst, out.src, out.bytes, cudaMemcpyDeviceToHost, hp.out));
+    if (out.bytes) QG_TRY(hp.stage.d2h(out.dst, 0, out.src, 0, out.bytes, 1, hp.out));
   }
   QG_TRY(cudaEventRecord(hp.done, hp.out));
   QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
   QG_TRY(cudaStreamSynchronize(hp.out));
+  QG_TRY(hp.stage.finish());
   ps.finish();
   return QG_OK;
 }
@@ -1355,7 +1358,7 @@ static int host_pipeline2d(
       panel(ib, &c0, &cols);
       const uint32_t* dbp = (const uint32_t*)db.p + c0 * k;
       if (k * cols)
-        QG_TRY(cudaMemcpy2DAsync((void*)dbp, cols * 4, b + c0, n * 4, cols * 4, k, cudaMemcpyHostToDevice, hp.in));
+        QG_TRY(hp.stage.h2d((void*)dbp, cols * 4, b + c0, n * 4, cols * 4, k, hp.in));
       QG_TRY(cudaEventRecord(ready, hp.in));
       QG_TRY(cudaStreamWaitEvent(ps_s, ready, 0));
       int st = pack_b_panel(c0, cols, dbp, ps_s);
@@ -1367,7 +1370,7 @@ static int host_pipeline2d(
     } else {
       const size_t r0 = ia * rows_per, rows = (m - r0) < rows_per ? (m - r0) : rows_per;
       const uint32_t* dap = (const uint32_t*)da.p + r0 * k;
-      if (rows * k) QG_TRY(cudaMemcpyAsync((void*)dap, a + r0 * k, rows * k * 4, cudaMemcpyHostToDevice, hp.in));
+      if (rows * k) QG_TRY(hp.stage.h2d((void*)dap, 0, a + r0 * k, 0, rows * k * 4, 1, hp.in));
       QG_TRY(cudaEventRecord(ready, hp.in));
       QG_TRY(cudaStreamWaitEvent(ps_s, ready, 0));
       int st = pack_a_chunk(r0, rows, dap, ps_s);
@@ -1397,8 +1400,7 @@ static int host_pipeline2d(
         QG_TRY(cudaEventRecord(done_t, cs));
         QG_TRY(cudaStreamWaitEvent(hp.out, done_t, 0));
         if (out.width && out.height)
-          QG_TRY(cudaMemcpy2DAsync(out.dst, out.dpitch, out.src, out.spitch, out.width, out.height,
-                                   cudaMemcpyDeviceToHost, hp.out));
+          QG_TRY(hp.stage.d2h(out.dst, out.dpitch, out.src, out.spitch, out.width, out.height, hp.out));
       }
     if (send_b) ++ib;
     else ++ia;
@@ -1406,6 +1408,7 @@ static int host_pipeline2d(
   QG_TRY(cudaEventRecord(hp.done, hp.out));
   QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));  // buffers are freed on `in` after everything
   QG_TRY(cudaStreamSynchronize(hp.out));
+  QG_TRY(hp.stage.finish());
   ps.finish();
   return QG_OK;
 }
@@ -1601,7 +1604,7 @@ int qg_host_pack_b_slot_tiled(const qg_gpu_plan* gplan, uint32_t bk, const uint3
   keep_pool_mapped();
   DevBuf db(s);
   QG_TRY(db.alloc(k * cols * 4));
-  QG_TRY(cudaMemcpy2DAsync(db.p, cols * 4, b + c0, ldb * 4, cols * 4, k, cudaMemcpyHostToDevice, s));
+  QG_TRY(host_pipe().stage.h2d(db.p, cols * 4, b + c0, ldb * 4, cols * 4, k, s));
   return qg_pack_b_tiled(gplan, bk, db.p, QG_U32, k, cols, cols, cb_slot, stream);
 }
 
@@ -1811,8 +1814,8 @@ static int host_redq_ksplit(
     if ((st = part_geo(kp, &bkp, &ktp))) return st;
     uint32_t* dap = (uint32_t*)da.p + m * k0;  // m x kp, contiguous (A's columns k0..)
     uint32_t* dbp = (uint32_t*)db.p + k0 * n;  // kp x n, contiguous (B's rows k0..)
-    QG_TRY(cudaMemcpyAsync(dbp, b + k0 * n, kp * n * 4, cudaMemcpyHostToDevice, hp.in));
-    QG_TRY(cudaMemcpy2DAsync(dap, kp * 4, a + k0, k * 4, kp * 4, m, cudaMemcpyHostToDevice, hp.in));
+    QG_TRY(hp.stage.h2d(dbp, 0, b + k0 * n, 0, kp * n * 4, 1, hp.in));
+    QG_TRY(hp.stage.h2d(dap, kp * 4, a + k0, k * 4, kp * 4, m, hp.in));
     cudaEvent_t ready = hp.event(ev++);
     if (!ready) return QG_CUDA_ERROR;
     QG_TRY(cudaEventRecord(ready, hp.in));
@@ -1840,8 +1843,7 @@ static int host_redq_ksplit(
         if (!done_c) return QG_CUDA_ERROR;
         QG_TRY(cudaEventRecord(done_c, cs));
         QG_TRY(cudaStreamWaitEvent(hp.out, done_c, 0));
-        QG_TRY(cudaMemcpyAsync(cc + r0 * cols_b, (double*)dcc.p + r0 * cols_b, rows * cols_b * 8,
-                               cudaMemcpyDeviceToHost, hp.out));
+        QG_TRY(hp.stage.d2h(cc + r0 * cols_b, 0, (double*)dcc.p + r0 * cols_b, 0, rows * cols_b * 8, 1, hp.out));
       }
     }
     contracted[pi] = hp.event(ev++);
@@ -1852,6 +1854,7 @@ static int host_redq_ksplit(
   QG_TRY(cudaEventRecord(hp.done, hp.out));
   QG_TRY(cudaStreamWaitEvent(hp.in, hp.done, 0));
   QG_TRY(cudaStreamSynchronize(hp.out));
+  QG_TRY(hp.stage.finish());
   ps.finish();
   return QG_OK;
 }

@@ -618,6 +618,12 @@ def our_arm(args):
     cb = torch.zeros(world * P * W if world > 1 else qg.lib.qg_tiled_words(n, k, pl.e, bk), dtype=torch.float64,
                      device=dev)
     c = torch.empty((max(m_rank, 1), n), dtype=torch.int32, device=dev)
+    # --output cc: the compressed-out product (mul_common_repacked, gemm.hpp:275-280), one GPU
+    repacked = args.output == "cc"
+    if repacked and world > 1:
+        raise SystemExit("--output cc runs on one GPU")
+    H = -(-n // pl.e)
+    cc_out = torch.empty((m_rank, H), dtype=torch.float64, device=dev) if repacked else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
     sp = qg._stream
@@ -660,7 +666,7 @@ def our_arm(args):
     # (both packs on forked branches, then the contraction) and replayed, so
     # host launch gaps stay out of the step (they dominate small shapes such
     # as config 1); the contraction's timing events are record nodes inside it.
-    use_graph = world == 1 and not args.no_graph
+    use_graph = world == 1 and (not args.no_graph or repacked)
     launches_per_step = None
     kernel_name = None
     if use_graph:
@@ -676,8 +682,12 @@ def our_arm(args):
             pack_rows(a)
             torch.cuda.current_stream().wait_stream(side)
             gc0.record()
-            qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca), qg._ptr(cb), m_rank, n, k,
-                                                 qg._ptr(c), n, sp()))
+            if repacked:  # mul_common_repacked: ReduceAndCompress fused into the epilogue (EPI_REPACK)
+                qg._check(qg.lib.qg_mul_common_repacked_tiled(ctypes.byref(gpc), qg._ptr(ca), qg._ptr(cb), m_rank, n,
+                                                              k, qg._ptr(cc_out), H, sp()))
+            else:
+                qg._check(qg.lib.qg_mul_common_tiled(ctypes.byref(gpc), qg._ptr(ca), qg._ptr(cb), m_rank, n, k,
+                                                     qg._ptr(c), n, sp()))
             gc1.record()
         launches_per_step = qg.kernel_launches() - n0
         kernel_name = qg.last_kernel()
@@ -727,6 +737,9 @@ def our_arm(args):
     value = 2.0 * m * n * k / (ms_per_step * 1e-3)
 
     # parity spot-check inside the bench: checksum of this rank's C
+    if repacked:  # C = uncompress(CC): its checksum must equal the plain product's
+        c = qg.uncompress(qg.CompressedMatrix(m_rank, n, m_rank, H, qg.PackOrientation(
+            qg.PackDirection.Forward, qg.PackAxis.Column, pl.e), pl, cc_out))
     checksum = qg.residue_checksum(c[:m_rank]) if m_rank else 0
     if world > 1:
         cs = torch.tensor([checksum], dtype=torch.int64, device=dev)
@@ -760,7 +773,8 @@ def our_arm(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
-        "config": {"workload": desc, "p": p, "m": m, "k": k, "n": n,
+        "config": {"workload": desc + ("; output CC = mul_common_repacked (ReduceAndCompress fused)" if repacked else ""),
+                   "p": p, "m": m, "k": k, "n": n,
                    "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
                             "balanced": bool(gp.balanced), "source": args.plan},
                    "layout": "tiled packed operands (128 x stage_words blocks, CB transposed)" + (
@@ -825,9 +839,15 @@ def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1, device_c=None):
 
     from paper_0803_1975_b200.dist import mul_common_allgather_host
 
+    repacked = args.output == "cc"
+    cc_host = np.empty((mr, -(-n // gp.plan.e)), dtype=np.float64) if repacked else None
+
     def call(a_, b_, c_):
         if world > 1:  # each rank sends only its slot of B over its PCIe link; NCCL all-gather of packed slots
             return mul_common_allgather_host(a_, b_, gp, rank, world, out=c_)
+        if repacked:  # CC words back (8/e bytes per residue), C unpacked on the device afterwards for the checks
+            qg.mul_common_repacked_host(a_, b_, gp, out=cc_host)
+            return c_
         return qg.mul_common_compressed_host(a_, b_, gp, out=c_)
 
     def timed(a_, b_, c_, steps):
@@ -848,10 +868,16 @@ def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1, device_c=None):
         return t
 
     t = timed(an, bn, cn, args.e2e_steps)
+    if repacked:
+        pl = gp.plan
+        cn[:] = qg.uncompress(qg.CompressedMatrix(mr, n, mr, cc_host.shape[1], qg.PackOrientation(
+            qg.PackDirection.Forward, qg.PackAxis.Column, pl.e), pl, torch.from_numpy(cc_host).cuda())).cpu().numpy()
     out = {"value": 2.0 * m * n * k / t, "unit": "mult-adds/s (2mnk/s)",
            "h2d_bytes_per_step": int((m * k + k * n) * 4),
-           "d2h_bytes_per_step": int(m * n * 4), "ms_per_step": t * 1e3,
-           "api": ("mul_common_compressed_host (qg_host_mul_common_gpu), pipelined H2D/compute/D2H, pinned buffers"
+           "d2h_bytes_per_step": int(cc_host.nbytes if repacked else m * n * 4), "ms_per_step": t * 1e3,
+           "api": ("mul_common_repacked_host (qg_host_mul_common_repacked_gpu: CC words back), pinned buffers"
+                   if repacked else
+                   "mul_common_compressed_host (qg_host_mul_common_gpu), pipelined H2D/compute/D2H, pinned buffers"
                    if world == 1 else
                    f"dist.mul_common_allgather_host on each of {world} ranks (its row shard of A and its 1/{world} "
                    "column slot of B over its own PCIe link, packed slots all-gathered over NCCL, C shard back), "
@@ -859,7 +885,7 @@ def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1, device_c=None):
            "checksum_rank0": int(cn.astype(np.uint64).sum() & 0xFFFFFFFF),
            "matches_device": None if device_c is None else
            bool(np.array_equal(cn, device_c.cpu().numpy().astype(np.uint32)))}
-    if args.pageable and world == 1:
+    if args.pageable and world == 1 and not repacked:
         del a, b, c
         ap_, bp_ = np.array(an), np.array(bn)  # plain (pageable) copies
         cp_ = np.empty_like(cn)
@@ -883,6 +909,8 @@ def make_parser():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path with several ranks on one GPU")
     ap.add_argument("--pageable", type=int, default=1, help="also time e2e from pageable host buffers (N=1)")
+    ap.add_argument("--output", default="c", choices=["c", "cc"],
+                    help="c: int32 C (mul_common_compressed); cc: forward-packed CC words (mul_common_repacked)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-s", type=float, default=4.0, help="target wall seconds of the CPU baseline sample")
     ap.add_argument("--cpu1-s", type=float, default=3.0, help="target seconds of the 1-thread CPU sample (0: skip)")

@@ -421,8 +421,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
-  constexpr int GROUP = 8;
+// Tile raster: groups of `group` tile rows, walked column by column, so the
+// CTAs resident at one time share their A and B panels in L2.
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int group, int& tm, int& tn) {
+  const int GROUP = group > 0 ? group : 8;
   const int per_group = GROUP * tiles_n;
   const int gid = tile / per_group;
   const int first_m = gid * GROUP;
@@ -539,7 +541,7 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
   if (warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise SMSP warp pairs
   for (int ts = 0; ts < my_tiles; ++ts) {
     int tm, tn;
-    tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+    tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, args.group, tm, tn);
     const int m0 = tm * BM, n0 = tn * BN;
     if (EPI != EPI_DIGIT && args.accumulate) {
       // continue from the words already in CC (a k-split host product: the
@@ -792,7 +794,7 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_bulk(GemmArgs args, int ti
     uint32_t slot = 0, phase = 0;
     for (int ts = 0; ts < my_tiles; ++ts) {
       int tm, tn;
-      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, args.group, tm, tn);
       const int m0 = tm * BM, n0 = tn * BN;
       const int mrows = (M - m0) < BM ? (M - m0) : BM;
       const int ncols = (N - n0) < BN ? (N - n0) : BN;
@@ -868,13 +870,15 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int t
   const int my_tiles = blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const bool nomem = args.debug & 1;
 
+  uint8_t* repack = reinterpret_cast<uint8_t*>(empty + S);  // EPI_REPACK staging (after the barriers)
+
   if (warp >= NWARPS) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (nomem || warp != NWARPS || lane != 0) return;
     uint32_t slot = 0, phase = 0;
     for (int ts = 0; ts < my_tiles; ++ts) {
       int tm, tn;
-      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, tm, tn);
+      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, args.group, tm, tn);
       const double* ablk = args.a + (size_t)tm * ktiles * BM * BK;
       const double* bblk = args.b + (size_t)tn * ktiles * BM * BK;
       for (int kt = 0; kt < ktiles; ++kt) {
@@ -892,7 +896,6 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int t
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-  uint8_t* repack = reinterpret_cast<uint8_t*>(empty + S);  // EPI_REPACK staging (after the barriers)
   // FLUSH (multi-block): 0 = at stage ends; for kb_stages == 1 also
   // 1 = staggered (warps 4..7 cut mid-stage; two inlined consumer bodies, so
   // instantiated separately) and 2 = fused into the next stage's first k-step.
@@ -1087,6 +1090,8 @@ static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   // +3 %, config 3 75.6 -> 78.9 % (profiles/r01_notes.md)
   const char* skew = getenv("QG_SKEW_NS");
   a2.skew_ns = skew ? (unsigned)atoi(skew) : 4000u;
+  const char* grp = getenv("QG_GROUP");  // experiments: tile-row group of the raster
+  a2.group = grp ? atoi(grp) : 8;
   if (BAL) {  // remove the Q/2 bias of every digit extraction (mod p)
     const unsigned long long ktiles = (unsigned long long)((a.K + BK - 1) / BK);
     const unsigned long long nb = !MULTI ? 1ull : (FLUSH == 0 ? ktiles / a.kb_stages + 1 : ktiles + 1);

@@ -70,6 +70,7 @@ struct GemmArgs {
   uint32_t corr;        // balanced: (p - (#extractions * Q/2) mod p) mod p, added in the epilogue
   double redq_off2;     // balanced REDQ: sum_s (Q/2) Q^s + 2^52 (makes every signed digit an unsigned one)
   uint32_t redq_ybias;  // balanced REDQ: p ceil(Q/2 / p) - Q/2, so x + ybias = D (mod p) and >= 0
+  int group;            // tile raster: rows per group (0 = 8)
 };
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);

@@ -135,12 +135,30 @@ __device__ __forceinline__ void load_stage(double* sA, double* sB, const double*
 // digit d of an accumulator: floor(acc / Q^d) mod Q. acc + 2^(td+52) rounded
 // toward zero has ulp exactly Q^d (the planner keeps acc < 2^(td+52)), so
 // its low mantissa bits hold floor(acc / Q^d) with no rounding.
+// The flush's DADD as a volatile asm statement: ptxas keeps volatile asm in
+// source order, so the DADDs of a flushing row group stay behind the other
+// row groups' DMMAs of the same k-step (issued after them in the source)
+// instead of being hoisted right behind the group's own DMMAs, where the warp
+// would stall on their latency with DMMAs still to issue.
+__device__ __forceinline__ double dadd_rz_ordered(double a, double b) {
+  double r;
+  asm volatile("add.rz.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ double dadd_rn_ordered(double a, double b) {
+  double r;
+  asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t block_digit(double acc, double anchor, uint32_t qmask) {
 #ifdef QG_INT_DIGIT
   // integer-pipe variant: floor(acc / 2^td) from the IEEE fields; anchor's
   // exponent field is 1023 + td + 52, so its high word gives the shift base
   const int sh_base = (int)((unsigned)__double2hiint(anchor) >> 20) - 52 - 1023 + 1075;
   return digit_at(acc, sh_base, qmask);
+#elif defined(QG_ORDERED_FLUSH)
+  return (uint32_t)__double2loint(dadd_rz_ordered(acc, anchor)) & qmask;
 #else
   return (uint32_t)__double2loint(__dadd_rz(acc, anchor)) & qmask;
 #endif
@@ -153,7 +171,11 @@ __device__ __forceinline__ uint32_t block_digit(double acc, double anchor, uint3
 // are removed mod p in the epilogue (args.corr).
 template <bool BAL>
 __device__ __forceinline__ uint32_t block_digit_t(double acc, double anchor, uint32_t qmask) {
+#ifdef QG_ORDERED_FLUSH
+  if (BAL) return (uint32_t)__double2loint(dadd_rn_ordered(acc, anchor)) & qmask;
+#else
   if (BAL) return (uint32_t)__double2loint(__dadd_rn(acc, anchor)) & qmask;
+#endif
   return block_digit(acc, anchor, qmask);
 }
 

@@ -13,7 +13,7 @@ for f in qg_abi.cu qg_dot.cu qg_small.cu qg_pack.cu qg_word64.cu; do
   nvcc $flags -c -o $bld/$f.o $here/paper_0803_1975_b200/csrc/$f &
   objs="$objs $bld/$f.o"
 done
-for f in qg_plan.cpp qg_io.cpp qg_multi.cpp; do
+for f in qg_plan.cpp qg_io.cpp qg_multi.cpp qg_stage.cpp; do
   nvcc $flags -x cu -c -o $bld/$f.o $here/paper_0803_1975_b200/csrc/$f &
   objs="$objs $bld/$f.o"
 done

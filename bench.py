@@ -741,10 +741,14 @@ def our_arm(args):
         c = qg.uncompress(qg.CompressedMatrix(m_rank, n, m_rank, H, qg.PackOrientation(
             qg.PackDirection.Forward, qg.PackAxis.Column, pl.e), pl, cc_out))
     checksum = qg.residue_checksum(c[:m_rank]) if m_rank else 0
+    # config 5: the reference's golden row shards (tests/golden/golden.json,
+    # made by oracle/_ref) that fall in this rank's rows, sha256 of the bytes
+    golden_rows = golden_row_shards(args.config, c, row0, m_rank)
     if world > 1:
-        cs = torch.tensor([checksum], dtype=torch.int64, device=dev)
+        cs = torch.tensor([checksum, golden_rows[0], golden_rows[1]], dtype=torch.int64, device=dev)
         dist.all_reduce(cs)
-        checksum = int(cs.item()) & 0xFFFFFFFF
+        checksum = int(cs[0].item()) & 0xFFFFFFFF
+        golden_rows = (int(cs[1].item()), int(cs[2].item()))
 
     contract_avg = sum(contract_ms) / len(contract_ms)
     packed_flop = 2.0 * m_rank * n * K  # per step on this rank: packed words, not padding
@@ -787,6 +791,9 @@ def our_arm(args):
         "roofline": roofline,
         "gpu_launches": launches,
         "checksum_c": checksum,
+        "golden_row_shards": ({"checked": golden_rows[0], "match": golden_rows[1] == golden_rows[0],
+                               "source": "tests/golden/golden.json config5_rows (reference-made), all ranks"}
+                              if golden_rows[0] else None),
         "per_rank_ms": [round(x, 3) for x in per_rank_ms],
         "wall_s_timed_region": round(wall, 4),
     }
@@ -810,6 +817,26 @@ def our_arm(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def golden_row_shards(config, c, row0, rows):
+    """(shards checked, shards matching) of the reference's golden row shards
+    of `config` (sha256 of the residues as bytes) inside rows [row0, row0+rows)
+    of this rank's C."""
+    import hashlib
+
+    if config != "config5":
+        return (0, 0)
+    g = load_json(os.path.join(ROOT, "tests", "golden", "golden.json")) or {}
+    shards = g.get("configs", {}).get("config5_rows", {}).get("shards", [])
+    checked = match = 0
+    for sh in shards:
+        r0, nr = sh["row0"], sh["rows"]
+        if r0 >= row0 and r0 + nr <= row0 + rows:
+            blk = c[r0 - row0:r0 - row0 + nr].cpu().numpy().astype("uint8")
+            checked += 1
+            match += hashlib.sha256(blk.tobytes()).hexdigest() == sh["sha256_u8"]
+    return (checked, match)
 
 
 def e2e_measure(qg, gp, p, m, k, n, args, rank=0, world=1, device_c=None):

@@ -5,8 +5,9 @@ mkdir -p gpurun_out
 for c in config1 config2 config3 config4 config4_left config4_full; do
   python bench.py --config $c --steps 20 --warmup 5 --cpu-s 4 2>/dev/null | tail -1 > gpurun_out/bench_$c.json
 done
-python bench.py --config config5 --steps 3 --warmup 3 --cpu-s 4 --e2e-steps 2 2>/dev/null | tail -1 > gpurun_out/bench_config5.json
-for c in config1 config2 config3 config4 config4_left config4_full config5; do
+python bench.py --config config2 --output cc --steps 20 --warmup 5 --no-cpu 2>/dev/null | tail -1 > gpurun_out/bench_config2_cc.json
+python bench.py --config config5 --steps 20 --warmup 5 --cpu-s 4 2>/dev/null | tail -1 > gpurun_out/bench_config5.json
+for c in config1 config2 config2_cc config3 config4 config4_left config4_full config5; do
   python - "$c" <<'PY'
 import json, sys
 c = sys.argv[1]

@@ -1,4 +1,6 @@
-"""Randomised parity soak of the entry points added late in round 1, against
+"""Randomised parity soak of the entry points added late in round 1 (and the
+round-2 ones: the fused repack, the all-gather host entry, pinned host
+buffers next to pageable ones), against
 the oracle (oracle/qg_oracle.c, pinned to the reference): the small-product
 cluster kernel (forced on and off), the one-call device entry, the 2-D and
 k-split host pipelines (forced), the mixed / left host paths and the
@@ -49,7 +51,7 @@ def main():
         a = orc.random_residue_matrix(m, k, p, rng.randrange(1 << 30))
         b = orc.random_residue_matrix(k, n, p, rng.randrange(1 << 30))
         want = orc.naive_gemm(p, a, b)
-        kind = rng.choice(["device", "host", "right", "left", "multi"])
+        kind = rng.choice(["device", "host", "right", "left", "multi", "repack", "repack_host", "allgather"])
         try:
             gp = qg.plan_gpu(p, k, balanced=rng.random() < 0.6)
         except qg.Error:
@@ -91,6 +93,36 @@ def main():
                 for s in range(e):
                     digits[s::e, :] = (w >> np.uint64(t * s)) & np.uint64((1 << t) - 1)
                 got = digits[:m].astype(np.uint32)
+        elif kind in ("repack", "repack_host"):  # mul_common_repacked: CC words, unpacked here
+            os.environ["QG_SMALL"] = rng.choice(["0", "1", "auto"])
+            plan = gp if rng.random() < 0.7 else None
+            if plan is None:
+                try:
+                    plan = qg.plan_compression(p, k)
+                except qg.Error:
+                    continue
+            base = plan.plan if isinstance(plan, qg.GpuPlan) else plan
+            if kind == "repack":
+                w = qg.mul_common_repacked(torch.from_numpy(a.astype(np.float64)).cuda(),
+                                           torch.from_numpy(b.astype(np.float64)).cuda(), plan).data.cpu().numpy()
+            else:
+                w = qg.mul_common_repacked_host(a, b, plan)
+            w = w.astype(np.uint64)
+            e, t = base.e, base.t
+            digits = np.zeros((m, -(-n // e) * e), dtype=np.uint64)
+            for s in range(e):
+                digits[:, s::e] = (w >> np.uint64(t * s)) & np.uint64((1 << t) - 1)
+            got = digits[:, :n].astype(np.uint32)
+            desc += f" small={os.environ['QG_SMALL']} repack_plan={base}"
+        elif kind == "allgather":  # the multi-process host entry at world size 1
+            from paper_0803_1975_b200.dist import mul_common_allgather_host
+
+            if rng.random() < 0.5:  # pinned host buffers (the other half pageable)
+                ap_ = torch.from_numpy(a.view(np.int32)).pin_memory().numpy().view(np.uint32)
+                bp_ = torch.from_numpy(b.view(np.int32)).pin_memory().numpy().view(np.uint32)
+                a, b = ap_, bp_
+                desc += " pinned"
+            got = mul_common_allgather_host(a, b, gp, 0, 1)
         else:
             got = qg.mul_common_multi_host(a, b, gp, list(range(torch.cuda.device_count())))
         n_cases += 1

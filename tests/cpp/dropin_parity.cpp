@@ -252,6 +252,33 @@ void backend_suite(const char* name, int beta) {
     return rm(c) + (c == naive_gemm(ab, bb, m7) ? " ==naive" : " !=naive");
   });
   show("blocked_accumulate kpanel 0", [&] { return rm(blocked_accumulate<B>(a, b, pl, 0)); });
+
+  // empty and degenerate shapes (value semantics must hold at the edges)
+  const ResidueMatrix e0(0, 53), e1(53, 0), e2(0, 0);
+  show("compress_rows_reversed 0 rows", [&] { return cm(compress_rows_reversed<B>(e0, pl)); });
+  show("compress_cols_forward 0 cols", [&] { return cm(compress_cols_forward<B>(e1, pl)); });
+  show("mul_common_compressed 0 x 53 x 29", [&] { return rm(mul_common_compressed<B>(e0, b, pl)); });
+  show("mul_common_compressed 37 x 53 x 0", [&] { return rm(mul_common_compressed<B>(a, e1, pl)); });
+  show("packed_common_product empty", [&] {
+    return words(packed_common_product(compress_rows_reversed<B>(e0, pl), compress_cols_forward<B>(b, pl)));
+  });
+  show("mul_right_compressed 0 rows", [&] { return cm(mul_right_compressed(ResidueMatrix(0, 64), cbo)); });
+  show("uncompress empty", [&] { return rm(uncompress(compress_outer_cols<B>(e2, pr))); });
+  show("mul_common_repacked 0 x 53", [&] { return cm(mul_common_repacked<B>(e0, b, pl)); });
+  show("k = 1 uncompressed plan", [&] {
+    const ResidueMatrix a1 = random_residue_matrix(9, 1, m3, 17), b1 = random_residue_matrix(1, 11, m3, 18);
+    return rm(mul_common_compressed<B>(a1, b1, uncompressed_plan(m3, 1, beta)));
+  });
+  show("one row, one column", [&] {
+    const ResidueMatrix a1 = random_residue_matrix(1, 40, m7, 19), b1 = random_residue_matrix(40, 1, m7, 20);
+    return rm(mul_common_compressed<B>(a1, b1, plan_compression(m7, 40, beta)));
+  });
+  show("ragged k (k % e != 0)", [&] {
+    const ResidueMatrix a1 = random_residue_matrix(13, 41, m5, 21), b1 = random_residue_matrix(41, 17, m5, 22);
+    const auto p41 = plan_compression(m5, 41, beta);
+    return rm(mul_common_compressed(compress_rows_reversed<B>(a1, p41), compress_cols_forward<B>(b1, p41))) +
+           " e=" + std::to_string(p41.e);
+  });
   show("blocked_accumulate kpanel>kmax", [&] { return rm(blocked_accumulate<B>(a, b, pl, pl.kmax + 1)); });
 }
 

@@ -145,3 +145,62 @@ def test_mul_right_compressed_compressed_left(qg, orc, cuda, p, m, k, n):
     assert np.array_equal(qg.uncompress(cc).cpu().numpy().astype(np.uint32), orc.naive_gemm(p, a, b))
     with pytest.raises(qg.PlanMismatch):
         qg.mul_right_compressed(qg.compress_rows_reversed(ad, plan), cbo)
+
+
+# ------------------------------------------------------------ reference-layout left product, digit extraction
+@pytest.mark.parametrize("p,m,k,n", [(7, 30, 40, 17), (3, 129, 500, 64), (5, 8, 1, 3)])
+@pytest.mark.parametrize("dtype", ["f64", "u32"])
+def test_left_product_reference_layout(qg, orc, cuda, p, m, k, n, dtype):
+    """qg_packed_left_product / qg_mul_left (gemm.hpp:340-371) on
+    compress_outer_rows words: the REDQ'd words equal the oracle's
+    mul_left_compressed bit for bit; the raw words unpack to the unreduced
+    digits (the dot products)."""
+    import torch
+
+    plan = qg.plan_packed_axis(p, k, m)
+    a = orc.random_residue_matrix(m, k, p, 7)
+    b = orc.random_residue_matrix(k, n, p, 8)
+    ca = qg.compress_outer_rows(torch.from_numpy(a.astype(np.float64)).to(cuda), plan)
+    bd = torch.from_numpy(b.astype(np.float64) if dtype == "f64" else b.view(np.int32)).to(cuda)
+    code = 0 if dtype == "f64" else 1
+    G = -(-m // plan.e)
+    pl = plan._c()
+    cc = torch.empty((G, n), dtype=torch.float64, device=cuda)
+    qg._check(qg.lib.qg_mul_left(ctypes.byref(pl), qg._ptr(ca.data), k, qg._ptr(bd), code, n, m, k, n, qg._ptr(cc),
+                                 qg._stream()))
+    want = orc.mul_left_compressed(orc.plan_of(plan), a, b)
+    assert np.array_equal(bits(cc.cpu().numpy()), bits(want))
+    raw = torch.empty((G, n), dtype=torch.float64, device=cuda)
+    qg._check(qg.lib.qg_packed_left_product(ctypes.byref(pl), qg._ptr(ca.data), k, qg._ptr(bd), code, n, m, k, n,
+                                            qg._ptr(raw), qg._stream()))
+    w = raw.cpu().numpy().astype(np.uint64)
+    dots = (a.astype(np.int64) @ b.astype(np.int64))
+    for s in range(plan.e):
+        rows = np.arange(s, m, plan.e)
+        got = (w[:len(rows)] >> np.uint64(plan.t * s)) & np.uint64((1 << plan.t) - 1)
+        assert np.array_equal(got.astype(np.int64), dots[rows])
+
+
+@pytest.mark.parametrize("u64", [False, True])
+def test_extract_digits(qg, cuda, u64):
+    """extract_all (pack.hpp:104-119) on the device: every base-Q digit of each
+    word, unreduced; a word >= Q^e (or negative) is DigitOverflow."""
+    import torch
+
+    plan = qg.make_plan(3, 5, 3)
+    vals = [0, 1, 31, 32, 33, 2081, 2048 + 32, 32767]
+    dt = torch.int64 if u64 else torch.float64
+    w = torch.tensor(vals, dtype=dt, device=cuda)
+    out = torch.zeros(len(vals) * 3, dtype=torch.int64, device=cuda)
+    pl = plan._c()
+    fn = qg.lib.qg_extract_digits_u64 if u64 else qg.lib.qg_extract_digits
+    qg._check(fn(ctypes.byref(pl), qg._ptr(w), len(vals), qg._ptr(out), qg._stream()))
+    got = out.view(-1, 3).cpu().tolist()
+    assert got == [[(v >> (5 * s)) & 31 for s in range(3)] for v in vals]
+    bad = torch.tensor([32768], dtype=dt, device=cuda)
+    with pytest.raises(qg.DigitOverflow):
+        qg._check(fn(ctypes.byref(pl), qg._ptr(bad), 1, qg._ptr(out), qg._stream()))
+    if not u64:
+        neg = torch.tensor([-1.0], dtype=dt, device=cuda)
+        with pytest.raises(qg.DigitOverflow):
+            qg._check(fn(ctypes.byref(pl), qg._ptr(neg), 1, qg._ptr(out), qg._stream()))

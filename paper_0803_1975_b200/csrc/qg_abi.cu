@@ -1315,15 +1315,17 @@ static int host_pipeline2d(
   // column panels (whole multiples of col_align columns; one col_align block =
   // out_tiles_per_block 128-wide output tile columns)
   const size_t col_blocks = ceil_div(n, col_align);
-  // up to 8 panels of >= 16 tile columns (config 5: 8 panels, 402 -> 393 ms e2e)
+  // up to 16 panels of >= 16 tile columns (config 5: 4 / 8 / 16 / 32 panels at
+  // two waves of tiles per launch: 403 / 390 / 389 / 389 ms e2e, tools/e2e_c5_sweep.py)
   size_t want_p = col_blocks * out_tiles_per_block / 16;
-  want_p = want_p < 2 ? 2 : (want_p > 8 ? 8 : want_p);
+  want_p = want_p < 2 ? 2 : (want_p > 16 ? 16 : want_p);
   if (const char* e = getenv("QG_HOST_PANELS")) want_p = (size_t)atoi(e);  // experiments
   const size_t npanels = col_blocks < want_p ? (col_blocks ? col_blocks : 1) : (want_p ? want_p : 1);
   const size_t blocks_per = ceil_div(col_blocks, npanels);
-  // row chunks large enough that one tile launch has ~96 output tiles of
-  // 128 x 128 (a tile launch on a few SMs would leave the GPU idle)
-  size_t want_tiles = 96;
+  // row chunks large enough that one tile launch has ~two waves of 128 x 128
+  // output tiles (a tile launch on a few SMs would leave the GPU idle; config 5:
+  // 96 / 148 / 296 / 444 tiles per launch at 16 panels: 395 / 389 / 389 / 391 ms)
+  size_t want_tiles = 2 * (size_t)device_sms();
   if (const char* e = getenv("QG_HOST_TILES")) want_tiles = (size_t)atoi(e);  // experiments
   const size_t tc = blocks_per * out_tiles_per_block;
   size_t rows_per = ceil_div(want_tiles, tc ? tc : 1) * 128;

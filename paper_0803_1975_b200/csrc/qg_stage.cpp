@@ -2,7 +2,6 @@
 // host paths (see qg_stage.h).
 #include "qg_stage.h"
 
-#include <atomic>
 #include <cstring>
 #include <functional>
 
@@ -34,8 +33,10 @@ class CopyPool {
       rows2d(dst, dpitch, src, spitch, width, 0, rows, rows);
       return;
     }
-    // split by rows when there are enough, else split a single row by bytes
-    std::atomic<int> left{parts};
+    // split by rows when there are enough, else split a single row by bytes;
+    // `left` is decremented under `m` so the waiter cannot return (and destroy
+    // m / done) before the last worker has released them
+    int left = parts;
     std::mutex m;
     std::condition_variable done;
     for (int i = 0; i < parts; ++i) {
@@ -48,14 +49,12 @@ class CopyPool {
             std::memcpy(dst + r * dpitch + b0, src + r * spitch + b0, b1 - b0);
           }
         }
-        if (left.fetch_sub(1) == 1) {
-          std::lock_guard<std::mutex> lk(m);
-          done.notify_all();
-        }
+        std::lock_guard<std::mutex> lk(m);
+        if (--left == 0) done.notify_all();
       });
     }
     std::unique_lock<std::mutex> lk(m);
-    done.wait(lk, [&] { return left.load() == 0; });
+    done.wait(lk, [&] { return left == 0; });
   }
 
  private:

@@ -482,6 +482,11 @@ int qg_read_matrix_file(const char* path, uint32_t* p, size_t* rows, size_t* col
 int qg_write_matrix_file(const char* path, uint32_t p, const uint32_t* data, size_t rows, size_t cols);
 void qg_free(void* ptr);
 
+/* Tile schedule of the tiled contraction kernels: 1 = tiles claimed from an
+ * atomic counter (a CTA that starts late, its SM held by another kernel such
+ * as an NCCL all-gather, takes fewer tiles), 0 = static round robin. Process-wide. */
+void qg_set_dynamic_tiles(int enable);
+
 /* ------------------------------------------------------------ diagnostics */
 /* qg_last_error(): description of the last failure on this thread (CUDA
  * error string, or the parse error text of a matrix file). */

@@ -248,6 +248,7 @@ def _load():
         "qg_copy_to_host": ([vp, vp, sz], i32),
         "qg_host_pack_b_slot_tiled": ([P(_GpuPlan), u32, vp, sz, sz, sz, sz, vp, vp], i32),
         "qg_host_mul_common_packed_b": ([P(_GpuPlan), vp, sz, sz, vp, sz, vp, vp], i32),
+        "qg_set_dynamic_tiles": ([i32], None),
         "qg_kernel_launches": ([], u64),
         "qg_last_kernel": ([], ctypes.c_char_p),
         "qg_last_error": ([], ctypes.c_char_p),

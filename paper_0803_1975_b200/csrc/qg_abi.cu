@@ -768,6 +768,7 @@ int qg_mul_common_compressed(const qg_gpu_plan* gplan, const void* a, size_t lda
 
 
 uint64_t qg_kernel_launches(void) { return qgk::g_launches.load(); }
+void qg_set_dynamic_tiles(int enable) { qgk::set_dynamic_tiles(enable); }
 const char* qg_last_error(void) {
   const std::string& m = qg::last_message();
   return m.empty() ? cudaGetErrorString(g_last_cuda_error) : m.c_str();
@@ -1318,7 +1319,9 @@ static int host_pipeline2d(
   // up to 16 panels of >= 16 tile columns (config 5: 4 / 8 / 16 / 32 panels at
   // two waves of tiles per launch: 403 / 390 / 389 / 389 ms e2e, tools/e2e_c5_sweep.py)
   size_t want_p = col_blocks * out_tiles_per_block / 16;
-  want_p = want_p < 2 ? 2 : (want_p > 16 ? 16 : want_p);
+  // (pageable B: at most 8 — its panels are staged row by row on the host)
+  const size_t max_p = qg::host_pinned(b) ? 16 : 8;
+  want_p = want_p < 2 ? 2 : (want_p > max_p ? max_p : want_p);
   if (const char* e = getenv("QG_HOST_PANELS")) want_p = (size_t)atoi(e);  // experiments
   const size_t npanels = col_blocks < want_p ? (col_blocks ? col_blocks : 1) : (want_p ? want_p : 1);
   const size_t blocks_per = ceil_div(col_blocks, npanels);

@@ -23,8 +23,11 @@
 // K5 (mixed / right variant, gemm.hpp:285-325): plain exact DGEMM of residues
 // by forward-packed words (every partial sum < Q^e < 2^53) with a fused REDQ
 // epilogue (pack.hpp:124-137).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "qg_kernels.h"
 #include "qg_device.cuh"
@@ -38,6 +41,7 @@ constexpr int NT = (BM / WM) * (BN / WN) * 32;  // 256 threads
 constexpr int MI = WM / 8, NI = WN / 8;
 constexpr int B_ST = BN + 4;  // 132 words = 1056 B = 32 mod 128: conflict-free B fragments
 constexpr int SMEM_BUDGET = 220 * 1024;
+constexpr bool kDynamicDefault = false;  // tiled kernels: dynamic tile schedule by default
 
 // Stage geometry for a stage depth of BK words. The A row stride is the
 // smallest s >= BK with s = 4 or 12 (mod 16) words: rows g = 0..3 of a
@@ -538,7 +542,7 @@ struct SplitFlush {
 template <int BK, int EPI, bool MULTI, int MID, bool TILED, bool PACK = false, bool SPLIT = false, bool BAL = false>
 __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint64_t* full, uint64_t* empty,
                                         int tiles_m, int tiles_n, int my_tiles, int ktiles, bool nomem,
-                                        uint8_t* repack = nullptr) {
+                                        uint8_t* repack = nullptr, const volatile int* tile_of = nullptr) {
   using G = Geo<BK>;
   using GT = GeoT<BK, epi_reserve<EPI>()>;
   constexpr int S = TILED ? GT::STAGES : G::STAGES;
@@ -561,9 +565,22 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
   uint32_t slot = 0, phase = 0;
   int nflush = 0;
   if (warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise SMSP warp pairs
-  for (int ts = 0; ts < my_tiles; ++ts) {
+  // dynamic schedule (tile_of != nullptr): the producer claims tiles from a
+  // global counter and posts each tile's index beside its first stage; a
+  // negative index ends the loop
+  const bool dyn = TILED && tile_of != nullptr && !nomem;
+  for (int ts = 0;; ++ts) {
+    int tile;
+    if (dyn) {
+      mbar_wait(full + slot, phase);  // the tile's first stage (and its index) has landed
+      tile = tile_of[slot];
+      if (tile < 0) break;
+    } else {
+      if (ts >= my_tiles) break;
+      tile = blockIdx.x + ts * gridDim.x;
+    }
     int tm, tn;
-    tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, args.group, tm, tn);
+    tile_coords(tile, tiles_m, tiles_n, args.group, tm, tn);
     const int m0 = tm * BM, n0 = tn * BN;
     if (EPI != EPI_DIGIT && args.accumulate) {
       // continue from the words already in CC (a k-split host product: the
@@ -581,7 +598,7 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
     }
     int kst = 0;
     for (int kt = 0; kt < ktiles; ++kt) {
-      if (!nomem) mbar_wait(full + slot, phase);
+      if (!nomem && !(dyn && kt == 0)) mbar_wait(full + slot, phase);
       const double* sA = smem + slot * STAGE;
       const double* sB = sA + A_TILE;
       const double* a_base = sA + (warp_m * WM + g) * AST + t;
@@ -892,20 +909,38 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int t
   const int my_tiles = blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const bool nomem = args.debug & 1;
 
-  uint8_t* repack = reinterpret_cast<uint8_t*>(empty + S);  // EPI_REPACK staging (after the barriers)
+  // dynamic tile schedule (args.tile_counter): index of the tile whose first
+  // stage sits in each ring slot, written by the producer before it arms the
+  // slot's `full` barrier (whose completion orders it for the consumers)
+  volatile int* tile_of = reinterpret_cast<volatile int*>(empty + S);
+  const bool dyn = args.tile_counter != nullptr && !nomem;
+  uint8_t* repack = reinterpret_cast<uint8_t*>(empty + S + 4);  // EPI_REPACK staging (after barriers + tile_of)
 
   if (warp >= NWARPS) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (nomem || warp != NWARPS || lane != 0) return;
     uint32_t slot = 0, phase = 0;
-    for (int ts = 0; ts < my_tiles; ++ts) {
+    for (int ts = 0;; ++ts) {
+      // static: every gridDim.x-th tile; dynamic: claimed from the counter, so
+      // a CTA that starts late (SMs held by another kernel, e.g. an NCCL
+      // all-gather) simply takes fewer tiles
+      const int tile = dyn ? atomicAdd(args.tile_counter, 1) : blockIdx.x + ts * gridDim.x;
+      if (tile >= total_tiles) {
+        if (dyn) {  // post the end marker in the next slot
+          mbar_wait(empty + slot, phase ^ 1);
+          tile_of[slot] = -1;
+          mbar_arrive(full + slot);
+        }
+        break;
+      }
       int tm, tn;
-      tile_coords(blockIdx.x + ts * gridDim.x, tiles_m, tiles_n, args.group, tm, tn);
+      tile_coords(tile, tiles_m, tiles_n, args.group, tm, tn);
       const double* ablk = args.a + (size_t)tm * ktiles * BM * BK;
       const double* bblk = args.b + (size_t)tn * ktiles * BM * BK;
       for (int kt = 0; kt < ktiles; ++kt) {
         mbar_wait(empty + slot, phase ^ 1);
         double* sA = smem + slot * GT::STAGE;
+        if (dyn && kt == 0) tile_of[slot] = tile;
         mbar_arrive_expect_tx(full + slot, 2 * CHUNK);
         bulk_g2s(sA, ablk + (size_t)kt * BM * BK, CHUNK, full + slot);
         bulk_g2s(sA + GT::A_TILE, bblk + (size_t)kt * BM * BK, CHUNK, full + slot);
@@ -922,15 +957,15 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_tiled(GemmArgs args, int t
   // 1 = staggered (warps 4..7 cut mid-stage; two inlined consumer bodies, so
   // instantiated separately) and 2 = fused into the next stage's first k-step.
   if (FLUSH == 3)  // split phases: odd accumulator rows flush mid-stage, even rows at stage ends
-    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, false, true, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, false, true, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack, dyn ? tile_of : nullptr);
   else if (FLUSH == 2)  // fused flush with packed digit sums (t <= 16)
-    consume<BK, EPI, MULTI, -1, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
+    consume<BK, EPI, MULTI, -1, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack, dyn ? tile_of : nullptr);
   else if (FLUSH == 1 && warp >= 4)
-    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
+    consume<BK, EPI, MULTI, (BK / 8 >= 1 ? BK / 8 : 1), true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack, dyn ? tile_of : nullptr);
   else if (FLUSH == 1)
-    consume<BK, EPI, MULTI, 0, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
+    consume<BK, EPI, MULTI, 0, true, true, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack, dyn ? tile_of : nullptr);
   else
-    consume<BK, EPI, MULTI, 0, true, false, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack);
+    consume<BK, EPI, MULTI, 0, true, false, false, BAL>(args, smem, full, empty, tiles_m, tiles_n, my_tiles, ktiles, nomem, repack, dyn ? tile_of : nullptr);
 }
 
 // Reference-semantics contraction (DoubleWord::high_part, word.hpp:28-30):
@@ -1094,11 +1129,43 @@ static cudaError_t launch_digit_bulk(const GemmArgs& a, int bk, cudaStream_t s) 
 }
 
 static int num_sms();
+// A zeroed tile counter for one launch of the dynamically scheduled tiled
+// kernel: a slot of a per-device pool (4096 launches in flight at most),
+// cleared by a memset on the launch's stream (a graph node when captured).
+static int* tile_counter(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<int, int*> pools;
+  static std::atomic<unsigned> next{0};
+  constexpr unsigned kSlots = 4096;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  int* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    int*& p = pools[dev];
+    if (!p && cudaMalloc(&p, kSlots * sizeof(int)) != cudaSuccess) p = nullptr;
+    base = p;
+  }
+  if (!base) return nullptr;
+  int* c = base + (next.fetch_add(1) % kSlots);
+  return cudaMemsetAsync(c, 0, sizeof(int), s) == cudaSuccess ? c : nullptr;
+}
+
+// Dynamic tile schedule for the tiled kernels: QG_DYN=0/1 (experiments),
+// default from qg_set_dynamic_tiles.
+static std::atomic<int> g_dynamic_tiles{-1};
+void set_dynamic_tiles(int enable) { g_dynamic_tiles.store(enable ? 1 : 0); }
+static bool dynamic_tiles() {
+  if (const char* e = getenv("QG_DYN")) return e[0] != '0';
+  const int v = g_dynamic_tiles.load();
+  return v < 0 ? kDynamicDefault : v != 0;
+}
+
 template <int BK, int EPI, bool MULTI, int FLUSH, bool BAL>
 static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   using GT = GeoT<BK, epi_reserve<EPI>()>;
   auto k = k_gemm_tiled<BK, EPI, MULTI, FLUSH, BAL>;
-  const size_t smem = GT::SMEM + 2 * GT::STAGES * sizeof(uint64_t) + epi_reserve<EPI>();
+  const size_t smem = GT::SMEM + (2 * GT::STAGES + 4) * sizeof(uint64_t) + epi_reserve<EPI>();
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err) return err;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
@@ -1114,6 +1181,11 @@ static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   a2.skew_ns = skew ? (unsigned)atoi(skew) : 4000u;
   const char* grp = getenv("QG_GROUP");  // experiments: tile-row group of the raster
   a2.group = grp ? atoi(grp) : 8;
+  a2.tile_counter = nullptr;
+  if (dynamic_tiles() && !(a2.debug & 1)) {
+    a2.tile_counter = tile_counter(s);
+    if (!a2.tile_counter) return cudaErrorMemoryAllocation;
+  }
   if (BAL) {  // remove the Q/2 bias of every digit extraction (mod p)
     const unsigned long long ktiles = (unsigned long long)((a.K + BK - 1) / BK);
     const unsigned long long nb = !MULTI ? 1ull : (FLUSH == 0 ? ktiles / a.kb_stages + 1 : ktiles + 1);

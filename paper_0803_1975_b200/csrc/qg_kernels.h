@@ -71,11 +71,15 @@ struct GemmArgs {
   double redq_off2;     // balanced REDQ: sum_s (Q/2) Q^s + 2^52 (makes every signed digit an unsigned one)
   uint32_t redq_ybias;  // balanced REDQ: p ceil(Q/2 / p) - Q/2, so x + ybias = D (mod p) and >= 0
   int group;            // tile raster: rows per group (0 = 8)
+  int* tile_counter;    // tiled kernels: dynamic tile schedule from this zeroed counter (NULL = static)
 };
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
 // Same contraction on the tiled layout (a = CA_t, b = CB_t; lda/ldb unused).
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
+// Tiled kernels: claim tiles dynamically from an atomic counter (on) or
+// statically every gridDim.x-th tile (off); QG_DYN overrides.
+void set_dynamic_tiles(int enable);
 // The same with ReduceAndCompress fused into the epilogue (p < 256): CC words
 // (a.cc, a.ldcc) = C's rows packed forward in groups of a.e under Q = 2^a.t.
 // Words that straddle 32-column warp segments are accumulated with atomics:

@@ -593,9 +593,14 @@ def our_arm(args):
             dist.init_process_group(args.dist_backend)
 
     p, m, k, n, desc = CONFIGS[args.config]
-    gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
+    # --output cc runs K4R (ReduceAndCompress epilogue), which has no anchored variant yet
+    gp = (qg.plan_gpu(p, k, anchored=args.output != "cc") if args.plan == "gpu"
+          else qg.gpu_plan_from(qg.plan_compression(p, k), k))
     if args.kblock:  # experiments: override the k-block of the chosen plan
-        gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words, gp.balanced)
+        gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words, gp.balanced,
+                        gp.anchored if args.anchored < 0 else args.anchored)
+    elif args.anchored >= 0:
+        gp = qg.GpuPlan(gp.plan, gp.kblock_words, gp.max_exact_words, gp.balanced, args.anchored)
     pl = gp.plan
     K = -(-k // pl.e)
     row0, m_rank = shard_rows_aligned(m, world, rank)
@@ -779,7 +784,7 @@ def our_arm(args):
         "data": "synthetic (SplitMix64 seeds 42/43, uniform residues, generated on device)",
         "config": {"workload": desc + ("; output CC = mul_common_repacked (ReduceAndCompress fused)" if repacked else ""),
                    "p": p, "m": m, "k": k, "n": n,
-                   "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk,
+                   "plan": {"t": pl.t, "e": pl.e, "kblock_words": gp.kblock_words, "stage_words": bk, "anchored": bool(gp.anchored),
                             "balanced": bool(gp.balanced), "source": args.plan},
                    "layout": "tiled packed operands (128 x stage_words blocks, CB transposed)" + (
                        "; contraction on 64x64 tiles with k split over a thread-block cluster"
@@ -933,6 +938,8 @@ def make_parser():
     ap.add_argument("--plan", default="gpu", choices=["gpu", "reference"],
                     help="gpu: planner-chosen (t, e, kblock); reference: plan_compression's plan")
     ap.add_argument("--kblock", type=int, default=0, help="override the plan's k-block (words)")
+    ap.add_argument("--anchored", type=int, default=-1,
+                    help="experiments: force the plan's anchored flag (K4A) on (1) / off (0)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path with several ranks on one GPU")
     ap.add_argument("--pageable", type=int, default=1, help="also time e2e from pageable host buffers (N=1)")

@@ -78,7 +78,14 @@ typedef struct {
    * read by rounding to nearest. Twice the exact block of
    * the unsigned packing at the same (t, e). Tiled path only. */
   int32_t balanced;
-  int32_t reserved;
+  /* 1 (balanced plans, tiled path): anchored accumulation —
+   * every k-block starts from the anchor 1.5*2^E inside the DMMA chain, so the
+   * block's digit is read from fixed bits of the accumulator on the integer
+   * pipe instead of by one FP64 add per accumulator. kblock_words is then
+   * bounded by qg_max_exact_block_anchored and is an odd multiple of 4. Any
+   * entry without an anchored kernel runs the same blocks with the FP64 flush
+   * (an anchored block is always within Eq. G). */
+  int32_t anchored;
 } qg_gpu_plan;
 
 /* PackOrientation, matrix.hpp:28-39: direction 0 Forward / 1 Reversed;
@@ -116,10 +123,17 @@ int qg_gpu_plan_from(const qg_plan* plan, uint64_t k, qg_gpu_plan* out);
 int qg_plan_gpu(uint32_t p, uint64_t k, qg_gpu_plan* out);
 /* qg_plan_gpu with flags: QG_PLAN_UNSIGNED_ONLY restricts to unsigned digits
  * (words bit-compatible with the reference packing, for the row layouts). */
-enum { QG_PLAN_UNSIGNED_ONLY = 1 };
+enum { QG_PLAN_UNSIGNED_ONLY = 1, QG_PLAN_NO_ANCHOR = 2 };
 int qg_plan_gpu_ex(uint32_t p, uint64_t k, int flags, qg_gpu_plan* out);
 /* Eq. G bound for balanced digits (qg_gpu_plan.balanced = 1). */
 int qg_max_exact_block_balanced(const qg_plan* plan, uint64_t* words);
+/* Largest k-block (words) of the anchored accumulation for (p, t, e): every
+ * partial sum of a block stays in one binade [2^E, 2^(E+1)) and Eq. G holds
+ * with the fixed ulp 2^(E-52). *exponent (may be NULL) gets
+ * the E of that block, 0 if no block is exact. */
+int qg_max_exact_block_anchored(const qg_plan* plan, uint64_t* words, int* exponent);
+/* qg_plan_gpu_ex flag: consider anchored plans too (the default planner does
+ * once QG_PLAN_ANCHORED is set; the planner picks by predicted time). */
 /* Eq. 3 bound (residues per k-block) that the contraction enforces for a GPU
  * plan, recomputed from (p, t): largest_common_dim (plan.hpp:113-115), capped
  * by a smaller plan.kmax, for unsigned plans; the balanced-digit bound

@@ -1157,6 +1157,7 @@ struct GpuPlan {
   std::uint64_t kblock_words = 0;
   std::uint64_t max_exact_words = 0;
   bool balanced = false;
+  bool anchored = false;  // anchored accumulation (integer-pipe block flush)
 };
 namespace detail {
 inline qg_gpu_plan to_c(const GpuPlan& g) {
@@ -1165,13 +1166,15 @@ inline qg_gpu_plan to_c(const GpuPlan& g) {
   c.kblock_words = g.kblock_words;
   c.max_exact_words = g.max_exact_words;
   c.balanced = g.balanced ? 1 : 0;
+  c.anchored = g.anchored ? 1 : 0;
   return c;
 }
 }  // namespace detail
-inline GpuPlan plan_gpu(const PrimeModulus& m, std::uint64_t k) {
+// flags: QG_PLAN_UNSIGNED_ONLY, QG_PLAN_NO_ANCHOR (qg_plan_gpu_ex)
+inline GpuPlan plan_gpu(const PrimeModulus& m, std::uint64_t k, int flags = 0) {
   qg_gpu_plan c{};
-  detail::check(qg_plan_gpu(m.value(), k, &c), "plan_gpu");
-  return GpuPlan{detail::from_c(c.plan), c.kblock_words, c.max_exact_words, c.balanced != 0};
+  detail::check(qg_plan_gpu_ex(m.value(), k, flags, &c), "plan_gpu");
+  return GpuPlan{detail::from_c(c.plan), c.kblock_words, c.max_exact_words, c.balanced != 0, c.anchored != 0};
 }
 // mul_common_compressed(A, B) under a GPU plan (k-blocked on the device).
 inline ResidueMatrix mul_common_compressed(const ResidueMatrix& a, const ResidueMatrix& b, const GpuPlan& plan) {

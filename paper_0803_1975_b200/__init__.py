@@ -123,7 +123,7 @@ class _Plan(ctypes.Structure):
 
 class _GpuPlan(ctypes.Structure):
     _fields_ = [("plan", _Plan), ("kblock_words", ctypes.c_uint64), ("max_exact_words", ctypes.c_uint64),
-                ("balanced", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("balanced", ctypes.c_int32), ("anchored", ctypes.c_int32)]
 
 
 class _FullPlan(ctypes.Structure):
@@ -157,6 +157,7 @@ def _load():
         "qg_plan_gpu_ex": ([u32, u64, i32, P(_GpuPlan)], i32),
         "qg_max_exact_block_balanced": ([P(_Plan), P(u64)], i32),
         "qg_gpu_plan_kmax": ([P(_GpuPlan), P(u64)], i32),
+        "qg_max_exact_block_anchored": ([P(_Plan), P(u64), P(i32)], i32),
         "qg_gen_residues": ([u64, u32, sz, sz, sz, vp, i32, vp], i32),
         "qg_compress_rows_reversed": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
         "qg_compress_cols_forward": ([P(_Plan), vp, i32, sz, sz, sz, vp, sz, vp], i32),
@@ -326,13 +327,14 @@ class GpuPlan:
     kblock_words: int
     max_exact_words: int
     balanced: int = 0
+    anchored: int = 0
 
     def _c(self) -> _GpuPlan:
-        return _GpuPlan(self.plan._c(), self.kblock_words, self.max_exact_words, self.balanced, 0)
+        return _GpuPlan(self.plan._c(), self.kblock_words, self.max_exact_words, self.balanced, self.anchored)
 
     @staticmethod
     def _from(c: "_GpuPlan") -> "GpuPlan":
-        return GpuPlan(CompressionPlan._from(c.plan), c.kblock_words, c.max_exact_words, c.balanced)
+        return GpuPlan(CompressionPlan._from(c.plan), c.kblock_words, c.max_exact_words, c.balanced, c.anchored)
 
     def eq3_kmax(self) -> int:
         """Residues a k-block may hold (Eq. 3) for this plan's digits
@@ -391,12 +393,23 @@ def gpu_plan_from(plan: CompressionPlan, k: int) -> GpuPlan:
     return GpuPlan._from(out)
 
 
-def plan_gpu(p: int, k: int, balanced: bool = True) -> GpuPlan:
-    """(t, e, k-block[, balanced digits]) for the tensor-core path; balanced=False
-    restricts to the reference's unsigned packing."""
+def plan_gpu(p: int, k: int, balanced: bool = True, anchored: bool = True) -> GpuPlan:
+    """(t, e, k-block[, balanced digits][, anchored accumulation]) for the
+    tensor-core path; balanced=False restricts to the reference's unsigned
+    packing, anchored=False to the FP64-add block flush (K4)."""
     out = _GpuPlan()
-    _check(lib.qg_plan_gpu_ex(p, k, 0 if balanced else 1, ctypes.byref(out)))
+    _check(lib.qg_plan_gpu_ex(p, k, (0 if balanced else 1) | (0 if anchored else 2), ctypes.byref(out)))
     return GpuPlan._from(out)
+
+
+def max_exact_block_anchored(plan: CompressionPlan):
+    """(words, E): the largest k-block of the anchored accumulation (DESIGN.md
+    §3g) and the binade exponent its anchor uses; (0, 0) if none is exact."""
+    out = ctypes.c_uint64()
+    ex = ctypes.c_int()
+    pl = plan._c()
+    _check(lib.qg_max_exact_block_anchored(ctypes.byref(pl), ctypes.byref(out), ctypes.byref(ex)))
+    return out.value, ex.value
 
 
 def max_exact_block_balanced(plan: CompressionPlan) -> int:

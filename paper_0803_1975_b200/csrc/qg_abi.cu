@@ -26,6 +26,9 @@ uint64_t stage_block_tiled(uint64_t limit, int* bk);
 uint64_t stage_block_redq(uint64_t limit, int* bk);
 int stage_single(uint64_t K);
 uint64_t max_exact_block_balanced(uint32_t p, int t, int e);
+uint64_t max_exact_block_anchored(uint32_t p, int t, int e);
+int anchored_exponent(uint32_t p, int t, int e, uint64_t kb);
+int anchored_stage(uint64_t kb);
 uint64_t largest_common_dim(uint32_t p, int t);
 uint64_t largest_common_dim_balanced(uint32_t p, int t);
 }  // namespace qg
@@ -196,6 +199,14 @@ int tiled_geometry(const qg_gpu_plan* gp, uint64_t K, int* bk, int* kb_stages) {
                                       : qg::max_exact_block(pl.p, pl.t, pl.e);
   const uint64_t kb = gp->kblock_words < K ? gp->kblock_words : K;
   if (kb > exact) return QG_NOT_EXACT;  // a block past Eq. G: refused, never clamped silently
+  if (gp->anchored && gp->balanced && kb < K) {  // anchored plan: blocks of exactly kb words = the stage depth
+    if (!qg::anchored_exponent(pl.p, pl.t, pl.e, kb)) return QG_NOT_EXACT;
+    const int b = qg::anchored_stage(kb);
+    if (!b) return QG_INVALID_ARGUMENT;
+    *bk = b;
+    *kb_stages = 1;
+    return QG_OK;
+  }
   if (kb >= K) {
     const char* e = getenv("QG_TILED_SINGLE_BK");  // experiments
     *bk = e ? atoi(e) : qg::stage_single(K);
@@ -614,6 +625,17 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   }
   // digit sums are uint32 (planner keeps nblocks * (Q-1) < 2^32); the fused
   // flush packs two per register as 16-bit lanes, reduced mod p in time
+  if (gplan->anchored && a.balanced && kb < K) {  // K4A (qg_anchor.cu)
+    const int E = qg::anchored_exponent(pl.p, pl.t, pl.e, kb);
+    const int sh = pl.t * pl.d - (E - 52);
+    a.anchored_kb = (int)kb;
+    a.anch_shift = sh;
+    a.anchor = std::ldexp(1.5, E) + std::ldexp(1.0, pl.t * pl.d - 1) + std::ldexp(1.0, pl.t * pl.d + pl.t - 1);
+    a.anchor_delta = std::ldexp(1.0, pl.t * pl.d + pl.t);  // Q^(d+1): above the digit field
+    const uint64_t nex = ceil_div(K, (size_t)kb) + 3;  // extractions per output (<= 2 zero blocks + the final one)
+    if (((unsigned __int128)nex * a.qmask << sh) + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+    return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));
+  }
   if (pl.t <= 16) a.pack_period = (int)((65535u - (pl.p - 1)) / a.qmask);
   const uint64_t nblocks = (kbs ? ceil_div(K, (size_t)kbs * bk) : 1) + 1;
   if ((unsigned __int128)nblocks * a.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;

@@ -1215,6 +1215,14 @@ static cudaError_t launch_tiled_b(const GemmArgs& a, int flush, cudaStream_t s) 
 
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
+  if (a.anchored_kb > 0) {  // K4A (qg_anchor.cu)
+    int* counter = nullptr;
+    if (dynamic_tiles()) {
+      counter = tile_counter(s);
+      if (!counter) return cudaErrorMemoryAllocation;
+    }
+    return launch_dot_anchor(a, a.anchored_kb, counter, s, variant);
+  }
   static thread_local char name[80];
   // k-block flush placement for one-stage blocks: 3 = split phases (default:
   // odd accumulator rows mid-stage, even rows at stage ends), 0 = stage ends,

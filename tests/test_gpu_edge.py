@@ -76,16 +76,25 @@ def route(monkeypatch, request):
 
 
 @pytest.mark.parametrize("route", ["0", "1"], indirect=True, ids=["main128", "small64"])
+@pytest.mark.parametrize("anchored", [True, False], ids=["anchored", "fp64flush"])
 @pytest.mark.parametrize("name,p,k", COMMON, ids=[c[0] for c in COMMON])
-def test_worst_case_common(qg, cuda, route, name, p, k):
-    """The benched plan (plan_gpu, balanced digits) on +-h operands: all
+def test_worst_case_common(qg, cuda, route, name, p, k, anchored):
+    """The benched plan (plan_gpu, balanced digits; anchored accumulation K4A
+    where the planner picks it, and the FP64-add flush K4) on +-h operands: all
     sign combinations, slot-skewed operands, at the plan's own block."""
     import torch
 
-    gp = qg.plan_gpu(p, k)
+    gp = qg.plan_gpu(p, k, anchored=anchored)
     pl = gp.plan
     K = -(-k // pl.e)
-    if gp.kblock_words < K:  # blocked: the block uses >= 90 % of Eq. G's maximum
+    if gp.kblock_words < K and gp.anchored:
+        # anchored blocks (DESIGN.md §3g): the largest odd multiple of 4 words the anchored bound
+        # (and Eq. 3) allow
+        amax, _ = qg.max_exact_block_anchored(pl)
+        lim = min(amax, gp.eq3_kmax() // pl.e, 52)
+        assert gp.kblock_words <= lim and gp.kblock_words % 8 == 4
+        assert gp.kblock_words + 8 > lim, (gp.kblock_words, lim)
+    elif gp.kblock_words < K:  # blocked: the block uses >= 90 % of Eq. G's maximum
         assert gp.kblock_words <= gp.max_exact_words
         assert gp.kblock_words >= 0.9 * gp.max_exact_words, (gp.kblock_words, gp.max_exact_words)
     m = n = 256
@@ -107,7 +116,7 @@ def test_block_past_eq_g_refused(qg, cuda, p, k, balanced):
     (PlanMismatch). The maximum itself is accepted by the checks."""
     import torch
 
-    gp = qg.plan_gpu(p, k, balanced=balanced)
+    gp = qg.plan_gpu(p, k, balanced=balanced, anchored=False)
     pl = gp.plan
     K = -(-k // pl.e)
     if gp.max_exact_words >= K:

@@ -9,7 +9,7 @@ bld=/tmp/qg_var_$name
 mkdir -p "$out" "$bld"
 flags="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr $*"
 objs=""
-for f in qg_abi.cu qg_dot.cu qg_small.cu qg_pack.cu qg_word64.cu; do
+for f in qg_abi.cu qg_dot.cu qg_small.cu qg_anchor.cu qg_pack.cu qg_word64.cu; do
   nvcc $flags -c -o $bld/$f.o $here/paper_0803_1975_b200/csrc/$f &
   objs="$objs $bld/$f.o"
 done

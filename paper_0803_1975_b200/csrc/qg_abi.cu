@@ -631,7 +631,7 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
     a.anchored_kb = (int)kb;
     a.anch_shift = sh;
     a.anchor = std::ldexp(1.5, E) + std::ldexp(1.0, pl.t * pl.d - 1) + std::ldexp(1.0, pl.t * pl.d + pl.t - 1);
-    a.anchor_delta = std::ldexp(1.0, pl.t * pl.d + pl.t);  // Q^(d+1): above the digit field
+    a.anchor1 = a.anchor + std::ldexp(1.0, pl.t * pl.d + pl.t);  // second anchor: + Q^(d+1), above the digit field
     const uint64_t nex = ceil_div(K, (size_t)kb) + 3;  // extractions per output (<= 2 zero blocks + the final one)
     if (((unsigned __int128)nex * a.qmask << sh) + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
     return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));

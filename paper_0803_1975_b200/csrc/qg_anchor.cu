@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_anchor(GemmArgs args, int 
   // invisible to the digit field; two DISTINCT values keep ptxas from rebuilding the pair in the
   // accumulator's registers (4 MOVs) before every such DMMA.
   const double anchor = args.anchor;
-  const double anchor1 = args.anchor + args.anchor_delta;
+  const double anchor1 = args.anchor1;
   const uint32_t amask = args.qmask << args.anch_shift;
   const int sh = args.anch_shift;
   double acc[MI][NI][2];

@@ -74,13 +74,14 @@ struct GemmArgs {
   int* tile_counter;    // tiled kernels: dynamic tile schedule from this zeroed counter (NULL = static)
   int anchored_kb;      // K4A (qg_anchor.cu): k-block words of the anchored contraction, 0 = K4
   int anch_shift;       // K4A: digit d sits at bits [anch_shift, anch_shift + t) of an accumulator's low word
-  double anchor_delta;  // K4A: the odd output columns start from anchor + anchor_delta (a multiple of Q^(d+1),
-                        // invisible to the digit field): two distinct values keep the C operand a fixed register quad
+  double anchor1;  // K4A: the odd output columns start from this second anchor = anchor + Q^(d+1) (the
+                        // difference is invisible to the digit field): two distinct values keep the C operand
+                        // of the restart DMMAs a fixed register quad
 };
 cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
 // K4A: anchored accumulators, integer-pipe block flush (balanced plans; a.anchor = A0,
-// a.anchor_delta, a.anch_shift, a.anchored_kb set; the tiled layout's stage depth is kb_words).
+// a.anchor1, a.anch_shift, a.anchored_kb set; the tiled layout's stage depth is kb_words).
 cudaError_t launch_dot_anchor(const GemmArgs& a, int kb_words, int* tile_counter, cudaStream_t s,
                               const char** variant);
 bool anchor_supported(int kb_words);

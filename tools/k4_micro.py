@@ -17,6 +17,10 @@ ap.add_argument("--k", type=int, default=32768)
 ap.add_argument("--kblock", type=int, default=0)
 ap.add_argument("--anchored", type=int, default=-1)
 ap.add_argument("--waves", type=int, default=8)
+ap.add_argument("--t", type=int, default=0, help="force the plan's (t, e) (with --e)")
+ap.add_argument("--e", type=int, default=0)
+ap.add_argument("--m", type=int, default=0, help="explicit shape instead of whole waves")
+ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--peak", type=float, default=37.09)
 args = ap.parse_args()
@@ -26,7 +30,11 @@ p, k = args.p, args.k
 tiles_n = 32
 tiles_m = sms * args.waves // tiles_n
 m, n = tiles_m * 128, tiles_n * 128
+if args.m:
+    m, n = args.m, args.n or args.m
 gp = qg.plan_gpu(p, k)
+if args.t:
+    gp = qg.GpuPlan(qg.make_plan(p, args.t, args.e), gp.kblock_words, 0, 1, 0)
 if args.kblock or args.anchored >= 0:
     gp = qg.GpuPlan(gp.plan, args.kblock or gp.kblock_words, gp.max_exact_words, gp.balanced,
                     gp.anchored if args.anchored < 0 else args.anchored)

@@ -593,9 +593,7 @@ def our_arm(args):
             dist.init_process_group(args.dist_backend)
 
     p, m, k, n, desc = CONFIGS[args.config]
-    # --output cc runs K4R (ReduceAndCompress epilogue), which has no anchored variant yet
-    gp = (qg.plan_gpu(p, k, anchored=args.output != "cc") if args.plan == "gpu"
-          else qg.gpu_plan_from(qg.plan_compression(p, k), k))
+    gp = qg.plan_gpu(p, k) if args.plan == "gpu" else qg.gpu_plan_from(qg.plan_compression(p, k), k)
     if args.kblock:  # experiments: override the k-block of the chosen plan
         gp = qg.GpuPlan(gp.plan, args.kblock, gp.max_exact_words, gp.balanced,
                         gp.anchored if args.anchored < 0 else args.anchored)

@@ -555,6 +555,22 @@ void small_geometry(size_t m, size_t n, size_t Kt, int kbs, int* splits, int* sp
 
 extern "C" {
 
+// K4A (qg_anchor.cu): anchor pair, digit position and block length of an anchored
+// plan's contraction; the block was validated by tiled_geometry. The digit sums (scaled by 2^shift)
+// of all extractions must fit the kernel's uint32 accumulators.
+static int set_anchored_args(const qg_plan& pl, size_t K, uint64_t kb, qgk::GemmArgs* a) {
+  const int E = qg::anchored_exponent(pl.p, pl.t, pl.e, kb);
+  if (!E) return QG_NOT_EXACT;
+  const int sh = pl.t * pl.d - (E - 52);
+  a->anchored_kb = (int)kb;
+  a->anch_shift = sh;
+  a->anchor = std::ldexp(1.5, E) + std::ldexp(1.0, pl.t * pl.d - 1) + std::ldexp(1.0, pl.t * pl.d + pl.t - 1);
+  a->anchor1 = a->anchor + std::ldexp(1.0, pl.t * pl.d + pl.t);  // second anchor: + Q^(d+1), above the digit field
+  const uint64_t nex = ceil_div(K, (size_t)kb) + 3;  // extractions per output (<= 2 zero blocks + the final one)
+  if (((unsigned __int128)nex * a->qmask << sh) + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+  return QG_OK;
+}
+
 int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const double* cb_t, size_t m, size_t n,
                         size_t k, int32_t* c, size_t ldc, void* stream) {
   if (!gplan) return QG_INVALID_ARGUMENT;
@@ -626,14 +642,7 @@ int qg_mul_common_tiled(const qg_gpu_plan* gplan, const double* ca_t, const doub
   // digit sums are uint32 (planner keeps nblocks * (Q-1) < 2^32); the fused
   // flush packs two per register as 16-bit lanes, reduced mod p in time
   if (gplan->anchored && a.balanced && kb < K) {  // K4A (qg_anchor.cu)
-    const int E = qg::anchored_exponent(pl.p, pl.t, pl.e, kb);
-    const int sh = pl.t * pl.d - (E - 52);
-    a.anchored_kb = (int)kb;
-    a.anch_shift = sh;
-    a.anchor = std::ldexp(1.5, E) + std::ldexp(1.0, pl.t * pl.d - 1) + std::ldexp(1.0, pl.t * pl.d + pl.t - 1);
-    a.anchor1 = a.anchor + std::ldexp(1.0, pl.t * pl.d + pl.t);  // second anchor: + Q^(d+1), above the digit field
-    const uint64_t nex = ceil_div(K, (size_t)kb) + 3;  // extractions per output (<= 2 zero blocks + the final one)
-    if (((unsigned __int128)nex * a.qmask << sh) + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+    if ((st = set_anchored_args(pl, K, kb, &a))) return st;
     return cuda_status(qgk::launch_dot_tiled(a, bk, as_stream(stream), &g_last_kernel));
   }
   if (pl.t <= 16) a.pack_period = (int)((65535u - (pl.p - 1)) / a.qmask);
@@ -692,8 +701,12 @@ int qg_mul_common_repacked_tiled(const qg_gpu_plan* gplan, const double* ca_t, c
   a.e = pl.e;
   a.cc = cc;
   a.ldcc = ldcc;
-  const uint64_t nblocks = (kbs ? ceil_div(K, (size_t)kbs * bk) : 1) + 1;
-  if ((unsigned __int128)nblocks * a.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+  if (gplan->anchored && a.balanced && kb < K) {  // K4A with the ReduceAndCompress epilogue
+    if ((st = set_anchored_args(pl, K, kb, &a))) return st;
+  } else {
+    const uint64_t nblocks = (kbs ? ceil_div(K, (size_t)kbs * bk) : 1) + 1;
+    if ((unsigned __int128)nblocks * a.qmask + 2 * pl.p >= ((unsigned __int128)1 << 32)) return QG_NOT_EXACT;
+  }
   // words cut by a 32-column warp segment are summed atomically from zero
   if (32 % pl.e) QG_TRY(cudaMemset2DAsync(cc, ldcc * 8, 0, H * 8, m, s));
   return cuda_status(qgk::launch_dot_tiled_repack(a, bk, s, &g_last_kernel));

@@ -132,10 +132,12 @@ __device__ double g_zero_blocks[2 * BM * 20];  // >= 2 * 128 * 12 (BK 12, SS 3) 
 // one full/empty barrier round; short blocks (BK = 12) then pay their barrier and producer overhead
 // once per SS blocks. A tile's last slot is filled up with zero blocks (exact no-ops that only add
 // extractions of the bias, counted in corr), so the consumers have no tail code.
-template <int BK, int SS>
+constexpr int REPACK_SMEM = BM * BN;  // REPACK: one byte per residue (p < 256), one 64 x 32 tile per warp
+
+template <int BK, int SS, bool REPACK>
 __global__ void __launch_bounds__(NT + 128, 1) k_gemm_anchor(GemmArgs args, int tiles_m, int tiles_n) {
   constexpr int SLOT = 2 * SS * BM * BK;  // doubles per slot: SS blocks of A, then SS blocks of B
-  constexpr int BUDGET = 232448 - 1024;
+  constexpr int BUDGET = 232448 - 1024 - (REPACK ? REPACK_SMEM : 0);
   constexpr int S_RAW = BUDGET / (SLOT * 8);
   constexpr int S = S_RAW > 8 ? 8 : S_RAW;
   static_assert(S >= 2, "at least two slots");
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_anchor(GemmArgs args, int 
   const int total_tiles = tiles_m * tiles_n;
   const int my_tiles = blockIdx.x < total_tiles ? (total_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   volatile int* tile_of = reinterpret_cast<volatile int*>(empty + S);
+  uint8_t* repack = reinterpret_cast<uint8_t*>(empty + S + 4);  // REPACK staging (after barriers + tile_of)
   const bool dyn = args.tile_counter != nullptr;
 
   if (warp >= NWARPS) {
@@ -255,6 +258,29 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_anchor(GemmArgs args, int 
       }
     }
     // epilogue: last block's digit + digit sums (scaled by 2^sh), biases removed mod p
+    if (REPACK) {  // mul_common_repacked: residues -> this warp's byte tile -> forward-packed words
+      uint8_t* st = repack + warp * (WM * WN);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          uint32_t r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t x =
+                ((((uint32_t)__double2loint(acc[mi][ni][h]) & amask) + ds[mi][ni][h]) >> sh) + args.corr;
+            const uint32_t r0 = x - __umulhi(x, modp.magic) * modp.p;
+            r[h] = min(r0, r0 - modp.p);
+            acc[mi][ni][h] = h ? anchor1 : anchor;
+            ds[mi][ni][h] = 0u;
+          }
+          *reinterpret_cast<uint16_t*>(st + (mi * 8 + g) * WN + ni * 8 + 2 * t) = (uint16_t)(r[0] | (r[1] << 8));
+        }
+      __syncwarp();
+      repack_warp_segment(st, args.cc, args.ldcc, M, N, args.e, args.t, m0 + warp_m * WM, n0 + warp_n * WN, lane);
+      __syncwarp();  // the next tile overwrites the staging tile
+      continue;
+    }
     const bool fast = !args.accumulate && m0 + BM <= M && n0 + BN <= N;
     if (fast) {
       int32_t* cbase = args.c + (size_t)(m0 + warp_m * WM + g) * args.ldc + n0 + warp_n * WN + 2 * t;
@@ -318,13 +344,13 @@ int num_sms_a() {
   return sms;
 }
 
-template <int BK, int SS>
+template <int BK, int SS, bool REPACK>
 cudaError_t launch_anchor_one(const GemmArgs& a, int* tile_counter, cudaStream_t s) {
-  auto k = k_gemm_anchor<BK, SS>;
+  auto k = k_gemm_anchor<BK, SS, REPACK>;
   constexpr int SLOT = 2 * SS * BM * BK;
-  constexpr int S_RAW = (232448 - 1024) / (SLOT * 8);
+  constexpr int S_RAW = (232448 - 1024 - (REPACK ? REPACK_SMEM : 0)) / (SLOT * 8);
   constexpr int S = S_RAW > 8 ? 8 : S_RAW;
-  const size_t smem = size_t(S) * SLOT * sizeof(double) + (2 * S + 4) * sizeof(uint64_t);
+  const size_t smem = size_t(S) * SLOT * sizeof(double) + (2 * S + 4) * sizeof(uint64_t) + (REPACK ? REPACK_SMEM : 0);
   cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err) return err;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
@@ -346,30 +372,28 @@ cudaError_t launch_anchor_one(const GemmArgs& a, int* tile_counter, cudaStream_t
   return cudaGetLastError();
 }
 
-}  // namespace
-
-bool anchor_supported(int kb_words) {
-  switch (kb_words) {
-    case 12: case 20: case 28: case 36: case 44: case 52: return true;
-  }
-  return false;
-}
-
 // kb_words: the block length = the stage depth of the tiled layout (a.K words per row, blocks of
 // kb_words). Extractions per output, for the caller's uint32 digit-sum check: <= ceil(K / kb_words) + 3.
+template <int BK, int SS>
+cudaError_t launch_anchor_bk(const GemmArgs& a, int* tile_counter, cudaStream_t s, bool repack) {
+  return repack ? launch_anchor_one<BK, SS, true>(a, tile_counter, s) : launch_anchor_one<BK, SS, false>(a, tile_counter, s);
+}
+
+}  // namespace
+
 cudaError_t launch_dot_anchor(const GemmArgs& a, int kb_words, int* tile_counter, cudaStream_t s,
-                              const char** variant) {
+                              const char** variant, bool repack) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
   static thread_local char name[80];
-  snprintf(name, sizeof name, "dot_tiled_anchor_kb%d_balanced", kb_words);
+  snprintf(name, sizeof name, "dot_tiled_%sanchor_kb%d_balanced", repack ? "repack_" : "", kb_words);
   *variant = name;
   switch (kb_words) {
-    case 12: return launch_anchor_one<12, 3>(a, tile_counter, s);
-    case 20: return launch_anchor_one<20, 2>(a, tile_counter, s);
-    case 28: return launch_anchor_one<28, 1>(a, tile_counter, s);
-    case 36: return launch_anchor_one<36, 1>(a, tile_counter, s);
-    case 44: return launch_anchor_one<44, 1>(a, tile_counter, s);
-    case 52: return launch_anchor_one<52, 1>(a, tile_counter, s);
+    case 12: return launch_anchor_bk<12, 3>(a, tile_counter, s, repack);
+    case 20: return launch_anchor_bk<20, 2>(a, tile_counter, s, repack);
+    case 28: return launch_anchor_bk<28, 1>(a, tile_counter, s, repack);
+    case 36: return launch_anchor_bk<36, 1>(a, tile_counter, s, repack);
+    case 44: return launch_anchor_bk<44, 1>(a, tile_counter, s, repack);
+    case 52: return launch_anchor_bk<52, 1>(a, tile_counter, s, repack);
   }
   return cudaErrorInvalidValue;
 }

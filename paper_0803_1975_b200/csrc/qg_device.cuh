@@ -49,4 +49,32 @@ struct ModP {
   }
 };
 
+// ReduceAndCompress of one warp's 64 x 32 residue tile (st, row-major, 32
+// bytes per row; rows r0.., columns c0.. of the M x N product): word h of a
+// row packs columns h e .. h e + e - 1 forward in base Q = 2^t
+// (compress_forward, pack.hpp:47-54; reduce_and_compress, pack.hpp:141-155).
+// Words whose columns all lie in this segment are stored; a word cut by the
+// segment's edge gets its part added atomically (the parts occupy disjoint
+// bits, so the float64 sums are exact integers < 2^53 in any order; the
+// launcher zeroes CC first whenever a word can straddle segments).
+__device__ __forceinline__ void repack_warp_segment(const uint8_t* st, double* cc, size_t ldcc, int M, int N, int e,
+                                                    int tb, int r0, int c0, int lane) {
+  constexpr int SEG_ROWS = 64, SEG_COLS = 32;
+  if (c0 >= N) return;
+  const int cend = min(c0 + SEG_COLS, N);
+  const int h_lo = c0 / e, h_hi = (cend - 1) / e, W = h_hi - h_lo + 1;
+  const int rows = min(SEG_ROWS, M - r0);
+  for (int idx = lane; idx < rows * W; idx += 32) {
+    const int row = idx / W, hw = h_lo + (idx - row * W);
+    const int wc0 = hw * e;
+    const int lo = max(wc0, c0), hi = min(wc0 + e, cend);
+    uint64_t word = 0;
+    for (int c = lo; c < hi; ++c) word |= (uint64_t)st[row * SEG_COLS + (c - c0)] << (tb * (c - wc0));
+    double* dst = cc + (size_t)(r0 + row) * ldcc + hw;
+    const double wd = __ull2double_rn(word);  // exact: word < Q^e <= 2^53
+    if (wc0 >= c0 && min(wc0 + e, N) <= cend) *dst = wd;
+    else atomicAdd(dst, wd);
+  }
+}
+
 }  // namespace qgk

@@ -195,30 +195,10 @@ constexpr int REPACK_SMEM = BM * BN;
 template <int EPI>
 constexpr int epi_reserve() { return EPI == EPI_REPACK ? REPACK_SMEM : 0; }
 
-// ReduceAndCompress of one warp's 64 x 32 residue tile (st, row-major, WN
-// bytes per row; rows r0.., columns c0..): word h of a row packs columns
-// h e .. h e + e - 1 forward in base Q = 2^t (compress_forward, pack.hpp:47-54).
-// Words whose columns all lie in this segment are stored; a word cut by the
-// segment's edge gets its part added atomically (the parts occupy disjoint
-// bits, so the float64 sums are exact integers < 2^53 in any order; the
-// launcher zeroes CC first whenever a word can straddle segments).
+// ReduceAndCompress of one warp's residue tile: repack_warp_segment (qg_device.cuh).
 __device__ __forceinline__ void repack_segment(const uint8_t* st, const GemmArgs& a, int r0, int c0, int lane) {
-  const int N = a.N, e = a.e, tb = a.t;
-  if (c0 >= N) return;
-  const int cend = min(c0 + WN, N);
-  const int h_lo = c0 / e, h_hi = (cend - 1) / e, W = h_hi - h_lo + 1;
-  const int rows = min(WM, a.M - r0);
-  for (int idx = lane; idx < rows * W; idx += 32) {
-    const int row = idx / W, hw = h_lo + (idx - row * W);
-    const int wc0 = hw * e;
-    const int lo = max(wc0, c0), hi = min(wc0 + e, cend);
-    uint64_t word = 0;
-    for (int c = lo; c < hi; ++c) word |= (uint64_t)st[row * WN + (c - c0)] << (tb * (c - wc0));
-    double* dst = a.cc + (size_t)(r0 + row) * a.ldcc + hw;
-    const double wd = __ull2double_rn(word);  // exact: word < Q^e <= 2^53
-    if (wc0 >= c0 && min(wc0 + e, N) <= cend) *dst = wd;
-    else atomicAdd(dst, wd);
-  }
+  static_assert(WM == 64 && WN == 32, "repack_warp_segment's tile");
+  repack_warp_segment(st, a.cc, a.ldcc, a.M, a.N, a.e, a.t, r0, c0, lane);
 }
 
 // redq, pack.hpp:124-137, on an exact integer-valued word w < 2^53: every
@@ -1262,6 +1242,14 @@ static cudaError_t launch_tiled_repack_b(const GemmArgs& a, int flush, cudaStrea
 
 cudaError_t launch_dot_tiled_repack(const GemmArgs& a, int bk, cudaStream_t s, const char** variant) {
   if (a.M == 0 || a.N == 0) return cudaSuccess;
+  if (a.anchored_kb > 0) {  // K4A with the ReduceAndCompress epilogue (qg_anchor.cu)
+    int* counter = nullptr;
+    if (dynamic_tiles()) {
+      counter = tile_counter(s);
+      if (!counter) return cudaErrorMemoryAllocation;
+    }
+    return launch_dot_anchor(a, a.anchored_kb, counter, s, variant, true);
+  }
   static thread_local char name[80];
   const char* e = getenv("QG_FLUSH");
   const int flush = e ? (atoi(e) == 3 ? 3 : 0) : 3;

@@ -82,9 +82,10 @@ cudaError_t launch_dot_dmma(const GemmArgs& a, int bk, cudaStream_t s, const cha
 cudaError_t launch_right_dmma(const GemmArgs& a, bool redq, cudaStream_t s, const char** variant);
 // K4A: anchored accumulators, integer-pipe block flush (balanced plans; a.anchor = A0,
 // a.anchor1, a.anch_shift, a.anchored_kb set; the tiled layout's stage depth is kb_words).
+// repack: ReduceAndCompress fused into the epilogue (CC words in a.cc / a.ldcc packed under a.t, a.e; p < 256;
+// the caller zeroes CC first unless a.e divides 32), else int32 C.
 cudaError_t launch_dot_anchor(const GemmArgs& a, int kb_words, int* tile_counter, cudaStream_t s,
-                              const char** variant);
-bool anchor_supported(int kb_words);
+                              const char** variant, bool repack = false);
 // Same contraction on the tiled layout (a = CA_t, b = CB_t; lda/ldb unused).
 cudaError_t launch_dot_tiled(const GemmArgs& a, int bk, cudaStream_t s, const char** variant);
 // Tiled kernels: claim tiles dynamically from an atomic counter (on) or

@@ -90,9 +90,33 @@ def test_anchored_plan_past_bound_refused(qg, cuda):
     torch.cuda.synchronize()
 
 
-def test_anchored_repack_and_small_entries_accept_the_plan(qg, orc, cuda, monkeypatch):
-    """Entries without an anchored kernel (the fused ReduceAndCompress epilogue, the small-product
-    kernel) run an anchored plan's blocks with the FP64 flush: same C."""
+@pytest.mark.parametrize("p,k,m,n", [(3, 9000, 200, 260), (7, 4096, 1000, 1030), (5, 20000, 384, 514), (3, 32768, 256, 96)])
+def test_anchored_repack(qg, orc, cuda, monkeypatch, p, k, m, n):
+    """mul_common_repacked (gemm.hpp:275-280) under an anchored plan: K4A with the fused
+    ReduceAndCompress epilogue; CC's words decode to naive_gemm's C and equal the FP64-flush
+    kernel's words bit for bit (ragged shapes, e that does not divide 32)."""
+    import torch
+
+    monkeypatch.setenv("QG_SMALL", "0")
+    a = orc.random_residue_matrix(m, k, p, 31)
+    b = orc.random_residue_matrix(k, n, p, 32)
+    want = orc.naive_gemm(p, a, b)
+    ga = qg.plan_gpu(p, k)
+    assert ga.anchored
+    gf = qg.GpuPlan(ga.plan, ga.kblock_words, ga.max_exact_words, 1, 0)  # the same blocks, FP64 flush (K4R)
+    ad = torch.from_numpy(a.astype(np.float64)).to(cuda)
+    bd = torch.from_numpy(b.astype(np.float64)).to(cuda)
+    cr = qg.mul_common_repacked(ad, bd, ga)
+    assert "repack_anchor" in qg.last_kernel(), qg.last_kernel()
+    assert np.array_equal(qg.uncompress(cr).cpu().numpy().astype(np.uint32), want)
+    cf = qg.mul_common_repacked(ad, bd, gf)
+    assert "anchor" not in qg.last_kernel()
+    assert torch.equal(cr.data, cf.data)
+
+
+def test_anchored_small_entry_accepts_the_plan(qg, orc, cuda, monkeypatch):
+    """The small-product kernel (no anchored variant) runs an anchored plan's blocks with the FP64
+    flush: same C."""
     import torch
 
     p, m, k, n = 3, 200, 9000, 260
@@ -103,8 +127,6 @@ def test_anchored_repack_and_small_entries_accept_the_plan(qg, orc, cuda, monkey
     assert gp.anchored
     ad = torch.from_numpy(a.astype(np.float64)).to(cuda)
     bd = torch.from_numpy(b.astype(np.float64)).to(cuda)
-    cr = qg.mul_common_repacked(ad, bd, gp)
-    assert np.array_equal(qg.uncompress(cr).cpu().numpy().astype(np.uint32), want)
     monkeypatch.setenv("QG_SMALL", "1")
     cs = qg.mul_common_compressed(ad, bd, gp).cpu().numpy().astype(np.uint32)
     assert "anchor" not in qg.last_kernel()

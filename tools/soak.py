@@ -53,7 +53,7 @@ def main():
         want = orc.naive_gemm(p, a, b)
         kind = rng.choice(["device", "host", "right", "left", "multi", "repack", "repack_host", "allgather"])
         try:
-            gp = qg.plan_gpu(p, k, balanced=rng.random() < 0.6)
+            gp = qg.plan_gpu(p, k, balanced=rng.random() < 0.6, anchored=rng.random() < 0.7)
         except qg.Error:
             continue
         desc = f"kind={kind} p={p} m={m} k={k} n={n} plan={gp}"

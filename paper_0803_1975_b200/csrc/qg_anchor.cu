@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(NT + 128, 1) k_gemm_anchor(GemmArgs args, int 
     }
   const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
   uint32_t slot = 0, phase = 0;
-  if (warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise the SMSP's two warps
+  if (warp >= 4 && args.skew_ns > 0) start_skew(args.skew_ns);  // desynchronise the SMSP's two warps
   const int a_off = (warp_m * WM + g) * BK + t;                // fragment bases inside an operand block
   const int b_off = SS * BM * BK + (warp_n * WN + g) * BK + t;
   for (int ts = 0;; ++ts) {
@@ -358,7 +358,9 @@ cudaError_t launch_anchor_one(const GemmArgs& a, int* tile_counter, cudaStream_t
   const int grid = tiles < num_sms_a() ? tiles : num_sms_a();
   GemmArgs a2 = a;
   const char* skew = getenv("QG_SKEW_NS");
-  a2.skew_ns = skew ? (unsigned)atoi(skew) : 4000u;
+  a2.skew_ns = skew ? (unsigned)atoi(skew) : 3000u;
+  if (const char* sl = getenv("QG_SKEW_SLEEP"))
+    if (sl[0] == '1' && a2.skew_ns) a2.skew_ns |= 0x80000000u;  // experiments: nanosleep instead of the clock spin
   const char* grp = getenv("QG_GROUP");
   a2.group = grp ? atoi(grp) : 8;
   a2.tile_counter = tile_counter;

@@ -49,6 +49,21 @@ struct ModP {
   }
 };
 
+// Start delay of the second warp of every SMSP (warps 4..7), so that the two warps sharing a DMMA
+// pipe run their k-block flushes / tile epilogues half a phase apart. A clock spin: __nanosleep(t)
+// sleeps anywhere in [0, 2t], which made the one-stage-per-tile products (config 3) bimodal across
+// runs. Bit 31 of skew_ns (QG_SKEW_SLEEP=1, experiments) selects the old nanosleep.
+__device__ __forceinline__ void start_skew(unsigned skew_ns) {
+  if (skew_ns & 0x80000000u) {
+    __nanosleep(skew_ns & 0x7fffffffu);
+    return;
+  }
+  const long long t0 = clock64();
+  const long long cycles = 2ll * skew_ns;  // ~2 SM cycles per ns (1.965 GHz)
+  while (clock64() - t0 < cycles) {
+  }
+}
+
 // ReduceAndCompress of one warp's 64 x 32 residue tile (st, row-major, 32
 // bytes per row; rows r0.., columns c0.. of the M x N product): word h of a
 // row packs columns h e .. h e + e - 1 forward in base Q = 2^t

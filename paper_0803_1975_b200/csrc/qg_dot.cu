@@ -544,7 +544,7 @@ __device__ __forceinline__ void consume(const GemmArgs& args, double* smem, uint
   const ModP modp{args.p, (uint32_t)(0x100000000ull / args.p)};
   uint32_t slot = 0, phase = 0;
   int nflush = 0;
-  if (warp >= 4 && args.skew_ns > 0) __nanosleep(args.skew_ns);  // desynchronise SMSP warp pairs
+  if (warp >= 4 && args.skew_ns > 0) start_skew(args.skew_ns);  // desynchronise SMSP warp pairs
   // dynamic schedule (tile_of != nullptr): the producer claims tiles from a
   // global counter and posts each tile's index beside its first stage; a
   // negative index ends the loop
@@ -1082,7 +1082,7 @@ static cudaError_t launch_bulk(const GemmArgs& a, cudaStream_t s) {
   GemmArgs a2 = a;
   const char* dbg = getenv("QG_DEBUG_MODE");
   a2.debug = dbg ? atoi(dbg) : 0;
-  // warps 4..7 start 4 us late so the two warps of an SMSP do not flush their
+  // warps 4..7 start 3 us late (a clock spin) so the two warps of an SMSP do not flush their
   // k-blocks at the same moment (+3% on config 2, profiles/r01_notes.md)
   const char* skew = getenv("QG_SKEW_NS");
   a2.skew_ns = skew ? (unsigned)atoi(skew) : (a.kb_stages ? 4000u : 0u);
@@ -1154,11 +1154,13 @@ static cudaError_t launch_tiled_one(const GemmArgs& a, cudaStream_t s) {
   GemmArgs a2 = a;
   const char* dbg = getenv("QG_DEBUG_MODE");
   a2.debug = dbg ? atoi(dbg) : 0;
-  // warps 4..7 start 4 us late so the two warps of an SMSP do not flush their
+  // warps 4..7 start 3 us late (a clock spin) so the two warps of an SMSP do not flush their
   // k-blocks (or run their tile epilogues) at the same moment: config 2
   // +3 %, config 3 75.6 -> 78.9 % (profiles/r01_notes.md)
   const char* skew = getenv("QG_SKEW_NS");
-  a2.skew_ns = skew ? (unsigned)atoi(skew) : 4000u;
+  a2.skew_ns = skew ? (unsigned)atoi(skew) : 3000u;
+  if (const char* sl = getenv("QG_SKEW_SLEEP"))
+    if (sl[0] == '1' && a2.skew_ns) a2.skew_ns |= 0x80000000u;  // experiments: nanosleep instead of the clock spin
   const char* grp = getenv("QG_GROUP");  // experiments: tile-row group of the raster
   a2.group = grp ? atoi(grp) : 8;
   a2.tile_counter = nullptr;

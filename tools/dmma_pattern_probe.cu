@@ -60,25 +60,25 @@ __global__ void __launch_bounds__(256, 1) probe(double* out, int ksteps) {
 }
 
 template <int MODE, int MI, int NI, int DATA = 0>
-void run(const char* name, int sms) {
+void run(const char* name, int sms, int threads = 256) {
   double* out;
   cudaMalloc(&out, 8);
   const int ksteps = 8192;
   const int smem = (128 * 36 + 32 * 132) * 8;
   cudaFuncSetAttribute(probe<MODE, MI, NI, DATA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<MODE, MI, NI, DATA><<<sms, 256, smem>>>(out, 64);
+  probe<MODE, MI, NI, DATA><<<sms, threads, smem>>>(out, 64);
   cudaDeviceSynchronize();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  probe<MODE, MI, NI, DATA><<<sms, 256, smem>>>(out, ksteps);
+  probe<MODE, MI, NI, DATA><<<sms, threads, smem>>>(out, ksteps);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  const double flop = 2.0 * 256 * sms * 8.0 * ksteps * MI * NI;  // 8 warps x 256 FMA x MI*NI per k-step
-  printf("{\"data\": %d, \"probe\": \"%s\", \"mi\": %d, \"ni\": %d, \"tflops\": %.3f, \"ms\": %.3f, \"err\": \"%s\"}\n", DATA, name, MI, NI,
+  const double flop = 2.0 * 256 * sms * (threads / 32.0) * ksteps * MI * NI;  // 8 warps x 256 FMA x MI*NI per k-step
+  printf("{\"threads\": %d, \"data\": %d, \"probe\": \"%s\", \"mi\": %d, \"ni\": %d, \"tflops\": %.3f, \"ms\": %.3f, \"err\": \"%s\"}\n", threads, DATA, name, MI, NI,
          flop / ms / 1e9, ms, cudaGetErrorString(cudaGetLastError()));
   cudaFree(out);
 }
@@ -92,6 +92,9 @@ int main() {
   run<2, 8, 4, 1>("regs", sms);
   run<3, 8, 4, 1>("lds", sms);
   run<4, 8, 4, 1>("lds_sync", sms);
+  run<2, 8, 4>("regs", sms, 128);
+  run<3, 8, 4>("lds", sms, 128);
+  run<4, 8, 4>("lds_sync", sms, 128);
   run<2, 4, 4>("regs", sms);
   run<3, 4, 4>("lds", sms);
   run<4, 4, 4>("lds_sync", sms);

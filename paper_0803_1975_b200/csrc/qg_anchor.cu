@@ -124,7 +124,7 @@ __device__ __forceinline__ void anchored_block(double (&acc)[MI][NI][2], uint32_
 }
 
 // Zero operand blocks for the slots that reach past the end of K (SS > 1): (SS - 1) blocks at most.
-__device__ double g_zero_blocks[2 * BM * 20];  // >= 2 * 128 * 12 (BK 12, SS 3) and 1 * 128 * 20 (BK 20, SS 2)
+__device__ __align__(128) double g_zero_blocks[2 * BM * 20];  // >= 2 * 128 * 12 (BK 12, SS 3) and 1 * 128 * 20 (BK 20, SS 2)
 
 // BK: words per k-block = stage depth of the tiled layout (an odd multiple of 4, conflict-free
 // fragment loads). SS: blocks per pipeline slot ("super-stage"): consecutive blocks of one row panel

@@ -10,7 +10,10 @@
 //
 // Here the anchor is folded into the accumulation instead: the first DMMA of
 // every block takes C = anchor = 1.5*2^E + Q^d/2 + Q^d*Q/2 (a uniform register
-// pair; D overwrites the accumulator, so nothing is zeroed), every partial sum
+// quad {anchor, anchor + Q^(d+1)} — two distinct values, or ptxas rebuilds the
+// pair with four MOVs before every such DMMA; the difference is invisible to
+// the digit field; D overwrites the accumulator, so nothing is zeroed), every
+// partial sum
 // of the block stays inside the binade [2^E, 2^(E+1)) (planner:
 // qg::max_exact_block_anchored), so its ulp is u = 2^(E-52) throughout and the
 // block's digit d sits at FIXED bits [s, s+t) of the accumulator's low word,
@@ -94,7 +97,8 @@ __device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double 
 // (dense 128 x BK, B transposed). Split flush: accumulator row mi ends its blocks after k-step
 // (mi % KBS) - 1 of every block (shifted windows of exactly KBS k-steps — any partition of k into
 // pieces of <= the exact block is exact), so every k-step carries 1/KBS of the integer flush work.
-// At a block boundary the finished block's digit leaves the accumulator's low word (LOP3 + IADD) and
+// Measured (profiles/r02_notes.md): 92.9-93.4 % of the DMMA peak on config 5 (12-word blocks); the
+// same loop without restarts 98.8 %. At a block boundary the finished block's digit leaves the accumulator's low word (LOP3 + IADD) and
 // the DMMA restarts the accumulator from the anchor pair {c0, c1}.
 template <int BK>
 __device__ __forceinline__ void anchored_block(double (&acc)[MI][NI][2], uint32_t (&ds)[MI][NI][2],

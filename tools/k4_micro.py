@@ -19,6 +19,7 @@ ap.add_argument("--anchored", type=int, default=-1)
 ap.add_argument("--waves", type=int, default=8)
 ap.add_argument("--t", type=int, default=0, help="force the plan's (t, e) (with --e)")
 ap.add_argument("--e", type=int, default=0)
+ap.add_argument("--plain", type=int, default=0, help="1: plan_gpu(p, k, anchored=False), the best FP64-flush plan")
 ap.add_argument("--m", type=int, default=0, help="explicit shape instead of whole waves")
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=5)
@@ -32,10 +33,10 @@ tiles_m = sms * args.waves // tiles_n
 m, n = tiles_m * 128, tiles_n * 128
 if args.m:
     m, n = args.m, args.n or args.m
-gp = qg.plan_gpu(p, k)
+gp = qg.plan_gpu(p, k, anchored=not args.plain)
 if args.t:
     gp = qg.GpuPlan(qg.make_plan(p, args.t, args.e), gp.kblock_words, 0, 1, 0)
-if args.kblock or args.anchored >= 0:
+if (args.kblock or args.anchored >= 0) and not args.plain:
     gp = qg.GpuPlan(gp.plan, args.kblock or gp.kblock_words, gp.max_exact_words, gp.balanced,
                     gp.anchored if args.anchored < 0 else args.anchored)
 bk = qg.tiled_stage_words(gp, k)
